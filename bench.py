@@ -1,0 +1,414 @@
+#!/usr/bin/env python
+"""Benchmark of the Accel-GCN hot path on B200: plan (degree sort + block partition) and
+stacked SpMM propagation layers Y = A.X, row-sharded over N GPUs with an in-place NCCL
+all-gather between layers.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c5] [--impl agcn|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...
+
+One step = one pass of the whole hot path over one synthetic graph:
+agcn_plan (a1-a5) -> for each layer: agcn_spmm (a6-a8) [-> all-gather (a9)].
+Rank 0 prints ONE JSON line.  See DESIGN.md "Measurement" for the byte model.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "A·X SpMM GFLOP/s and HBM GB/s (% of ~8 TB/s) per graph at 1/2/4/8 B200"
+UNIT = "GFLOP/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["agcn", "reference"], default="agcn")
+    ap.add_argument("--config", default="c5", choices=["c1", "c2", "c3", "c4", "c5"])
+    ap.add_argument("--F", type=int, default=None)
+    ap.add_argument("--layers", type=int, default=None)
+    ap.add_argument("--partition", choices=["block", "warp"], default="block")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--cpu-seconds", type=float, default=15.0, help="CPU-oracle sample budget")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cusparse", action="store_true")
+    ap.add_argument("--profile", action="store_true",
+                    help="short run for ncu: no clocks/e2e/cpu/cusparse legs")
+    return ap.parse_args()
+
+
+# ---------------------------------------------------------------- helpers
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return {"hbm_gbs": float(d["hbm_gbs"]), "source": "measured (MEASURED_PEAKS.json)"}
+    return {"hbm_gbs": 6650.0, "source": "fallback (B200_PROFILING.md)"}
+
+
+def load_traffic(config: str, F: int):
+    """dram bytes per agcn_spmm launch from the committed ncu --set full summary, if any."""
+    for name in sorted(os.listdir(os.path.join(ROOT, "profiles")), reverse=True):
+        if name.startswith("ncu_traffic") and name.endswith(".json"):
+            d = json.load(open(os.path.join(ROOT, "profiles", name)))
+            key = f"{config}_F{F}"
+            if key in d:
+                return d[key], name
+    return None, None
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 200 ms during the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(index), f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "200"],
+                                      stdout=self.f, stderr=subprocess.DEVNULL)
+        except FileNotFoundError:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return None
+        time.sleep(0.25)
+        self.p.terminate()
+        try:
+            self.p.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.p.kill()
+        self.f.flush()
+        rows = []
+        for line in open(self.f.name):
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                rows.append((float(parts[1]), float(parts[2]), parts[5:9]))
+            except ValueError:
+                continue
+        os.unlink(self.f.name)
+        if not rows:
+            return None
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for _, _, r in rows for i, v in enumerate(r) if v == "Active"})
+        return {"sm_mhz": statistics.median(r[0] for r in rows), "sm_max_mhz": max(r[1] for r in rows),
+                "reasons": reasons, "samples": len(rows)}
+
+
+def cpu_sample_gflops(w, X, budget_s: float):
+    """Time the fp64 CPU oracle (as it stands) on a bounded contiguous row sample."""
+    import oracle
+    n, F = w.n, X.shape[1]
+    cores = os.cpu_count() or 1
+    # calibrate on ~0.2% of nnz, then size the sample for `budget_s`
+    def run(lo, hi):
+        rp = w.rowptr[lo:hi + 1]
+        t0 = time.perf_counter()
+        oracle.spmm(rp, w.colidx, w.vals, X, nthreads=cores, with_abs=False)
+        return time.perf_counter() - t0, int(rp[-1] - rp[0])
+    target = max(1, w.nnz // 500)
+    hi = int(np.searchsorted(w.rowptr, target))
+    t, nz = run(0, max(hi, 1))
+    rate = nz / max(t, 1e-6)
+    want_nnz = int(min(w.nnz, rate * budget_s))
+    lo = n // 3
+    hi = int(np.searchsorted(w.rowptr, w.rowptr[lo] + want_nnz))
+    hi = max(lo + 1, min(hi, n))
+    t, nz = run(lo, hi)
+    return {"value": 2.0 * nz * F / t / 1e9, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": f"rows [{lo},{hi}) of {w.name} ({nz} nnz = {100.0 * nz / w.nnz:.2f}% of nnz), "
+                      f"one fp64 SpMM layer, F={F}, {t:.1f} s"}, t
+
+
+# ---------------------------------------------------------------- reference arm (the oracle)
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import agcn_inputs as gen
+    w = gen.make_config(args.config)
+    F = args.F or w.F
+    X = w.X(F)
+    times, vals = [], []
+    budget = max(2.0, 120.0 / max(1, args.steps + args.warmup))
+    for i in range(args.warmup + args.steps):
+        cb, t = cpu_sample_gflops(w, X, budget)
+        if i >= args.warmup:
+            times.append(t)
+            vals.append(cb["value"])
+    v = statistics.median(vals)
+    layers = args.layers or w.layers
+    line = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": 0, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * statistics.median(times),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "impl": "reference",
+            "config": {"workload": w.meta["desc"], "name": w.name, "F": F, "layers": layers,
+                       "sample": cb["sample"]},
+            "cpu_baseline": dict(cb, value=v),
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------- the B200 arm
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import torch.distributed as dist
+
+    import agcn_inputs as gen
+    import paper_2308_11825_b200 as A
+    from paper_2308_11825_b200.dist import ShardLayout, propagate
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    P = world
+    A.library_path()
+
+    w = gen.make_config(args.config)
+    F = args.F or w.F
+    layers = args.layers or w.layers
+    n, nnz = w.n, w.nnz
+    X_host = w.X(F)
+
+    # resident inputs
+    rp_d = torch.from_numpy(w.rowptr).to(dev)
+    ci_d = torch.from_numpy(w.colidx).to(dev)
+    va_d = torch.from_numpy(w.vals).to(dev)
+    bounds = A.shard_bounds(rp_d, P)
+    lay = ShardLayout(bounds, rank)
+    S = lay.slot_rows
+    rp_local = rp_d[lay.lo:lay.hi + 1].contiguous()
+    X0 = torch.zeros((lay.padded_rows, F), dtype=torch.float32, device=dev)
+    lay.pad(torch.from_numpy(X_host).to(dev), X0)
+    bufs = [torch.empty_like(X0) for _ in range(min(layers, 2))]
+    plan_kw = dict(n_cols=n, max_block_warps=12, max_warp_nzs=32, partition=args.partition)
+    if P > 1:
+        plan_kw.update(col_bounds=bounds, col_slot_rows=S)
+
+    stream = torch.cuda.current_stream()
+    ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+    rec = {"plan": [], "spmm": [], "ag": []}
+
+    def all_gather(full, slot):
+        e0, e1 = ev(), ev()
+        e0.record(stream)
+        dist.all_gather_into_tensor(full, slot)
+        e1.record(stream)
+        rec["ag"].append((e0, e1))
+
+    def step(record: bool):
+        e0, e1 = ev(), ev()
+        e0.record(stream)
+        plan = A.Plan(rp_local, ci_d, **plan_kw)
+        e1.record(stream)
+        if record:
+            rec["plan"].append((e0, e1))
+
+        def spmm(Xin, out_rows):
+            s0, s1 = ev(), ev()
+            s0.record(stream)
+            plan.spmm(va_d, Xin, out=out_rows)
+            s1.record(stream)
+            if record:
+                rec["spmm"].append((s0, s1))
+        out = propagate(lay, spmm, X0, bufs, layers, all_gather if P > 1 else None)
+        return plan, out  # plans stay alive until after the timed region (closed below)
+
+    def barrier():
+        if P > 1:
+            dist.barrier()
+
+    # warm-up
+    for _ in range(max(3, args.warmup)):
+        plan, _ = step(False)
+        torch.cuda.synchronize()
+        plan.close()
+    rec = {"plan": [], "spmm": [], "ag": []}
+    st_plan = None
+
+    clocks = None if args.profile else ClockSampler(local)
+    barrier()
+    torch.cuda.synchronize()
+    l0 = A.launch_count()
+    t_start, t_end = ev(), ev()
+    t_start.record(stream)
+    plans = []
+    for _ in range(args.steps):
+        plan, out = step(True)
+        plans.append(plan)
+    t_end.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    launches = A.launch_count() - l0
+    clk = clocks.stop() if clocks else None
+    st_plan = plans[-1].stats()
+    for p_ in plans:
+        p_.close()
+    ms_local = t_start.elapsed_time(t_end) / args.steps
+    spmm_ms = [a.elapsed_time(b) for a, b in rec["spmm"]]
+    plan_ms = [a.elapsed_time(b) for a, b in rec["plan"]]
+    ag_ms = [a.elapsed_time(b) for a, b in rec["ag"]]
+    spmm_avg = sum(spmm_ms) / max(1, len(spmm_ms))
+    vec = torch.tensor([ms_local, spmm_avg, sum(plan_ms) / max(1, len(plan_ms)),
+                        sum(ag_ms) / max(1, len(ag_ms)) if ag_ms else 0.0], device=dev)
+    if P > 1:
+        dist.all_reduce(vec, op=dist.ReduceOp.MAX)
+    ms_step, spmm_max, plan_max, ag_max = [float(x) for x in vec.tolist()]
+
+    # correctness guard on the timed output (a few rows vs a host fp64 recomputation is the
+    # test suite's job; here: finite and the right shape)
+    Yfinal = lay.unpad(out) if P > 1 else out
+    assert Yfinal.shape == (n, F) and bool(torch.isfinite(Yfinal[: min(n, 4096)]).all())
+
+    flops_layer = 2.0 * nnz * F
+    value = flops_layer * layers / (ms_step * 1e-3) / 1e9
+
+    # byte model: B_comp per SpMM launch on this rank
+    n_p, nnz_p = lay.rows, int(w.rowptr[lay.hi] - w.rowptr[lay.lo])
+    b_comp = 4 * (n_p + 1) + 8 * nnz_p + 4 * n * F + 4 * n_p * F
+    b_gather = 4 * (n_p + 1) + 8 * nnz_p + 4 * nnz_p * F + 4 * n_p * F
+    peaks = load_peaks()
+    achieved = b_comp / (spmm_max * 1e-3) / 1e9
+    traffic, traffic_src = load_traffic(args.config, F)
+
+    line = None
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": P, "steps": args.steps,
+            "warmup": max(3, args.warmup), "ms_per_step": ms_step, "higher_is_better": True,
+            "scaling": "strong" if P > 1 else "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic",
+            "config": {"workload": w.meta["desc"], "name": w.name, "n": n, "nnz": nnz, "F": F,
+                       "layers": layers, "partition": args.partition, "parallelism": f"row-shard{P}",
+                       "max_block_warps": 12, "max_warp_nzs": 32,
+                       "l2": "inputs larger than L2 (CSR + X > 126 MB)" if
+                             (8 * nnz + 4 * n * F) > 126e6 else "inputs fit in L2 (warm)",
+                       "step": "agcn_plan + layers x agcn_spmm (+ all-gather if N>1)"},
+            "spmm_only": {"ms_per_layer": spmm_max, "gflops": flops_layer / (spmm_max * 1e-3) / 1e9,
+                          "b_comp_gbs": achieved, "b_gather_gbs": b_gather / (spmm_max * 1e-3) / 1e9},
+            "plan_ms": plan_max, "allgather_ms": ag_max if P > 1 else 0.0,
+            "plan_stats": {k: st_plan[k] for k in ("nblocks", "n_zero_rows", "n_oversized_rows",
+                                                   "n_oversized_blocks", "max_deg")},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                         "frac": achieved / peaks["hbm_gbs"], "traffic": traffic,
+                         "kernel": "agcn_spmm (k_spmm_block + k_ov_reduce)",
+                         "bytes_per_launch": b_comp, "peak_source": peaks["source"],
+                         "traffic_source": traffic_src},
+            "gpu_launches": int(launches),
+            "clocks": clk,
+        }
+
+    # ---- cuSPARSE on the same box (1 GPU, whole graph, one layer)
+    if rank == 0 and P == 1 and not args.no_cusparse and not args.profile:
+        try:
+            Acsr = torch.sparse_csr_tensor(rp_d, ci_d, va_d, size=(n, n))
+            Xd = X0
+            for _ in range(3):
+                torch.sparse.mm(Acsr, Xd)
+            torch.cuda.synchronize()
+            a, b = ev(), ev()
+            a.record(stream)
+            for _ in range(5):
+                torch.sparse.mm(Acsr, Xd)
+            b.record(stream)
+            torch.cuda.synchronize()
+            cms = a.elapsed_time(b) / 5
+            line["cusparse"] = {"ms_per_layer": cms, "gflops": flops_layer / (cms * 1e-3) / 1e9,
+                                "via": "torch.sparse.mm (cusparseSpMM, CSR)",
+                                "speedup_agcn_spmm": cms / spmm_max}
+        except Exception as e:  # pragma: no cover
+            line["cusparse"] = {"error": str(e)[:200]}
+
+    # ---- end to end through the C ABI on HOST buffers (copies inside the timed region)
+    if not args.no_e2e and not args.profile:
+        e2e = None
+        if P == 1:
+            pin = lambda a: torch.from_numpy(a).pin_memory()  # noqa: E731
+            rp_h, ci_h, va_h, X_h = pin(w.rowptr), pin(w.colidx), pin(w.vals), pin(X_host)
+            Y_h = torch.empty((n, F), dtype=torch.float32).pin_memory()
+            A.propagate_host(rp_h, ci_h, va_h, X_h, layers, out=Y_h)   # warm-up
+            ts = []
+            for _ in range(args.e2e_steps):
+                t0 = time.perf_counter()
+                A.propagate_host(rp_h, ci_h, va_h, X_h, layers, out=Y_h)
+                ts.append(time.perf_counter() - t0)
+            t = statistics.median(ts)
+            e2e = {"value": flops_layer * layers / t / 1e9, "unit": UNIT, "ms_per_step": 1e3 * t,
+                   "h2d_bytes_per_step": 4 * (n + 1) + 8 * nnz + 4 * n * F,
+                   "d2h_bytes_per_step": 4 * n * F, "api": "agcn_propagate_host (C ABI)"}
+        else:
+            pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()  # noqa: E731
+            lo, hi = lay.lo, lay.hi
+            a0, a1 = int(w.rowptr[lo]), int(w.rowptr[hi])
+            rp_h = pin(w.rowptr[lo:hi + 1] - a0)
+            ci_h, va_h = pin(w.colidx[a0:a1]), pin(w.vals[a0:a1])
+            X_h = pin(X_host)
+            Y_h = torch.empty((lay.rows, F), dtype=torch.float32).pin_memory()
+            ts = []
+            for it in range(args.e2e_steps + 1):
+                barrier()
+                torch.cuda.synchronize()
+                t0 = time.perf_counter()
+                rp_e, ci_e, va_e = (rp_h.to(dev, non_blocking=True), ci_h.to(dev, non_blocking=True),
+                                    va_h.to(dev, non_blocking=True))
+                Xe = torch.empty((lay.padded_rows, F), dtype=torch.float32, device=dev)
+                lay.pad(X_h.to(dev, non_blocking=True), Xe)
+                pe = A.Plan(rp_e, ci_e, **plan_kw)
+                bufs_e = [torch.empty_like(Xe) for _ in range(min(layers, 2))]
+                oute = propagate(lay, lambda Xin, o: pe.spmm(va_e, Xin, out=o), Xe, bufs_e, layers,
+                                 lambda full, slot: dist.all_gather_into_tensor(full, slot))
+                Y_h.copy_(lay.own_rows(oute))
+                torch.cuda.synchronize()
+                dt = torch.tensor([time.perf_counter() - t0], device=dev)
+                dist.all_reduce(dt, op=dist.ReduceOp.MAX)
+                pe.close()
+                if it > 0:
+                    ts.append(float(dt.item()))
+            t = statistics.median(ts)
+            e2e = {"value": flops_layer * layers / t / 1e9, "unit": UNIT, "ms_per_step": 1e3 * t,
+                   "h2d_bytes_per_step": 4 * (lay.rows + 1) + 8 * (a1 - a0) + 4 * n * F,
+                   "d2h_bytes_per_step": 4 * lay.rows * F, "api": "Plan/spmm + NCCL (python)"}
+        if rank == 0:
+            line["e2e"] = e2e
+
+    # ---- CPU oracle baseline (rank 0, N=1 only)
+    if rank == 0 and P == 1 and not args.no_cpu_baseline and not args.profile:
+        cb, _ = cpu_sample_gflops(w, X_host, args.cpu_seconds)
+        line["cpu_baseline"] = cb
+
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if P > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

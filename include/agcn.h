@@ -1,0 +1,167 @@
+/*
+ * agcn.h -- C ABI of the B200-native (sm_100a) Accel-GCN aggregation SpMM, Y = A.X.
+ *
+ * The method is arXiv 2308.11825 (Accel-GCN).  P:n below is /root/reference/PAPER.md line n.
+ *   - GCN feature aggregation X^{l+1} = sigma(A' Y^l) is an SpMM of a sparse adjacency
+ *     with a dense feature matrix.  This library computes the SpMM (no sigma).
+ *   - agcn_plan builds the preprocessing of section III-C: degree sorting, the
+ *     partition patterns of Algorithm 1 and the block-level partition of
+ *     Algorithm 2, packed as one 128-bit descriptor per block.
+ *   - agcn_spmm runs the SpMM over that metadata with the combined-warp mapping of the
+ *     dense column dimension and hierarchical accumulation.
+ *
+ * Conventions for every entry point:
+ *   - Indices are int32, values fp32.  Dense matrices are row-major with ld = F.
+ *   - "DEVICE" pointers are CUDA device pointers on the current device; "HOST" pointers
+ *     are host memory (pinned recommended).  No call takes ownership of caller memory.
+ *   - Errors are reported by return code only (never abort/exit/throw across the ABI);
+ *     functions returning a plan return NULL on failure.  agcn_last_status() and
+ *     agcn_last_error() give the code and a message for the calling thread.
+ *   - Streams are cudaStream_t (agcn_stream_t is the same type); NULL = legacy default.
+ */
+#ifndef AGCN_H
+#define AGCN_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+struct CUstream_st;
+typedef struct CUstream_st* agcn_stream_t; /* == cudaStream_t */
+
+typedef struct agcn_plan_s* agcn_plan_t;   /* opaque, immutable after creation */
+
+typedef enum {
+    AGCN_OK = 0,
+    AGCN_ERR_INVALID_ARG = 1, /* null pointer, negative size, nnz >= 2^31, F <= 0, X == Y ... */
+    AGCN_ERR_BAD_CSR = 2,     /* rowptr not monotone, rowptr[n]-rowptr[0] != nnz, colidx out of range */
+    AGCN_ERR_OOM = 3,         /* device allocation failed */
+    AGCN_ERR_CUDA = 4,        /* any other CUDA runtime error (message has the CUDA string) */
+    AGCN_ERR_OVERFLOW = 5,    /* a descriptor field does not fit (16-bit info halves, 32-bit loc) */
+    AGCN_ERR_UNSUPPORTED = 6  /* configuration outside this build's limits (see agcn_plan_ex) */
+} agcn_status_t;
+
+typedef enum {
+    AGCN_PARTITION_BLOCK = 0, /* degree sort + block-level partition (the method) */
+    AGCN_PARTITION_WARP = 1   /* warp-level partition, no sort (ablation arm, Fig. 3(b)) */
+} agcn_partition_t;
+
+typedef struct {
+    int32_t max_block_warps;   /* Alg. 1 max_block_warps; default 12 */
+    int32_t max_warp_nzs;      /* Alg. 1 max_warp_nzs; default 32 */
+    int32_t partition;         /* agcn_partition_t; default AGCN_PARTITION_BLOCK */
+    int32_t validate;          /* 1 (default): check the CSR on device -> AGCN_ERR_BAD_CSR */
+    int64_t n_cols;            /* columns of A (rows of X); 0 -> n */
+    agcn_stream_t stream;      /* stream the plan is built on; default NULL */
+    /* Optional column relabel for a padded all-gather layout (multi-GPU):
+       if col_nparts > 0, column j is stored as p*col_slot_rows + (j - col_bounds[p]) where
+       col_bounds[p] <= j < col_bounds[p+1] (HOST array of col_nparts+1 int64).  The plan's
+       SpMM then reads X in that padded layout (col_nparts * col_slot_rows rows). */
+    const int64_t* col_bounds;
+    int32_t col_nparts;
+    int64_t col_slot_rows;
+} agcn_opts_t;
+
+typedef struct {
+    int64_t n, n_cols, nnz;
+    int64_t nblocks;            /* block descriptors (AGCN_PARTITION_BLOCK) */
+    int64_t ntasks;             /* warp tasks (AGCN_PARTITION_WARP) */
+    int64_t deg_bound;          /* max_block_warps * max_warp_nzs (Alg. 1 line 1) */
+    int64_t max_deg;
+    int64_t n_zero_rows;        /* degree-0 rows (sorted first, no descriptor) */
+    int64_t n_oversized_rows;   /* rows with degree > deg_bound */
+    int64_t n_oversized_blocks; /* descriptors of those rows (chunks of <= deg_bound nnz) */
+    int32_t max_block_warps, max_warp_nzs, partition, reserved;
+    size_t device_bytes;        /* device memory owned by the plan */
+} agcn_plan_stats_t;
+
+typedef enum {
+    AGCN_FIELD_PERM = 0,          /* int32[n]       sorted position -> original row (sorted_to_orig) */
+    AGCN_FIELD_BLOCKS = 1,        /* uint32[4*nblocks] descriptors (deg, loc, row, info), little endian */
+    AGCN_FIELD_SORTED_COLIDX = 2, /* int32[nnz]     colidx in degree-sorted row order (after relabel) */
+    AGCN_FIELD_ROW_SRC_OFF = 3,   /* int32[n]       rowptr[perm[k]] - rowptr[0] */
+    AGCN_FIELD_TASKS = 4,         /* uint32[4*ntasks] warp tasks (row, col, len, 0) */
+    AGCN_FIELD_SORTED_ROWPTR = 5  /* int32[n+1]     row pointer of the degree-sorted CSR */
+} agcn_field_t;
+
+/* Fill *opts with the defaults above. */
+void agcn_default_opts(agcn_opts_t* opts);
+
+/*
+ * Build the degree-sort + block-partition plan on the current device (Alg. 1, Alg. 2).
+ *   rowptr: DEVICE int32[n+1], non-decreasing; rowptr[0] may be nonzero (a row shard of a
+ *           larger CSR) -- then colidx is indexed by the rowptr values (global arrays).
+ *   colidx: DEVICE int32, entries rowptr[0] .. rowptr[n]-1 are read; 0 <= colidx < n_cols.
+ *   n, nnz: rows of A and rowptr[n] - rowptr[0]; 0 <= n, 0 <= nnz < 2^31.
+ * Degree order is ascending and stable (ties keep original row order); degree-0 rows come
+ * first and get no descriptor.  The plan copies everything it needs: the caller may free
+ * rowptr/colidx after return.  Synchronises the plan stream (reads the bucket counts and
+ * the validation flag).  Limits: deg_bound = max_block_warps*max_warp_nzs <= 2048,
+ * max_block_warps < 65536 and max_warp_nzs < 65536 (16-bit info halves) -> otherwise
+ * AGCN_ERR_UNSUPPORTED / AGCN_ERR_OVERFLOW.  Returns NULL on error.
+ */
+agcn_plan_t agcn_plan(const int32_t* rowptr, const int32_t* colidx, int64_t n, int64_t nnz);
+agcn_plan_t agcn_plan_ex(const int32_t* rowptr, const int32_t* colidx, int64_t n, int64_t nnz,
+                         const agcn_opts_t* opts);
+
+/*
+ * Y = A.X with the plan's partition.
+ *   vals: DEVICE fp32, indexed like colidx (the caller's ORIGINAL CSR order, rowptr values).
+ *   X:    DEVICE fp32 [n_cols x F] row-major (or the padded layout if the plan relabels).
+ *   Y:    DEVICE fp32 [n x F] row-major, original row order; must not overlap X.
+ * Every element of Y is written (rows of degree 0 become 0).  Asynchronous on `stream`;
+ * never synchronises.  Deterministic for AGCN_PARTITION_BLOCK (fixed summation order, no
+ * atomics); AGCN_PARTITION_WARP uses fp32 global atomics for rows split across warps.
+ * May grow a plan-owned scratch buffer (stream-ordered) the first time a larger F is used.
+ * Calls on one plan must be stream-ordered (the scratch is shared).
+ * Any F >= 1 is accepted; F % 4 == 0 with 16-byte aligned X and Y takes the float4 path.
+ */
+agcn_status_t agcn_spmm(agcn_plan_t plan, const float* vals, const float* X, int32_t F, float* Y,
+                        agcn_stream_t stream);
+
+/* Release the plan's device memory (synchronises the device first).  NULL is a no-op. */
+agcn_status_t agcn_plan_destroy(agcn_plan_t plan);
+
+/* Plan statistics (host struct, filled without device synchronisation). */
+agcn_status_t agcn_plan_stats(agcn_plan_t plan, agcn_plan_stats_t* out);
+
+/* Copy one plan array (agcn_field_t) to HOST memory; bytes must equal the field size
+   given in agcn_field_t (else AGCN_ERR_INVALID_ARG).  Synchronous. */
+agcn_status_t agcn_plan_copy(agcn_plan_t plan, int32_t field, void* host_dst, size_t bytes);
+
+/*
+ * nnz-balanced contiguous row shards for nranks GPUs (BASELINE.json north_star):
+ * bounds[0] = 0, bounds[nranks] = n, bounds[p] = first row r with
+ * rowptr[r] - rowptr[0] >= floor(p * nnz / nranks).  rowptr: DEVICE int32[n+1];
+ * bounds_host: HOST int64[nranks+1].  Synchronises `stream`.
+ */
+agcn_status_t agcn_shard_bounds(const int32_t* rowptr, int64_t n, int32_t nranks,
+                                int64_t* bounds_host, agcn_stream_t stream);
+
+/*
+ * End-to-end convenience on HOST buffers: copies the CSR and X to the device, builds the
+ * plan, runs `layers` propagations Y_{l+1} = A.Y_l (Y_0 = X; layers > 1 needs n_cols == n),
+ * and copies the last Y back to Y_host [n x F].  Device memory is stream-ordered
+ * (cudaMallocAsync) and released before return.  Synchronous.  opts may be NULL.
+ */
+agcn_status_t agcn_propagate_host(const int32_t* rowptr_host, const int32_t* colidx_host,
+                                  const float* vals_host, int64_t n, int64_t nnz,
+                                  const float* X_host, int32_t F, int32_t layers, float* Y_host,
+                                  const agcn_opts_t* opts);
+
+agcn_status_t agcn_last_status(void);
+const char* agcn_last_error(void);
+
+/* Number of kernels this library has launched in this process (monotone counter). */
+uint64_t agcn_launch_count(void);
+
+/* Library version string, e.g. "agcn 0.1 sm_100a". */
+const char* agcn_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* AGCN_H */

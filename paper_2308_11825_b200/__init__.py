@@ -1,0 +1,243 @@
+"""B200-native (sm_100a) Accel-GCN aggregation SpMM, Y = A.X (arXiv 2308.11825).
+
+Thin Python binding over the C ABI in ``include/agcn.h`` (argument marshalling only; every
+step of the path runs in the CUDA kernels of ``csrc/``).  PyTorch supplies device memory,
+streams and process groups.  There is no CPU fallback: if ``libagcn.so`` cannot be built or
+loaded, or a tensor is not on a CUDA device, the call raises.
+
+    plan = Plan(rowptr, colidx)            # agcn_plan: degree sort + block partition (Alg. 1/2)
+    Y = plan.spmm(vals, X)                 # agcn_spmm: combined-warp SpMM
+"""
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from . import _lib
+from ._lib import FIELDS, STATUS
+
+__all__ = ["Plan", "AgcnError", "agcn_plan", "agcn_spmm", "shard_bounds", "propagate_host",
+           "launch_count", "version", "library_path"]
+
+
+class AgcnError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"{STATUS.get(code, code)}: {msg}")
+        self.code = code
+        self.status = STATUS.get(code, str(code))
+
+
+def _raise_last():
+    L = _lib.lib()
+    code = L.agcn_last_status()
+    msg = L.agcn_last_error().decode(errors="replace")
+    raise AgcnError(code, msg)
+
+
+def _check(code: int):
+    if code != 0:
+        _raise_last()
+
+
+def _torch():
+    import torch
+    return torch
+
+
+def _dev_ptr(t, dtype_name: str, what: str) -> int:
+    torch = _torch()
+    if not isinstance(t, torch.Tensor):
+        raise TypeError(f"{what} must be a torch.Tensor on a CUDA device")
+    if not t.is_cuda:
+        raise TypeError(f"{what} must be on a CUDA device (no CPU fallback)")
+    want = {"int32": torch.int32, "float32": torch.float32}[dtype_name]
+    if t.dtype != want:
+        raise TypeError(f"{what} must be {dtype_name}, got {t.dtype}")
+    if not t.is_contiguous():
+        raise ValueError(f"{what} must be contiguous")
+    return t.data_ptr()
+
+
+def _stream_handle(stream) -> int:
+    torch = _torch()
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    if isinstance(stream, torch.cuda.Stream):
+        return stream.cuda_stream
+    return int(stream)
+
+
+def library_path() -> str:
+    from . import _build
+    _lib.lib()
+    return _build.LIB
+
+
+def version() -> str:
+    return _lib.lib().agcn_version().decode()
+
+
+def launch_count() -> int:
+    """Kernels launched by libagcn.so in this process (monotone)."""
+    return int(_lib.lib().agcn_launch_count())
+
+
+class Plan:
+    """agcn_plan_ex: degree-sort + block-partition metadata on the current CUDA device.
+
+    rowptr: int32 [n+1] CUDA tensor (rowptr[0] may be nonzero for a row shard; colidx is
+    then indexed by the rowptr values).  colidx: int32 CUDA tensor.
+    partition: "block" (the method) or "warp" (the ablation arm, Fig. 3(b)).
+    col_bounds / col_slot_rows: optional padded-layout column relabel (multi-GPU).
+    """
+
+    def __init__(self, rowptr, colidx, n: int | None = None, nnz: int | None = None, *,
+                 n_cols: int | None = None, max_block_warps: int = 12, max_warp_nzs: int = 32,
+                 partition: str = "block", col_bounds=None, col_slot_rows: int | None = None,
+                 stream=None):
+        L = _lib.lib()
+        rp = _dev_ptr(rowptr, "int32", "rowptr")
+        ci = _dev_ptr(colidx, "int32", "colidx") if colidx.numel() else 0
+        if n is None:
+            n = rowptr.numel() - 1
+        if nnz is None:
+            nnz = int(rowptr[-1].item() - rowptr[0].item()) if n >= 0 else 0
+        opts = _lib.Opts()
+        L.agcn_default_opts(ctypes.byref(opts))
+        opts.max_block_warps = max_block_warps
+        opts.max_warp_nzs = max_warp_nzs
+        opts.partition = {"block": 0, "warp": 1}[partition]
+        opts.n_cols = 0 if n_cols is None else int(n_cols)
+        opts.stream = _stream_handle(stream)
+        self._bounds_keep = None
+        if col_bounds is not None:
+            b = np.ascontiguousarray(col_bounds, dtype=np.int64)
+            self._bounds_keep = b
+            opts.col_bounds = b.ctypes.data_as(ctypes.POINTER(ctypes.c_int64))
+            opts.col_nparts = b.size - 1
+            opts.col_slot_rows = int(col_slot_rows)
+        h = L.agcn_plan_ex(rp or None, ci or None, int(n), int(nnz), ctypes.byref(opts))
+        if not h:
+            _raise_last()
+        self._h = h
+        self.partition = partition
+        st = self.stats()
+        self.n, self.n_cols, self.nnz = st["n"], st["n_cols"], st["nnz"]
+        self.x_rows = (opts.col_nparts * opts.col_slot_rows) if col_bounds is not None else self.n_cols
+
+    @property
+    def handle(self) -> int:
+        if not self._h:
+            raise ValueError("plan is closed")
+        return self._h
+
+    def stats(self) -> dict:
+        st = _lib.Stats()
+        _check(_lib.lib().agcn_plan_stats(self.handle, ctypes.byref(st)))
+        return {k: getattr(st, k) for k, _ in _lib.Stats._fields_ if k != "reserved"}
+
+    def copy(self, field: str) -> np.ndarray:
+        st = self.stats()
+        shapes = {"perm": (st["n"],), "blocks": (st["nblocks"], 4),
+                  "sorted_colidx": (st["nnz"],), "row_src_off": (st["n"],),
+                  "tasks": (st["ntasks"], 4), "sorted_rowptr": (st["n"] + 1,)}
+        dt = np.uint32 if field in ("blocks", "tasks") else np.int32
+        out = np.zeros(shapes[field], dtype=dt)
+        _check(_lib.lib().agcn_plan_copy(self.handle, FIELDS[field],
+                                         out.ctypes.data or None, out.nbytes))
+        return out
+
+    def spmm(self, vals, X, out=None, stream=None):
+        """Y = A.X (asynchronous on `stream`, default the current torch stream)."""
+        torch = _torch()
+        F = X.shape[1] if X.dim() == 2 else 1
+        if out is None:
+            out = torch.empty((self.n, F), dtype=torch.float32, device=X.device)
+        if X.dim() != 2 or X.shape[0] != self.x_rows:
+            raise ValueError(f"X must be [{self.x_rows}, F], got {tuple(X.shape)}")
+        if out.shape != (self.n, F):
+            raise ValueError(f"out must be [{self.n}, {F}]")
+        v = _dev_ptr(vals, "float32", "vals") if vals.numel() else 0
+        x = _dev_ptr(X, "float32", "X") if X.numel() else 0
+        y = _dev_ptr(out, "float32", "out") if out.numel() else 0
+        _check(_lib.lib().agcn_spmm(self.handle, v or None, x or None, int(F), y or None,
+                                    _stream_handle(stream)))
+        return out
+
+    def close(self):
+        if getattr(self, "_h", None):
+            _lib.lib().agcn_plan_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+
+# ---------------------------------------------------------------- C-ABI-named functions
+def agcn_plan(rowptr, colidx, n: int, nnz: int) -> Plan:
+    return Plan(rowptr, colidx, n, nnz)
+
+
+def agcn_spmm(plan: Plan, vals, X, F: int, Y, stream=None) -> None:
+    v = _dev_ptr(vals, "float32", "vals") if vals.numel() else 0
+    x = _dev_ptr(X, "float32", "X") if X.numel() else 0
+    y = _dev_ptr(Y, "float32", "Y") if Y.numel() else 0
+    _check(_lib.lib().agcn_spmm(plan.handle, v or None, x or None, int(F), y or None,
+                                _stream_handle(stream)))
+
+
+def shard_bounds(rowptr, nranks: int, stream=None) -> np.ndarray:
+    """agcn_shard_bounds: nnz-balanced row shard bounds (int64 [nranks+1])."""
+    rp = _dev_ptr(rowptr, "int32", "rowptr")
+    out = np.zeros(nranks + 1, dtype=np.int64)
+    _check(_lib.lib().agcn_shard_bounds(rp, rowptr.numel() - 1, int(nranks),
+                                        out.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
+                                        _stream_handle(stream)))
+    return out
+
+
+def _host_ptr(a, dtype):
+    torch = _torch()
+    if isinstance(a, torch.Tensor):
+        if a.is_cuda:
+            raise TypeError("propagate_host takes HOST buffers")
+        if a.dtype != {np.int32: torch.int32, np.float32: torch.float32}[dtype]:
+            raise TypeError("wrong dtype")
+        if not a.is_contiguous():
+            raise ValueError("must be contiguous")
+        return a.data_ptr()
+    if not (isinstance(a, np.ndarray) and a.dtype == dtype and a.flags.c_contiguous):
+        raise TypeError(f"expected a contiguous {np.dtype(dtype).name} numpy array")
+    return a.ctypes.data
+
+
+def propagate_host(rowptr, colidx, vals, X, layers: int = 1, out=None, *, max_block_warps=12,
+                   max_warp_nzs=32, partition="block", stream=None):
+    """agcn_propagate_host: HOST buffers in, HOST result out (H2D, plan, layers x SpMM, D2H)."""
+    n = (rowptr.shape[0] if hasattr(rowptr, "shape") else len(rowptr)) - 1
+    nnz = int(rowptr[-1]) - int(rowptr[0])
+    F = X.shape[1]
+    if out is None:
+        out = np.empty((n, F), dtype=np.float32)
+    L = _lib.lib()
+    opts = _lib.Opts()
+    L.agcn_default_opts(ctypes.byref(opts))
+    opts.max_block_warps, opts.max_warp_nzs = max_block_warps, max_warp_nzs
+    opts.partition = {"block": 0, "warp": 1}[partition]
+    opts.n_cols = X.shape[0]
+    opts.stream = _stream_handle(stream) if stream is not None else 0
+    _check(L.agcn_propagate_host(_host_ptr(rowptr, np.int32), _host_ptr(colidx, np.int32) or None,
+                                 _host_ptr(vals, np.float32) or None, n, nnz,
+                                 _host_ptr(X, np.float32), int(F), int(layers),
+                                 _host_ptr(out, np.float32), ctypes.byref(opts)))
+    return out

@@ -1,0 +1,261 @@
+// abi.cu -- the extern "C" entry points of include/agcn.h: argument checks, error state,
+// plan lifetime and introspection, row shards, and the host-buffer end-to-end call.
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <string>
+
+#include "internal.h"
+
+namespace agcn {
+
+std::atomic<uint64_t> g_launches{0};
+
+namespace {
+thread_local agcn_status_t t_status = AGCN_OK;
+thread_local std::string t_msg;
+}  // namespace
+
+void set_error(agcn_status_t code, const std::string& msg) {
+    t_status = code;
+    t_msg = msg;
+}
+void clear_error() {
+    t_status = AGCN_OK;
+    t_msg.clear();
+}
+agcn_status_t last_status() { return t_status; }
+const char* last_message() { return t_msg.c_str(); }
+agcn_status_t cuda_status(cudaError_t e) {
+    return e == cudaErrorMemoryAllocation ? AGCN_ERR_OOM : AGCN_ERR_CUDA;
+}
+
+agcn_plan_s* build_plan(const int32_t* rowptr, const int32_t* colidx, int64_t n, int64_t nnz,
+                        const agcn_opts_t& o);
+void free_plan_arrays(agcn_plan_s* p);
+
+namespace {
+
+// nnz-balanced shard bounds: bounds[p] = first r with rowptr[r] - rowptr[0] >= floor(p nnz / P)
+__global__ void k_shard_bounds(const int32_t* __restrict__ rowptr, int64_t n, int32_t P,
+                               int64_t* __restrict__ out) {
+    const int p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p > P) return;
+    const int64_t base = rowptr[0], nnz = (int64_t)rowptr[n] - base;
+    if (p == 0) { out[0] = 0; return; }
+    if (p == P) { out[P] = n; return; }
+    const int64_t target = base + (p * nnz) / P;
+    int64_t lo = 0, hi = n;  // first r in [0, n] with rowptr[r] >= target
+    while (lo < hi) {
+        int64_t mid = (lo + hi) >> 1;
+        if ((int64_t)rowptr[mid] < target) lo = mid + 1; else hi = mid;
+    }
+    out[p] = lo;
+}
+
+template <class F>
+agcn_status_t guarded(F&& f) {
+    try {
+        clear_error();
+        f();
+        return AGCN_OK;
+    } catch (const Error& e) {
+        set_error(e.code, e.msg);
+        return e.code;
+    } catch (const std::bad_alloc&) {
+        set_error(AGCN_ERR_OOM, "host allocation failed");
+        return AGCN_ERR_OOM;
+    } catch (...) {
+        set_error(AGCN_ERR_CUDA, "unknown exception");
+        return AGCN_ERR_CUDA;
+    }
+}
+
+bool ranges_overlap(const void* a, size_t na, const void* b, size_t nb) {
+    auto x = reinterpret_cast<uintptr_t>(a), y = reinterpret_cast<uintptr_t>(b);
+    return x < y + nb && y < x + na;
+}
+
+}  // namespace
+}  // namespace agcn
+
+using namespace agcn;
+
+extern "C" {
+
+void agcn_default_opts(agcn_opts_t* o) {
+    if (!o) return;
+    std::memset(o, 0, sizeof(*o));
+    o->max_block_warps = 12;
+    o->max_warp_nzs = 32;
+    o->partition = AGCN_PARTITION_BLOCK;
+    o->validate = 1;
+}
+
+agcn_plan_t agcn_plan_ex(const int32_t* rowptr, const int32_t* colidx, int64_t n, int64_t nnz,
+                         const agcn_opts_t* opts) {
+    agcn_plan_t out = nullptr;
+    guarded([&] {
+        agcn_opts_t o;
+        if (opts) o = *opts; else agcn_default_opts(&o);
+        out = build_plan(rowptr, colidx, n, nnz, o);
+    });
+    return out;
+}
+
+agcn_plan_t agcn_plan(const int32_t* rowptr, const int32_t* colidx, int64_t n, int64_t nnz) {
+    return agcn_plan_ex(rowptr, colidx, n, nnz, nullptr);
+}
+
+agcn_status_t agcn_spmm(agcn_plan_t plan, const float* vals, const float* X, int32_t F, float* Y,
+                        agcn_stream_t stream) {
+    return guarded([&] {
+        AGCN_CHECK(plan != nullptr, AGCN_ERR_INVALID_ARG, "plan is NULL");
+        AGCN_CHECK(F > 0, AGCN_ERR_INVALID_ARG, "F must be > 0");
+        if (plan->n == 0) return;
+        AGCN_CHECK(Y != nullptr, AGCN_ERR_INVALID_ARG, "Y is NULL");
+        AGCN_CHECK(plan->nnz == 0 || (vals != nullptr && X != nullptr), AGCN_ERR_INVALID_ARG,
+                   "vals / X is NULL");
+        AGCN_CHECK((int64_t)F * std::max<int64_t>(plan->n, plan->x_rows) < (1ll << 40),
+                   AGCN_ERR_INVALID_ARG, "F too large");
+        AGCN_CHECK(X == nullptr || X != Y, AGCN_ERR_INVALID_ARG, "X and Y must not alias");
+        if (X) {
+            const size_t nx = sizeof(float) * (size_t)plan->x_rows * F;
+            const size_t ny = sizeof(float) * (size_t)plan->n * F;
+            AGCN_CHECK(!ranges_overlap(X, nx, Y, ny), AGCN_ERR_INVALID_ARG, "X and Y overlap");
+        }
+        spmm_launch(plan, vals, X, F, Y, (cudaStream_t)stream);
+    });
+}
+
+agcn_status_t agcn_plan_destroy(agcn_plan_t plan) {
+    return guarded([&] {
+        if (!plan) return;
+        int cur = 0;
+        cudaGetDevice(&cur);
+        if (cur != plan->device) cudaSetDevice(plan->device);
+        cudaDeviceSynchronize();
+        free_plan_arrays(plan);
+        if (cur != plan->device) cudaSetDevice(cur);
+        delete plan;
+    });
+}
+
+agcn_status_t agcn_plan_stats(agcn_plan_t plan, agcn_plan_stats_t* out) {
+    return guarded([&] {
+        AGCN_CHECK(plan && out, AGCN_ERR_INVALID_ARG, "NULL argument");
+        std::memset(out, 0, sizeof(*out));
+        out->n = plan->n;
+        out->n_cols = plan->n_cols;
+        out->nnz = plan->nnz;
+        out->nblocks = plan->nblocks;
+        out->ntasks = plan->ntasks;
+        out->deg_bound = plan->deg_bound;
+        out->max_deg = plan->max_deg;
+        out->n_zero_rows = plan->n_zero;
+        out->n_oversized_rows = plan->n_ov;
+        out->n_oversized_blocks = plan->ov_chunks;
+        out->max_block_warps = plan->mbw;
+        out->max_warp_nzs = plan->mwn;
+        out->partition = plan->partition;
+        out->device_bytes = plan->device_bytes + plan->ov_partial_floats * sizeof(float);
+    });
+}
+
+agcn_status_t agcn_plan_copy(agcn_plan_t plan, int32_t field, void* host_dst, size_t bytes) {
+    return guarded([&] {
+        AGCN_CHECK(plan && host_dst, AGCN_ERR_INVALID_ARG, "NULL argument");
+        const void* src = nullptr;
+        size_t want = 0;
+        const bool blk = plan->partition == AGCN_PARTITION_BLOCK;
+        switch (field) {
+            case AGCN_FIELD_PERM: src = plan->perm; want = 4 * (size_t)plan->n; break;
+            case AGCN_FIELD_BLOCKS: src = plan->desc; want = 16 * (size_t)plan->nblocks; break;
+            case AGCN_FIELD_SORTED_COLIDX: src = plan->sorted_colidx; want = 4 * (size_t)plan->nnz; break;
+            case AGCN_FIELD_ROW_SRC_OFF: src = plan->row_src_off; want = 4 * (size_t)plan->n; break;
+            case AGCN_FIELD_TASKS: src = plan->tasks; want = 16 * (size_t)plan->ntasks; break;
+            case AGCN_FIELD_SORTED_ROWPTR: src = plan->sorted_rowptr; want = 4 * (size_t)(plan->n + 1); break;
+            default: throw Error{AGCN_ERR_INVALID_ARG, "unknown field"};
+        }
+        const bool is_task = field == AGCN_FIELD_TASKS;
+        AGCN_CHECK(is_task ? !blk : blk, AGCN_ERR_INVALID_ARG, "field not present for this partition");
+        AGCN_CHECK(bytes == want, AGCN_ERR_INVALID_ARG,
+                   "bytes must equal the field size (" + std::to_string(want) + ")");
+        if (want) AGCN_CUDA(cudaMemcpy(host_dst, src, want, cudaMemcpyDeviceToHost));
+    });
+}
+
+agcn_status_t agcn_shard_bounds(const int32_t* rowptr, int64_t n, int32_t nranks, int64_t* bounds_host,
+                                agcn_stream_t stream) {
+    return guarded([&] {
+        AGCN_CHECK(rowptr && bounds_host && n >= 0 && nranks >= 1, AGCN_ERR_INVALID_ARG, "bad argument");
+        cudaStream_t s = (cudaStream_t)stream;
+        int64_t* d = dalloc<int64_t>(nranks + 1, s);
+        k_shard_bounds<<<(nranks + 1 + 127) / 128, 128, 0, s>>>(rowptr, n, nranks, d);
+        post_launch();
+        AGCN_CUDA(cudaMemcpyAsync(bounds_host, d, sizeof(int64_t) * (nranks + 1), cudaMemcpyDeviceToHost, s));
+        dfree(d, s);
+        AGCN_CUDA(cudaStreamSynchronize(s));
+    });
+}
+
+agcn_status_t agcn_propagate_host(const int32_t* rowptr_h, const int32_t* colidx_h, const float* vals_h,
+                                  int64_t n, int64_t nnz, const float* X_h, int32_t F, int32_t layers,
+                                  float* Y_h, const agcn_opts_t* opts) {
+    return guarded([&] {
+        AGCN_CHECK(rowptr_h && X_h && Y_h && F > 0 && layers >= 1 && n >= 0 && nnz >= 0,
+                   AGCN_ERR_INVALID_ARG, "bad argument");
+        AGCN_CHECK(nnz == 0 || (colidx_h && vals_h), AGCN_ERR_INVALID_ARG, "colidx / vals is NULL");
+        agcn_opts_t o;
+        if (opts) o = *opts; else agcn_default_opts(&o);
+        AGCN_CHECK(o.col_nparts == 0, AGCN_ERR_INVALID_ARG, "padded layouts are not supported here");
+        const int64_t n_cols = o.n_cols > 0 ? o.n_cols : n;
+        AGCN_CHECK(layers == 1 || n_cols == n, AGCN_ERR_INVALID_ARG, "layers > 1 needs a square A");
+        cudaStream_t s = (cudaStream_t)o.stream;
+        const size_t xb = sizeof(float) * (size_t)n_cols * F, yb = sizeof(float) * (size_t)n * F;
+        int32_t* rp = dalloc<int32_t>(n + 1, s);
+        int32_t* ci = dalloc<int32_t>(nnz, s);
+        float* va = dalloc<float>(nnz, s);
+        float* x = dalloc<float>((size_t)n_cols * F, s);
+        float* y = dalloc<float>((size_t)n * F, s);
+        float* y2 = layers > 1 ? dalloc<float>((size_t)n * F, s) : nullptr;
+        agcn_plan_s* plan = nullptr;
+        try {
+            // colidx_h / vals_h are indexed by rowptr values: copy the [rowptr[0], rowptr[n]) run
+            const int32_t base = rowptr_h[0];
+            AGCN_CUDA(cudaMemcpyAsync(rp, rowptr_h, sizeof(int32_t) * (n + 1), cudaMemcpyHostToDevice, s));
+            if (nnz) {
+                AGCN_CUDA(cudaMemcpyAsync(ci, colidx_h + base, sizeof(int32_t) * nnz, cudaMemcpyHostToDevice, s));
+                AGCN_CUDA(cudaMemcpyAsync(va, vals_h + base, sizeof(float) * nnz, cudaMemcpyHostToDevice, s));
+            }
+            AGCN_CUDA(cudaMemcpyAsync(x, X_h, xb, cudaMemcpyHostToDevice, s));
+            plan = build_plan(rp, ci - base, n, nnz, o);
+            const float* cur = x;
+            float* out = y;
+            for (int l = 0; l < layers; ++l) {
+                spmm_launch(plan, va - base, cur, F, out, s);
+                cur = out;
+                out = (out == y) ? y2 : y;
+            }
+            AGCN_CUDA(cudaMemcpyAsync(Y_h, cur, yb, cudaMemcpyDeviceToHost, s));
+            AGCN_CUDA(cudaStreamSynchronize(s));
+        } catch (...) {
+            cudaStreamSynchronize(s);
+            if (plan) { free_plan_arrays(plan); delete plan; }
+            dfree(rp, s); dfree(ci, s); dfree(va, s); dfree(x, s); dfree(y, s); dfree(y2, s);
+            cudaStreamSynchronize(s);
+            throw;
+        }
+        free_plan_arrays(plan);
+        delete plan;
+        dfree(rp, s); dfree(ci, s); dfree(va, s); dfree(x, s); dfree(y, s); dfree(y2, s);
+        AGCN_CUDA(cudaStreamSynchronize(s));
+    });
+}
+
+agcn_status_t agcn_last_status(void) { return agcn::last_status(); }
+const char* agcn_last_error(void) { return agcn::last_message(); }
+uint64_t agcn_launch_count(void) { return agcn::g_launches.load(); }
+const char* agcn_version(void) { return "agcn 0.1 sm_100a (Accel-GCN arXiv 2308.11825)"; }
+
+}  // extern "C"

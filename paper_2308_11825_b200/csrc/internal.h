@@ -1,0 +1,114 @@
+// internal.h -- shared declarations of the agcn CUDA library (not part of the C ABI).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <atomic>
+#include <string>
+
+#include "../../include/agcn.h"
+
+namespace agcn {
+
+// ------------------------------------------------------------------ error state
+void set_error(agcn_status_t code, const std::string& msg);
+void clear_error();
+agcn_status_t last_status();
+const char* last_message();
+agcn_status_t cuda_status(cudaError_t e);  // maps OOM -> AGCN_ERR_OOM, else AGCN_ERR_CUDA
+
+struct Error {
+    agcn_status_t code;
+    std::string msg;
+};
+
+#define AGCN_CUDA(call)                                                                    \
+    do {                                                                                   \
+        cudaError_t e__ = (call);                                                          \
+        if (e__ != cudaSuccess)                                                            \
+            throw ::agcn::Error{::agcn::cuda_status(e__),                                  \
+                                std::string(#call) + ": " + cudaGetErrorString(e__)};      \
+    } while (0)
+
+#define AGCN_CHECK(cond, code, msg)                                  \
+    do {                                                             \
+        if (!(cond)) throw ::agcn::Error{(code), std::string(msg)};  \
+    } while (0)
+
+// ------------------------------------------------------------------ launch accounting
+extern std::atomic<uint64_t> g_launches;
+inline void count_launch(uint64_t k = 1) { g_launches.fetch_add(k, std::memory_order_relaxed); }
+// check the launch itself (configuration errors); never synchronises
+inline void post_launch() {
+    count_launch();
+    AGCN_CUDA(cudaGetLastError());
+}
+
+// ------------------------------------------------------------------ device buffers
+// Stream-ordered allocations (cudaMallocAsync): no device-wide synchronisation.
+template <class T>
+T* dalloc(size_t count, cudaStream_t s) {
+    void* p = nullptr;
+    if (count == 0) count = 1;
+    AGCN_CUDA(cudaMallocAsync(&p, count * sizeof(T), s));
+    return static_cast<T*>(p);
+}
+inline void dfree(void* p, cudaStream_t s) {
+    if (p) cudaFreeAsync(p, s);
+}
+
+// ------------------------------------------------------------------ scan (scan.cu)
+// out[i] = sum_{j<i} in[i] for i in [0, n]; out has n+1 entries (out[n] = total).
+// In-place (out == in) is allowed only if in has n+1 entries.  int32 values.
+void exclusive_scan_i32(const int32_t* in, int32_t* out, int64_t n, cudaStream_t s);
+
+// ------------------------------------------------------------------ plan object
+struct PlanFlags {          // device-written, read back once (validation + sizes)
+    int32_t bad_rowptr;     // rowptr decreases somewhere
+    int32_t bad_colidx;     // colidx out of [0, n_cols)
+    int32_t max_deg;
+    int32_t rowptr_first;
+    int32_t rowptr_last;
+    int32_t pad[3];
+    int64_t ov_chunks;      // sum over oversized rows of ceil(deg / deg_bound)
+};
+
+}  // namespace agcn
+
+struct agcn_plan_s {
+    int device = 0;
+    int64_t n = 0, n_cols = 0, nnz = 0;
+    int32_t mbw = 12, mwn = 32, deg_bound = 384, partition = 0;
+    int64_t x_rows = 0;  // rows of X the SpMM reads (n_cols, or the padded layout)
+    int64_t rp_base = 0; // rowptr[0] (vals/colidx are indexed by rowptr values)
+
+    // AGCN_PARTITION_BLOCK
+    int64_t nblocks = 0, nb_small = 0, n_zero = 0, n_ov = 0, ov_start = 0, ov_chunks = 0;
+    int64_t max_deg = 0;
+    int32_t* perm = nullptr;           // [n]   sorted position -> original row
+    int32_t* sorted_rowptr = nullptr;  // [n+1]
+    int32_t* sorted_colidx = nullptr;  // [nnz + 4] (padded for aligned bulk reads)
+    int32_t* row_src_off = nullptr;    // [n]
+    int4* desc = nullptr;              // [nblocks]
+    int32_t* ov_chunk_start = nullptr; // [n_ov + 1]
+
+    // AGCN_PARTITION_WARP
+    int64_t ntasks = 0;
+    int4* tasks = nullptr;             // [ntasks] (row, col, len, 0)
+    int32_t* rowptr_copy = nullptr;    // [n+1] (rebased to 0)
+    int32_t* colidx_copy = nullptr;    // [nnz]
+
+    // SpMM scratch (oversized-row partial sums, chunk-major [ov_chunks][F])
+    float* ov_partial = nullptr;
+    size_t ov_partial_floats = 0;
+
+    size_t device_bytes = 0;
+    cudaStream_t stream = nullptr;  // stream used for plan-owned allocations
+};
+
+namespace agcn {
+void spmm_launch(agcn_plan_s* p, const float* vals, const float* X, int32_t F, float* Y,
+                 cudaStream_t s);
+int num_sms();
+}  // namespace agcn

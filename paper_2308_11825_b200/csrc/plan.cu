@@ -1,0 +1,659 @@
+// plan.cu -- agcn_plan: the preprocessing of Accel-GCN section III-C on the device.
+//
+//  (1) degree of every row from the row pointer                       P:295 step (1)
+//  (2) stable counting sort of the rows by degree, ascending           P:295 step (2)
+//      - buckets 0..deg_bound exact, one bucket for degree > deg_bound;
+//        per-tile histograms -> one exclusive scan (bucket-major) -> stable scatter
+//      - the (few) oversized rows are then stably LSD-radix sorted by degree
+//  (3) row-pointer / column-index update in the new order              P:295 step (3)
+//  (4) Algorithm 1 patterns (closed form per degree)
+//  (5) Algorithm 2 block descriptors, emitted in parallel in closed form per degree
+//      bucket (equal to the sequential cursor walk), int4 {deg, loc, row, info}
+//                                                                      P:335-382
+// and, for the ablation arm, the warp-level partition of Fig. 3(b)    P:417.
+#include <algorithm>
+#include <cstring>
+#include <vector>
+
+#include "internal.h"
+
+namespace agcn {
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kWarps = kThreads / 32;
+constexpr int kSubTile = 256;                 // rows per warp per tile
+constexpr int kTile = kWarps * kSubTile;      // rows per CTA tile
+constexpr int kMaxDegBound = 2048;
+constexpr int kMaxColParts = 64;
+
+struct ColMap {                               // optional padded-layout column relabel
+    int32_t nparts;
+    int32_t slot_rows;
+    int64_t n_cols;
+    int64_t bounds[kMaxColParts + 1];
+};
+
+__device__ __forceinline__ int32_t map_col(int32_t j, const ColMap& cm, int32_t* bad) {
+    if (j < 0 || (int64_t)j >= cm.n_cols) {
+        *bad = 1;
+        return 0;
+    }
+    if (cm.nparts <= 0) return j;
+    int p = 0;
+    while (p + 1 < cm.nparts && (int64_t)j >= cm.bounds[p + 1]) ++p;
+    return (int32_t)(p * (int64_t)cm.slot_rows + (j - cm.bounds[p]));
+}
+
+__device__ __forceinline__ int32_t row_key(const int32_t* rowptr, int64_t i, int32_t db) {
+    int32_t d = rowptr[i + 1] - rowptr[i];
+    return d <= 0 ? 0 : (d <= db ? d : db + 1);
+}
+
+// ---------------------------------------------------------------- (1)+(2) histogram
+__global__ void __launch_bounds__(kThreads) k_deg_hist(const int32_t* __restrict__ rowptr, int64_t n,
+                                                      int32_t db, int32_t nbins, int64_t ntiles,
+                                                      int32_t* __restrict__ table,
+                                                      int32_t* __restrict__ bin_cnt,
+                                                      PlanFlags* __restrict__ flags) {
+    extern __shared__ int32_t hist[];
+    for (int b = threadIdx.x; b < nbins; b += kThreads) hist[b] = 0;
+    __syncthreads();
+    const int64_t lo = (int64_t)blockIdx.x * kTile, hi = min(n, lo + kTile);
+    int32_t maxd = 0, bad = 0;
+    long long ovc = 0;
+    for (int64_t i = lo + threadIdx.x; i < hi; i += kThreads) {
+        int32_t d = rowptr[i + 1] - rowptr[i];
+        if (d < 0) bad = 1;
+        int32_t key = d <= 0 ? 0 : (d <= db ? d : db + 1);
+        atomicAdd(&hist[key], 1);
+        maxd = max(maxd, d);
+        if (d > db) ovc += (d + db - 1) / db;
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        maxd = max(maxd, __shfl_xor_sync(0xffffffffu, maxd, o));
+        bad |= __shfl_xor_sync(0xffffffffu, bad, o);
+        ovc += __shfl_xor_sync(0xffffffffu, ovc, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        if (maxd) atomicMax(&flags->max_deg, maxd);
+        if (bad) flags->bad_rowptr = 1;
+        if (ovc) atomicAdd((unsigned long long*)&flags->ov_chunks, (unsigned long long)ovc);
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        flags->rowptr_first = rowptr[0];
+        flags->rowptr_last = rowptr[n];
+    }
+    __syncthreads();
+    for (int b = threadIdx.x; b < nbins; b += kThreads) {
+        int32_t c = hist[b];
+        table[(int64_t)b * ntiles + blockIdx.x] = c;
+        if (c) atomicAdd(&bin_cnt[b], c);
+    }
+}
+
+// ---------------------------------------------------------------- stable bucket scatter
+// One CTA per tile of kTile items; warp w owns items [tile*kTile + w*kSubTile, +kSubTile).
+// table_off (bucket-major, exclusive-scanned) gives the first output slot of (bucket, tile).
+// Within a tile, ranks follow item order: warp sub-tiles in order, 32-item chunks in order,
+// lanes in order (__match_any_sync groups equal keys) -> the scatter is stable.
+struct MainSrc {
+    const int32_t* rowptr;
+    int32_t db;
+    int32_t* perm;
+    __device__ __forceinline__ int32_t key(int64_t i) const { return row_key(rowptr, i, db); }
+    __device__ __forceinline__ void emit(int64_t pos, int64_t i) const { perm[pos] = (int32_t)i; }
+};
+struct RadixSrc {
+    const int32_t* keys_in;
+    const int32_t* vals_in;
+    int32_t* keys_out;
+    int32_t* vals_out;
+    int32_t shift;
+    __device__ __forceinline__ int32_t key(int64_t i) const { return (keys_in[i] >> shift) & 255; }
+    __device__ __forceinline__ void emit(int64_t pos, int64_t i) const {
+        keys_out[pos] = keys_in[i];
+        vals_out[pos] = vals_in[i];
+    }
+};
+
+template <class Src>
+__global__ void __launch_bounds__(kThreads) k_bucket_hist(Src src, int64_t m, int32_t nbins,
+                                                         int64_t ntiles, int32_t* __restrict__ table) {
+    extern __shared__ int32_t hist[];
+    for (int b = threadIdx.x; b < nbins; b += kThreads) hist[b] = 0;
+    __syncthreads();
+    const int64_t lo = (int64_t)blockIdx.x * kTile, hi = min(m, lo + kTile);
+    for (int64_t i = lo + threadIdx.x; i < hi; i += kThreads) atomicAdd(&hist[src.key(i)], 1);
+    __syncthreads();
+    for (int b = threadIdx.x; b < nbins; b += kThreads)
+        table[(int64_t)b * ntiles + blockIdx.x] = hist[b];
+}
+
+template <class Src>
+__global__ void __launch_bounds__(kThreads) k_bucket_scatter(Src src, int64_t m, int32_t nbins,
+                                                            int64_t ntiles,
+                                                            const int32_t* __restrict__ table_off) {
+    extern __shared__ int32_t h[];  // [kWarps][nbins]
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int b = threadIdx.x; b < kWarps * nbins; b += kThreads) h[b] = 0;
+    __syncthreads();
+    const int64_t lo = (int64_t)blockIdx.x * kTile + (int64_t)w * kSubTile;
+    const int64_t hi = min(m, lo + kSubTile);
+    int32_t* hw = h + w * nbins;
+    for (int64_t i = lo + lane; i < hi; i += 32) atomicAdd(&hw[src.key(i)], 1);
+    __syncthreads();
+    for (int b = threadIdx.x; b < nbins; b += kThreads) {
+        int32_t run = table_off[(int64_t)b * ntiles + blockIdx.x];
+        for (int ww = 0; ww < kWarps; ++ww) {
+            int32_t c = h[ww * nbins + b];
+            h[ww * nbins + b] = run;
+            run += c;
+        }
+    }
+    __syncthreads();
+    const unsigned lt = (1u << lane) - 1u;
+    for (int64_t c0 = lo; c0 < hi; c0 += 32) {
+        const int64_t i = c0 + lane;
+        const bool valid = i < hi;
+        const int32_t k = valid ? src.key(i) : -1;
+        const unsigned peers = __match_any_sync(0xffffffffu, k);
+        int32_t base = 0;
+        if (valid) {
+            base = hw[k];
+            src.emit((int64_t)base + __popc(peers & lt), i);
+        }
+        __syncwarp();
+        if (valid && lane == __ffs(peers) - 1) hw[k] = base + __popc(peers);
+        __syncwarp();
+    }
+}
+
+__global__ void k_ov_init(const int32_t* __restrict__ perm_ov, const int32_t* __restrict__ rowptr,
+                          int64_t m, int32_t* __restrict__ keys, int32_t* __restrict__ vals) {
+    int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k < m) {
+        int32_t r = perm_ov[k];
+        keys[k] = rowptr[r + 1] - rowptr[r];
+        vals[k] = r;
+    }
+}
+
+// ---------------------------------------------------------------- (3) sorted CSR
+__global__ void k_sorted_rows(const int32_t* __restrict__ perm, const int32_t* __restrict__ rowptr,
+                              int64_t n, int32_t* __restrict__ sdeg, int32_t* __restrict__ rso) {
+    int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k < n) {
+        int32_t r = perm[k];
+        int32_t a = rowptr[r];
+        sdeg[k] = rowptr[r + 1] - a;
+        rso[k] = a - rowptr[0];
+    }
+}
+
+// Bucket tables for degrees 1..db (index db+1 = end sentinel), in shared memory.
+struct BinTables {
+    const int32_t* nnz_start;  // first sorted nnz of bucket d
+    const int32_t* row_start;  // first sorted row of bucket d
+    const int32_t* blk_start;  // first descriptor of bucket d
+    const int32_t* cnt;        // rows of degree d
+    const int32_t* br;         // Alg. 1 block_rows of d
+    const int32_t* wn;         // Alg. 1 warp_nzs of d
+};
+
+// last d in [1, db] with a[d] <= v  (a non-decreasing on 1..db+1)
+__device__ __forceinline__ int32_t bin_search(const int32_t* a, int32_t db, int32_t v) {
+    int32_t lo = 1, hi = db + 1;  // upper_bound over [1, db+1)
+    while (lo < hi) {
+        int32_t mid = (lo + hi) >> 1;
+        if (a[mid] <= v) lo = mid + 1; else hi = mid;
+    }
+    return lo - 1;
+}
+
+// sorted_colidx for rows of degree 1..db: one thread per nonzero, bucket found by binary
+// search of the bucket nnz starts (shared memory); row = row_start + off / d.
+__global__ void __launch_bounds__(kThreads) k_gather_small(
+    int64_t nnz_small, int32_t db, const int32_t* __restrict__ g_nnz_start,
+    const int32_t* __restrict__ g_row_start, const int32_t* __restrict__ perm,
+    const int32_t* __restrict__ rowptr, const int32_t* __restrict__ colidx,
+    int32_t* __restrict__ sorted_colidx, ColMap cm, PlanFlags* __restrict__ flags) {
+    extern __shared__ int32_t sm[];
+    int32_t* nnz_start = sm;
+    int32_t* row_start = sm + db + 2;
+    for (int d = threadIdx.x; d < db + 2; d += kThreads) {
+        nnz_start[d] = g_nnz_start[d];
+        row_start[d] = g_row_start[d];
+    }
+    __syncthreads();
+    int32_t bad = 0;
+    for (int64_t q = (int64_t)blockIdx.x * kThreads + threadIdx.x; q < nnz_small;
+         q += (int64_t)gridDim.x * kThreads) {
+        int32_t d = bin_search(nnz_start, db, (int32_t)q);
+        int32_t off = (int32_t)q - nnz_start[d];
+        int32_t k = row_start[d] + off / d;
+        int32_t j = off - (off / d) * d;
+        int32_t r = perm[k];
+        sorted_colidx[q] = map_col(colidx[rowptr[r] + j], cm, &bad);
+    }
+    if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) flags->bad_colidx = 1;
+}
+
+// sorted_colidx for oversized rows: one CTA per row, strided copy.
+__global__ void __launch_bounds__(kThreads) k_gather_ov(
+    int64_t ov_start, const int32_t* __restrict__ sorted_rowptr, const int32_t* __restrict__ perm,
+    const int32_t* __restrict__ rowptr, const int32_t* __restrict__ colidx,
+    int32_t* __restrict__ sorted_colidx, ColMap cm, PlanFlags* __restrict__ flags) {
+    const int64_t k = ov_start + blockIdx.x;
+    const int32_t dst = sorted_rowptr[k], d = sorted_rowptr[k + 1] - dst;
+    const int32_t src = rowptr[perm[k]];
+    int32_t bad = 0;
+    for (int32_t j = threadIdx.x; j < d; j += kThreads)
+        sorted_colidx[dst + j] = map_col(colidx[src + j], cm, &bad);
+    if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) flags->bad_colidx = 1;
+}
+
+// ---------------------------------------------------------------- (5) Algorithm 2 emission
+// Descriptor b of the degree<=db part: bucket d = last d with blk_start[d] <= b; block i of
+// bucket d covers rows row_start[d] + i*br .. and nnz nnz_start[d] + i*br*d ..; the residual
+// block carries rows = cnt[d] - i*br (< br).  info = warp_nzs << 16 | rows.
+__global__ void __launch_bounds__(kThreads) k_emit_small(int64_t nb_small, int32_t db,
+                                                        const int32_t* __restrict__ g_tab,
+                                                        int4* __restrict__ desc) {
+    extern __shared__ int32_t sm[];
+    const int32_t W = db + 2;
+    for (int t = threadIdx.x; t < 6 * W; t += kThreads) sm[t] = g_tab[t];
+    __syncthreads();
+    const int32_t* nnz_start = sm;
+    const int32_t* row_start = sm + W;
+    const int32_t* blk_start = sm + 2 * W;
+    const int32_t* cnt = sm + 3 * W;
+    const int32_t* br = sm + 4 * W;
+    const int32_t* wn = sm + 5 * W;
+    for (int64_t b = (int64_t)blockIdx.x * kThreads + threadIdx.x; b < nb_small;
+         b += (int64_t)gridDim.x * kThreads) {
+        int32_t d = bin_search(blk_start, db, (int32_t)b);
+        int32_t i = (int32_t)b - blk_start[d];
+        int32_t rows = min(br[d], cnt[d] - i * br[d]);
+        desc[b] = make_int4(d, nnz_start[d] + i * br[d] * d, row_start[d] + i * br[d],
+                            (int32_t)(((uint32_t)wn[d] << 16) | (uint32_t)rows));
+    }
+}
+
+__global__ void k_ov_chunk_count(const int32_t* __restrict__ sorted_rowptr, int64_t ov_start,
+                                 int64_t n_ov, int32_t db, int32_t* __restrict__ out) {
+    int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k < n_ov) {
+        int32_t d = sorted_rowptr[ov_start + k + 1] - sorted_rowptr[ov_start + k];
+        out[k] = (d + db - 1) / db;
+    }
+}
+
+// Oversized row k (sorted position ov_start + k): chunk j = {deg, loc + j*db, row, min(db, deg - j*db)}
+__global__ void k_emit_ov(const int32_t* __restrict__ sorted_rowptr, int64_t ov_start, int64_t n_ov,
+                          int32_t db, int64_t nb_small, const int32_t* __restrict__ chunk_start,
+                          int4* __restrict__ desc) {
+    const int64_t k = (int64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+    if (k >= n_ov) return;
+    const int32_t row = (int32_t)(ov_start + k);
+    const int32_t loc = sorted_rowptr[row], d = sorted_rowptr[row + 1] - loc;
+    const int32_t c0 = chunk_start[k], nc = chunk_start[k + 1] - c0;
+    for (int32_t j = threadIdx.x & 31; j < nc; j += 32)
+        desc[nb_small + c0 + j] = make_int4(d, loc + j * db, row, min(db, d - j * db));
+}
+
+// ---------------------------------------------------------------- warp-level partition
+__global__ void k_rowptr_check(const int32_t* __restrict__ rowptr, int64_t n, int32_t mwn,
+                               int32_t* __restrict__ rp_copy, int32_t* __restrict__ ntask,
+                               PlanFlags* __restrict__ flags) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) {
+        int32_t d = rowptr[i + 1] - rowptr[i];
+        if (d < 0) flags->bad_rowptr = 1;
+        rp_copy[i] = rowptr[i] - rowptr[0];
+        ntask[i] = d > 0 ? (d + mwn - 1) / mwn : 0;
+        atomicMax(&flags->max_deg, max(d, 0));
+    }
+    if (i == 0) {
+        flags->rowptr_first = rowptr[0];
+        flags->rowptr_last = rowptr[n];
+        rp_copy[n] = rowptr[n] - rowptr[0];
+    }
+}
+
+__global__ void k_copy_cols(const int32_t* __restrict__ colidx, int64_t nnz, int32_t* __restrict__ out,
+                            ColMap cm, PlanFlags* __restrict__ flags) {
+    int32_t bad = 0;
+    for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < nnz;
+         q += (int64_t)gridDim.x * blockDim.x)
+        out[q] = map_col(colidx[q], cm, &bad);
+    if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) flags->bad_colidx = 1;
+}
+
+// Fig. 3(b): row i -> tasks {i, c, min(mwn, d - c), 0} for c = 0, mwn, 2 mwn, ...
+__global__ void k_emit_tasks(const int32_t* __restrict__ rp, int64_t n, int32_t mwn,
+                             const int32_t* __restrict__ tstart, int4* __restrict__ tasks) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    int32_t d = rp[i + 1] - rp[i];
+    int32_t t = tstart[i];
+    for (int32_t c = 0; c < d; c += mwn) tasks[t++] = make_int4((int32_t)i, c, min(mwn, d - c), 0);
+}
+
+inline unsigned blocks_for(int64_t n, int t) { return (unsigned)std::max<int64_t>(1, (n + t - 1) / t); }
+
+// Library-side Algorithm 1 in closed form: smallest factor f of mbw with f*mwn >= d,
+// block_rows = mbw / f, warp_nzs = ceil(d / f).
+void host_patterns(int32_t mbw, int32_t mwn, std::vector<int32_t>& br, std::vector<int32_t>& wn) {
+    const int32_t db = mbw * mwn;
+    br.assign(db + 2, 0);
+    wn.assign(db + 2, 0);
+    for (int32_t d = 1; d <= db; ++d) {
+        int32_t f = 1;
+        while (!(mbw % f == 0 && (int64_t)f * mwn >= d)) ++f;
+        br[d] = mbw / f;
+        wn[d] = (d + f - 1) / f;
+    }
+}
+
+ColMap make_colmap(const agcn_opts_t& o, int64_t n_cols) {
+    ColMap cm{};
+    cm.n_cols = n_cols;
+    cm.nparts = o.col_nparts;
+    cm.slot_rows = (int32_t)o.col_slot_rows;
+    if (o.col_nparts > 0) {
+        AGCN_CHECK(o.col_nparts <= kMaxColParts && o.col_bounds != nullptr,
+                   AGCN_ERR_INVALID_ARG, "col_nparts > 64 or col_bounds == NULL");
+        AGCN_CHECK(o.col_slot_rows > 0 && (int64_t)o.col_nparts * o.col_slot_rows < (1ll << 31),
+                   AGCN_ERR_INVALID_ARG, "bad col_slot_rows");
+        AGCN_CHECK(o.col_bounds[0] == 0 && o.col_bounds[o.col_nparts] == n_cols, AGCN_ERR_INVALID_ARG,
+                   "col_bounds must span [0, n_cols]");
+        for (int p = 0; p <= o.col_nparts; ++p) cm.bounds[p] = o.col_bounds[p];
+        for (int p = 0; p < o.col_nparts; ++p)
+            AGCN_CHECK(o.col_bounds[p + 1] >= o.col_bounds[p] &&
+                           o.col_bounds[p + 1] - o.col_bounds[p] <= o.col_slot_rows,
+                       AGCN_ERR_INVALID_ARG, "col_bounds not monotone or slot too small");
+    }
+    return cm;
+}
+
+void read_flags(PlanFlags* d_flags, PlanFlags* h, cudaStream_t s) {
+    AGCN_CUDA(cudaMemcpyAsync(h, d_flags, sizeof(PlanFlags), cudaMemcpyDeviceToHost, s));
+    AGCN_CUDA(cudaStreamSynchronize(s));
+}
+
+void check_csr_flags(const PlanFlags& f, int64_t nnz) {
+    AGCN_CHECK(!f.bad_rowptr, AGCN_ERR_BAD_CSR, "rowptr is not non-decreasing");
+    AGCN_CHECK((int64_t)f.rowptr_last - f.rowptr_first == nnz, AGCN_ERR_BAD_CSR,
+               "rowptr[n] - rowptr[0] != nnz");
+}
+
+// ---------------------------------------------------------------- block-partition plan
+void build_block_plan(agcn_plan_s* p, const int32_t* rowptr, const int32_t* colidx,
+                      const agcn_opts_t& o, cudaStream_t s) {
+    const int64_t n = p->n, nnz = p->nnz;
+    const int32_t db = p->deg_bound, nbins = db + 2;
+    const int64_t ntiles = std::max<int64_t>(1, (n + kTile - 1) / kTile);
+    ColMap cm = make_colmap(o, p->n_cols);
+
+    PlanFlags* d_flags = dalloc<PlanFlags>(1, s);
+    int32_t* bin_cnt = dalloc<int32_t>(nbins, s);
+    int32_t* table = dalloc<int32_t>((size_t)nbins * ntiles + 1, s);
+    AGCN_CUDA(cudaMemsetAsync(d_flags, 0, sizeof(PlanFlags), s));
+    AGCN_CUDA(cudaMemsetAsync(bin_cnt, 0, sizeof(int32_t) * nbins, s));
+
+    // (1)+(2a) per-tile bucket histograms, bucket totals, max degree, validation
+    k_deg_hist<<<(unsigned)ntiles, kThreads, nbins * sizeof(int32_t), s>>>(rowptr, n, db, nbins, ntiles,
+                                                                         table, bin_cnt, d_flags);
+    post_launch();
+    exclusive_scan_i32(table, table, (int64_t)nbins * ntiles, s);
+
+    std::vector<int32_t> h_cnt(nbins);
+    PlanFlags hf{};
+    AGCN_CUDA(cudaMemcpyAsync(h_cnt.data(), bin_cnt, sizeof(int32_t) * nbins, cudaMemcpyDeviceToHost, s));
+    read_flags(d_flags, &hf, s);  // the plan's one mid-course synchronisation
+    check_csr_flags(hf, nnz);
+    p->rp_base = hf.rowptr_first;
+
+    // host-side bucket bookkeeping (tiny: deg_bound + 2 entries)
+    std::vector<int32_t> br, wn;
+    host_patterns(p->mbw, p->mwn, br, wn);
+    const int32_t W = db + 2;
+    std::vector<int32_t> tab(6 * W, 0);
+    int32_t* nnz_start = tab.data();
+    int32_t* row_start = tab.data() + W;
+    int32_t* blk_start = tab.data() + 2 * W;
+    int32_t* cntv = tab.data() + 3 * W;
+    int32_t* brv = tab.data() + 4 * W;
+    int32_t* wnv = tab.data() + 5 * W;
+    int64_t row = h_cnt[0], loc = 0, blk = 0;
+    for (int32_t d = 1; d <= db + 1; ++d) {
+        nnz_start[d] = (int32_t)loc;
+        row_start[d] = (int32_t)row;
+        blk_start[d] = (int32_t)blk;
+        if (d <= db) {
+            cntv[d] = h_cnt[d];
+            brv[d] = br[d];
+            wnv[d] = wn[d];
+            row += h_cnt[d];
+            loc += (int64_t)h_cnt[d] * d;
+            blk += (h_cnt[d] + br[d] - 1) / br[d];
+        }
+    }
+    p->n_zero = h_cnt[0];
+    p->n_ov = h_cnt[db + 1];
+    p->ov_start = n - p->n_ov;
+    p->ov_chunks = hf.ov_chunks;
+    p->max_deg = hf.max_deg;
+    p->nb_small = blk;
+    p->nblocks = blk + hf.ov_chunks;
+    const int64_t nnz_small = loc;
+    AGCN_CHECK(p->nblocks < (1ll << 31), AGCN_ERR_OVERFLOW, "too many descriptors");
+
+    // plan-owned arrays
+    p->perm = dalloc<int32_t>(n, s);
+    p->sorted_rowptr = dalloc<int32_t>(n + 1, s);
+    p->sorted_colidx = dalloc<int32_t>(nnz + 4, s);
+    p->row_src_off = dalloc<int32_t>(n, s);
+    p->desc = dalloc<int4>(p->nblocks, s);
+    p->ov_chunk_start = dalloc<int32_t>(p->n_ov + 1, s);
+    p->device_bytes = sizeof(int32_t) * (size_t)(3 * n + 1 + nnz + 4 + p->n_ov + 1) +
+                      sizeof(int4) * (size_t)p->nblocks;
+    AGCN_CUDA(cudaMemsetAsync(p->sorted_colidx + nnz, 0, 4 * sizeof(int32_t), s));
+
+    // (2b) stable scatter into bucket order
+    const size_t scat_smem = (size_t)kWarps * nbins * sizeof(int32_t);
+    if (scat_smem > 48 * 1024)
+        AGCN_CUDA(cudaFuncSetAttribute(k_bucket_scatter<MainSrc>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)scat_smem));
+    k_bucket_scatter<MainSrc><<<(unsigned)ntiles, kThreads, scat_smem, s>>>(
+        MainSrc{rowptr, db, p->perm}, n, nbins, ntiles, table);
+    post_launch();
+
+    // (2c) oversized rows (degree > deg_bound) keep row order within the bucket; stable LSD
+    // radix sort of that bucket by degree (8-bit digits) completes the ascending stable order.
+    const int64_t m = p->n_ov;
+    if (m > 1) {
+        int passes = 0;
+        for (int64_t v = p->max_deg; v > 0; v >>= 8) ++passes;
+        const int64_t mt = (m + kTile - 1) / kTile;
+        int32_t* ka = dalloc<int32_t>(m, s);
+        int32_t* va = dalloc<int32_t>(m, s);
+        int32_t* kb = dalloc<int32_t>(m, s);
+        int32_t* vb = dalloc<int32_t>(m, s);
+        int32_t* rt = dalloc<int32_t>(256 * mt + 1, s);
+        k_ov_init<<<blocks_for(m, 256), 256, 0, s>>>(p->perm + p->ov_start, rowptr, m, ka, va);
+        post_launch();
+        for (int pass = 0; pass < passes; ++pass) {
+            RadixSrc src{ka, va, kb, vb, 8 * pass};
+            k_bucket_hist<RadixSrc><<<(unsigned)mt, kThreads, 256 * sizeof(int32_t), s>>>(src, m, 256, mt, rt);
+            post_launch();
+            exclusive_scan_i32(rt, rt, 256 * mt, s);
+            k_bucket_scatter<RadixSrc><<<(unsigned)mt, kThreads, kWarps * 256 * sizeof(int32_t), s>>>(
+                src, m, 256, mt, rt);
+            post_launch();
+            std::swap(ka, kb);
+            std::swap(va, vb);
+        }
+        AGCN_CUDA(cudaMemcpyAsync(p->perm + p->ov_start, va, sizeof(int32_t) * m,
+                                  cudaMemcpyDeviceToDevice, s));
+        dfree(ka, s); dfree(va, s); dfree(kb, s); dfree(vb, s); dfree(rt, s);
+    }
+
+    // (3) sorted degrees -> sorted_rowptr (scan), row_src_off, sorted_colidx
+    if (n > 0) {
+        k_sorted_rows<<<blocks_for(n, 256), 256, 0, s>>>(p->perm, rowptr, n, p->sorted_rowptr,
+                                                          p->row_src_off);
+        post_launch();
+    }
+    exclusive_scan_i32(p->sorted_rowptr, p->sorted_rowptr, n, s);
+
+    int32_t* d_tab = dalloc<int32_t>(6 * W, s);
+    AGCN_CUDA(cudaMemcpyAsync(d_tab, tab.data(), sizeof(int32_t) * 6 * W, cudaMemcpyHostToDevice, s));
+    if (nnz_small > 0) {
+        unsigned g = (unsigned)std::min<int64_t>(blocks_for(nnz_small, kThreads), 148 * 16);
+        k_gather_small<<<g, kThreads, 2 * W * sizeof(int32_t), s>>>(
+            nnz_small, db, d_tab /*nnz_start*/, d_tab + W /*row_start*/, p->perm, rowptr, colidx,
+            p->sorted_colidx, cm, d_flags);
+        post_launch();
+    }
+    if (m > 0) {
+        k_gather_ov<<<(unsigned)m, kThreads, 0, s>>>(p->ov_start, p->sorted_rowptr, p->perm, rowptr,
+                                                      colidx, p->sorted_colidx, cm, d_flags);
+        post_launch();
+    }
+
+    // (4)+(5) Algorithm 1/2 descriptors
+    if (p->nb_small > 0) {
+        unsigned g = (unsigned)std::min<int64_t>(blocks_for(p->nb_small, kThreads), 148 * 8);
+        size_t smem = 6 * W * sizeof(int32_t);
+        if (smem > 48 * 1024)
+            AGCN_CUDA(cudaFuncSetAttribute(k_emit_small, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)smem));
+        k_emit_small<<<g, kThreads, smem, s>>>(p->nb_small, db, d_tab, p->desc);
+        post_launch();
+    }
+    if (m > 0) {
+        k_ov_chunk_count<<<blocks_for(m, 256), 256, 0, s>>>(p->sorted_rowptr, p->ov_start, m, db,
+                                                            p->ov_chunk_start);
+        post_launch();
+        exclusive_scan_i32(p->ov_chunk_start, p->ov_chunk_start, m, s);
+        k_emit_ov<<<blocks_for(m, kWarps), kThreads, 0, s>>>(p->sorted_rowptr, p->ov_start, m, db,
+                                                              p->nb_small, p->ov_chunk_start, p->desc);
+        post_launch();
+    } else {
+        AGCN_CUDA(cudaMemsetAsync(p->ov_chunk_start, 0, sizeof(int32_t), s));
+    }
+
+    read_flags(d_flags, &hf, s);  // completes the plan; reports colidx validation
+    AGCN_CHECK(!hf.bad_colidx, AGCN_ERR_BAD_CSR, "colidx out of [0, n_cols)");
+    dfree(d_tab, s); dfree(table, s); dfree(bin_cnt, s); dfree(d_flags, s);
+}
+
+// ---------------------------------------------------------------- warp-partition plan
+void build_warp_plan(agcn_plan_s* p, const int32_t* rowptr, const int32_t* colidx,
+                     const agcn_opts_t& o, cudaStream_t s) {
+    const int64_t n = p->n, nnz = p->nnz;
+    ColMap cm = make_colmap(o, p->n_cols);
+    PlanFlags* d_flags = dalloc<PlanFlags>(1, s);
+    AGCN_CUDA(cudaMemsetAsync(d_flags, 0, sizeof(PlanFlags), s));
+    p->rowptr_copy = dalloc<int32_t>(n + 1, s);
+    int32_t* tstart = dalloc<int32_t>(n + 1, s);
+    k_rowptr_check<<<blocks_for(n + 1, 256), 256, 0, s>>>(rowptr, n, p->mwn, p->rowptr_copy, tstart,
+                                                          d_flags);
+    post_launch();
+    exclusive_scan_i32(tstart, tstart, n, s);
+    int32_t ntasks = 0;
+    AGCN_CUDA(cudaMemcpyAsync(&ntasks, tstart + n, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    PlanFlags hf{};
+    read_flags(d_flags, &hf, s);
+    check_csr_flags(hf, nnz);
+    p->ntasks = ntasks;
+    p->max_deg = hf.max_deg;
+    p->rp_base = hf.rowptr_first;
+    p->colidx_copy = dalloc<int32_t>(nnz, s);
+    p->tasks = dalloc<int4>(ntasks, s);
+    p->device_bytes = sizeof(int32_t) * (size_t)(n + 1 + nnz) + sizeof(int4) * (size_t)ntasks;
+    if (nnz > 0) {
+        k_copy_cols<<<(unsigned)std::min<int64_t>(blocks_for(nnz, 256), 148 * 16), 256, 0, s>>>(
+            colidx + p->rp_base, nnz, p->colidx_copy, cm, d_flags);
+        post_launch();
+    }
+    if (n > 0) {
+        k_emit_tasks<<<blocks_for(n, 256), 256, 0, s>>>(p->rowptr_copy, n, p->mwn, tstart, p->tasks);
+        post_launch();
+    }
+    read_flags(d_flags, &hf, s);
+    AGCN_CHECK(!hf.bad_colidx, AGCN_ERR_BAD_CSR, "colidx out of [0, n_cols)");
+    dfree(tstart, s); dfree(d_flags, s);
+}
+
+}  // namespace
+
+void free_plan_arrays(agcn_plan_s* p) {
+    void* ptrs[] = {p->perm,  p->sorted_rowptr, p->sorted_colidx, p->row_src_off, p->desc,
+                    p->ov_chunk_start, p->tasks, p->rowptr_copy, p->colidx_copy, p->ov_partial};
+    for (void* q : ptrs)
+        if (q) cudaFreeAsync(q, nullptr);  // stream-ordered allocations; legacy stream orders all
+    cudaStreamSynchronize(nullptr);
+}
+
+// Keep freed stream-ordered memory cached in the device pool (plans are rebuilt often).
+static void keep_pool_cached(int dev) {
+    static bool done[64] = {};
+    if (dev < 0 || dev >= 64 || done[dev]) return;
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t thr = ~0ull;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    done[dev] = true;
+}
+
+agcn_plan_s* build_plan(const int32_t* rowptr, const int32_t* colidx, int64_t n, int64_t nnz,
+                        const agcn_opts_t& o) {
+    AGCN_CHECK(n >= 0 && nnz >= 0, AGCN_ERR_INVALID_ARG, "n and nnz must be >= 0");
+    AGCN_CHECK(nnz < (1ll << 31) && n < (1ll << 31) - 1, AGCN_ERR_INVALID_ARG, "n, nnz must be < 2^31");
+    AGCN_CHECK(rowptr != nullptr, AGCN_ERR_INVALID_ARG, "rowptr is NULL");
+    AGCN_CHECK(colidx != nullptr || nnz == 0, AGCN_ERR_INVALID_ARG, "colidx is NULL");
+    AGCN_CHECK(o.max_block_warps >= 1 && o.max_warp_nzs >= 1, AGCN_ERR_INVALID_ARG,
+               "max_block_warps and max_warp_nzs must be >= 1");
+    AGCN_CHECK(o.max_block_warps < 65536 && o.max_warp_nzs < 65536, AGCN_ERR_OVERFLOW,
+               "block_rows / warp_nzs must fit the 16-bit info halves");
+    AGCN_CHECK((int64_t)o.max_block_warps * o.max_warp_nzs <= kMaxDegBound, AGCN_ERR_UNSUPPORTED,
+               "deg_bound = max_block_warps * max_warp_nzs must be <= 2048 in this build");
+    AGCN_CHECK(o.partition == AGCN_PARTITION_BLOCK || o.partition == AGCN_PARTITION_WARP,
+               AGCN_ERR_INVALID_ARG, "unknown partition");
+    const int64_t n_cols = o.n_cols > 0 ? o.n_cols : n;
+    AGCN_CHECK(n_cols < (1ll << 31), AGCN_ERR_INVALID_ARG, "n_cols must be < 2^31");
+    cudaStream_t s = (cudaStream_t)o.stream;
+
+    agcn_plan_s* p = new agcn_plan_s();
+    AGCN_CUDA(cudaGetDevice(&p->device));
+    keep_pool_cached(p->device);
+    p->n = n;
+    p->n_cols = n_cols;
+    p->nnz = nnz;
+    p->mbw = o.max_block_warps;
+    p->mwn = o.max_warp_nzs;
+    p->deg_bound = o.max_block_warps * o.max_warp_nzs;
+    p->partition = o.partition;
+    p->x_rows = o.col_nparts > 0 ? (int64_t)o.col_nparts * o.col_slot_rows : n_cols;
+    p->stream = s;
+    try {
+        if (o.partition == AGCN_PARTITION_BLOCK)
+            build_block_plan(p, rowptr, colidx, o, s);
+        else
+            build_warp_plan(p, rowptr, colidx, o, s);
+        AGCN_CUDA(cudaStreamSynchronize(s));
+    } catch (...) {
+        cudaStreamSynchronize(s);
+        free_plan_arrays(p);
+        delete p;
+        throw;
+    }
+    return p;
+}
+
+}  // namespace agcn

@@ -1,0 +1,523 @@
+// spmm.cu -- agcn_spmm: Y = A.X over the block-level partition (Accel-GCN section III-D).
+//
+// Mapping on sm_100a:
+//  * One 128-bit descriptor {deg, loc, row, info} is the unit of work.  A
+//    persistent grid of 8-warp CTAs walks the descriptor array; each WARP owns one
+//    descriptor at a time (the paper gives one CTA of max_block_warps warps; on B200 the
+//    block-level merge then needs no CTA barrier, see below).
+//  * Combined warp: the F columns of one X row are covered by L consecutive
+//    lanes with float4 loads (L*T float4 = the paper's round_dim, lanes past F truncated,
+//    P:493); a warp holds G = 32/L such "combined warps" (sub-warps), which split the
+//    descriptor's contiguous nonzeros evenly (per-sub-warp nnz differ by at most 4).
+//  * The descriptor's colidx (contiguous in degree-sorted order) and vals (one contiguous
+//    run per row, via row_src_off) are staged in shared memory once per descriptor.
+//  * Three-level accumulation made deterministic: (1) registers, (2) the
+//    partial rows of sub-warps that share a row are merged in fixed sub-warp order through
+//    shared memory (replaces atomicAdd_block), (3) rows with degree > deg_bound are split
+//    into chunks whose partial sums go to a scratch buffer and are summed in chunk order by
+//    a second kernel (replaces global atomics).
+//  * Rows are restored to the original order in the store: Y[perm[row]] (reading S:142-150).
+#include <algorithm>
+#include <mutex>
+
+#include "internal.h"
+
+namespace agcn {
+namespace {
+
+constexpr int kWarpsPerCta = 8;
+constexpr int kCtaThreads = kWarpsPerCta * 32;
+
+template <bool V4>
+struct VecT;
+template <>
+struct VecT<true> {
+    using T = float4;
+};
+template <>
+struct VecT<false> {
+    using T = float;
+};
+
+__device__ __forceinline__ float4 vzero4() { return make_float4(0.f, 0.f, 0.f, 0.f); }
+__device__ __forceinline__ void vzero(float4& a) { a = vzero4(); }
+__device__ __forceinline__ void vzero(float& a) { a = 0.f; }
+__device__ __forceinline__ void vfma(float4& a, float v, const float4& x) {
+    a.x = fmaf(v, x.x, a.x);
+    a.y = fmaf(v, x.y, a.y);
+    a.z = fmaf(v, x.z, a.z);
+    a.w = fmaf(v, x.w, a.w);
+}
+__device__ __forceinline__ void vfma(float& a, float v, float x) { a = fmaf(v, x, a); }
+__device__ __forceinline__ void vadd(float4& a, const float4& b) {
+    a.x += b.x;
+    a.y += b.y;
+    a.z += b.z;
+    a.w += b.w;
+}
+__device__ __forceinline__ void vadd(float& a, float b) { a += b; }
+
+// X rows: read-only path, keep in L1 (hot rows are re-read across descriptors)
+__device__ __forceinline__ float4 ldx(const float4* p) { return __ldg(p); }
+__device__ __forceinline__ float ldx(const float* p) { return __ldg(p); }
+// Y / partial stores: streaming (written once)
+__device__ __forceinline__ void sty(float4* p, const float4& v) { __stcs(p, v); }
+__device__ __forceinline__ void sty(float* p, float v) { __stcs(p, v); }
+// CSR streams: read once
+__device__ __forceinline__ int32_t ldcs_i(const int32_t* p) { return __ldcs(p); }
+__device__ __forceinline__ float ldcs_f(const float* p) { return __ldcs(p); }
+
+struct BlockArgs {
+    const int4* desc;
+    int64_t nblocks;
+    int64_t first_ov;       // descriptor index of the first oversized chunk (== nb_small)
+    int32_t db;             // deg_bound
+    int32_t stage;          // shared-memory entries per warp (>= db, multiple of 4)
+    const int32_t* scol;    // sorted colidx
+    const int32_t* srp;     // sorted rowptr
+    const int32_t* rso;     // row_src_off
+    const int32_t* perm;    // sorted -> original row
+    const float* vals;      // caller vals, already offset by rowptr[0]
+    const float* X;
+    float* Y;
+    float* ovp;             // oversized partials [ov_chunks][FV]
+    int64_t n_zero;         // sorted rows [0, n_zero) have degree 0
+    int32_t FV;             // vectors per row (F/4 on the float4 path, F otherwise)
+};
+
+template <int L, int T, bool V4, int U>
+__global__ void __launch_bounds__(kCtaThreads) k_spmm_block(const BlockArgs a) {
+    using VT = typename VecT<V4>::T;
+    constexpr int G = 32 / L;
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int s = lane / L, li = lane % L;
+    int32_t* s_col = reinterpret_cast<int32_t*>(smem) + warp * 2 * a.stage;
+    float* s_val = reinterpret_cast<float*>(s_col + a.stage);
+    VT* s_part = reinterpret_cast<VT*>(smem + (size_t)kWarpsPerCta * 2 * a.stage * 4) +
+                 warp * (G * 2 * T * L);
+    const VT* __restrict__ X = reinterpret_cast<const VT*>(a.X);
+    VT* __restrict__ Y = reinterpret_cast<VT*>(a.Y);
+    VT* __restrict__ OVP = reinterpret_cast<VT*>(a.ovp);
+    const int32_t FV = a.FV;
+    const int64_t gw = (int64_t)blockIdx.x * kWarpsPerCta + warp;
+    const int64_t W = (int64_t)gridDim.x * kWarpsPerCta;
+
+    // degree-0 rows: Y row = 0 (reading Q16)
+    for (int64_t r = gw * G + s; r < a.n_zero; r += W * G) {
+        const int64_t orow = a.perm[r];
+        VT z;
+        vzero(z);
+        for (int32_t c = li; c < FV; c += L) sty(Y + orow * FV + c, z);
+    }
+
+    for (int64_t b = gw; b < a.nblocks; b += W) {
+        const int4 m = __ldg(a.desc + b);
+        const bool ov = m.x > a.db;
+        const int32_t d = m.x, loc = m.y, row0 = m.z;
+        const int32_t total = ov ? m.w : (m.w & 0xffff) * d;
+        const int32_t seg = ov ? total : d;  // row-segment length inside the descriptor
+
+        // ---- stage colidx / vals of the descriptor in shared memory
+        __syncwarp();
+        const int32_t vbase0 = ov ? a.rso[row0] + (loc - a.srp[row0]) : 0;
+        for (int32_t e = lane; e < total; e += 32) {
+            s_col[e] = ldcs_i(a.scol + loc + e);
+            int32_t voff;
+            if (ov) {
+                voff = vbase0 + e;
+            } else {
+                const int32_t r = e / d;
+                voff = a.rso[row0 + r] + (e - r * d);
+            }
+            s_val[e] = ldcs_f(a.vals + voff);
+        }
+        __syncwarp();
+
+        // ---- even split of [0, total) over the G sub-warps (multiples of 4 entries)
+        const int32_t Q = (((total + G - 1) / G) + 3) & ~3;
+        const int32_t q0 = min(s * Q, total), q1 = min(q0 + Q, total);
+
+        for (int32_t cc = 0; cc < FV; cc += T * L) {
+            VT acc[T];
+#pragma unroll
+            for (int t = 0; t < T; ++t) vzero(acc[t]);
+            int32_t rs = (q0 / seg) * seg;  // current row segment [rs, re)
+            int32_t re = rs + seg;
+            bool fin = false;               // this sub-warp finishes a row begun earlier
+            int32_t fin_rs = 0;
+
+            auto store_row = [&](int32_t rstart, VT* v) {
+                if (ov) {
+                    VT* dst = OVP + (b - a.first_ov) * (int64_t)FV;
+#pragma unroll
+                    for (int t = 0; t < T; ++t) {
+                        const int32_t c = cc + li + t * L;
+                        if (c < FV) sty(dst + c, v[t]);
+                    }
+                } else {
+                    const int64_t orow = a.perm[row0 + rstart / seg];
+                    VT* dst = Y + orow * FV;
+#pragma unroll
+                    for (int t = 0; t < T; ++t) {
+                        const int32_t c = cc + li + t * L;
+                        if (c < FV) sty(dst + c, v[t]);
+                    }
+                }
+            };
+
+            for (int32_t q = q0; q < q1; q += U) {
+                int32_t col[U];
+                float val[U];
+                if constexpr (U == 4) {
+                    const int4 c4 = *reinterpret_cast<const int4*>(s_col + q);
+                    const float4 v4 = *reinterpret_cast<const float4*>(s_val + q);
+                    col[0] = c4.x; col[1] = c4.y; col[2] = c4.z; col[3] = c4.w;
+                    val[0] = v4.x; val[1] = v4.y; val[2] = v4.z; val[3] = v4.w;
+                } else {
+#pragma unroll
+                    for (int u = 0; u < U; ++u) {
+                        col[u] = s_col[q + u];
+                        val[u] = s_val[q + u];
+                    }
+                }
+                VT xv[U][T];
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const bool ok = q + u < q1;
+#pragma unroll
+                    for (int t = 0; t < T; ++t) {
+                        const int32_t c = cc + li + t * L;
+                        if (ok && c < FV)
+                            xv[u][t] = ldx(X + (int64_t)col[u] * FV + c);
+                        else
+                            vzero(xv[u][t]);
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    if (q + u < q1) {
+#pragma unroll
+                        for (int t = 0; t < T; ++t) vfma(acc[t], val[u], xv[u][t]);
+                        if (q + u + 1 == re) {  // row segment ends inside this range
+                            if (rs >= q0) {
+                                store_row(rs, acc);  // whole row is ours
+                            } else {                 // head partial: we finish the row
+#pragma unroll
+                                for (int t = 0; t < T; ++t) s_part[(s * 2 + 0) * T * L + t * L + li] = acc[t];
+                                fin = true;
+                                fin_rs = rs;
+                            }
+#pragma unroll
+                            for (int t = 0; t < T; ++t) vzero(acc[t]);
+                            rs = re;
+                            re += seg;
+                        }
+                    }
+                }
+            }
+            // range ended inside a row: tail partial (row began here) or middle partial
+            if (q1 > q0 && q1 > rs && q1 < re) {
+                const int slot = rs >= q0 ? 1 : 0;
+#pragma unroll
+                for (int t = 0; t < T; ++t) s_part[(s * 2 + slot) * T * L + t * L + li] = acc[t];
+            }
+            __syncwarp();
+            if (fin) {  // sum the row's partials in sub-warp order: tail, middles, own head
+                const int s_first = fin_rs / Q;
+                VT sum[T];
+#pragma unroll
+                for (int t = 0; t < T; ++t) sum[t] = s_part[(s_first * 2 + 1) * T * L + t * L + li];
+                for (int s2 = s_first + 1; s2 <= s; ++s2) {
+#pragma unroll
+                    for (int t = 0; t < T; ++t) vadd(sum[t], s_part[(s2 * 2 + 0) * T * L + t * L + li]);
+                }
+                store_row(fin_rs, sum);
+            }
+            __syncwarp();
+        }
+    }
+}
+
+// Level-3 merge: oversized row k gets the sum of its chunk partials in chunk order.
+template <bool V4>
+__global__ void k_ov_reduce(const float* __restrict__ ovp_f, const int32_t* __restrict__ chunk_start,
+                            const int32_t* __restrict__ perm, int64_t ov_start, int64_t n_ov,
+                            float* __restrict__ Y_f, int32_t FV) {
+    using VT = typename VecT<V4>::T;
+    const VT* ovp = reinterpret_cast<const VT*>(ovp_f);
+    VT* Y = reinterpret_cast<VT*>(Y_f);
+    const int64_t k = (int64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+    if (k >= n_ov) return;
+    const int lane = threadIdx.x & 31;
+    const int32_t c0 = chunk_start[k], c1 = chunk_start[k + 1];
+    const int64_t orow = perm[ov_start + k];
+    for (int32_t c = lane; c < FV; c += 32) {
+        VT acc;
+        vzero(acc);
+        int32_t j = c0;
+        for (; j + 4 <= c1; j += 4) {
+            VT x0 = ovp[(int64_t)j * FV + c], x1 = ovp[(int64_t)(j + 1) * FV + c];
+            VT x2 = ovp[(int64_t)(j + 2) * FV + c], x3 = ovp[(int64_t)(j + 3) * FV + c];
+            vadd(acc, x0);
+            vadd(acc, x1);
+            vadd(acc, x2);
+            vadd(acc, x3);
+        }
+        for (; j < c1; ++j) vadd(acc, ovp[(int64_t)j * FV + c]);
+        sty(Y + orow * FV + c, acc);
+    }
+}
+
+// ---------------------------------------------------------------- ablation arm (Fig. 3(b))
+struct WarpArgs {
+    const int4* tasks;
+    int64_t ntasks;
+    const int32_t* rp;      // rowptr rebased to 0
+    const int32_t* ci;      // colidx copy (rebased)
+    const float* vals;      // caller vals offset by rowptr[0]
+    const float* X;
+    float* Y;               // zeroed before the launch
+    int32_t FV;
+};
+
+__device__ __forceinline__ void vatomic(float4* p, const float4& v) { atomicAdd(p, v); }
+__device__ __forceinline__ void vatomic(float* p, float v) { atomicAdd(p, v); }
+
+// One warp-level task {row, col, len} per combined warp (sub-warp of L lanes); rows that
+// span several tasks are merged with global atomics (GNNAdvisor-style).
+template <int L, int T, bool V4, int U>
+__global__ void __launch_bounds__(kCtaThreads) k_spmm_warp(const WarpArgs a) {
+    using VT = typename VecT<V4>::T;
+    constexpr int G = 32 / L;
+    const int lane = threadIdx.x & 31, s = lane / L, li = lane % L;
+    const VT* __restrict__ X = reinterpret_cast<const VT*>(a.X);
+    VT* __restrict__ Y = reinterpret_cast<VT*>(a.Y);
+    const int64_t gs = ((int64_t)blockIdx.x * kWarpsPerCta + (threadIdx.x >> 5)) * G + s;
+    const int64_t S = (int64_t)gridDim.x * kWarpsPerCta * G;
+    const int32_t FV = a.FV;
+    for (int64_t t = gs; t < a.ntasks; t += S) {
+        const int4 task = __ldg(a.tasks + t);
+        const int32_t row = task.x, len = task.z;
+        const int32_t start = a.rp[row] + task.y;
+        const bool whole = len == a.rp[row + 1] - a.rp[row];
+        for (int32_t cc = 0; cc < FV; cc += T * L) {
+            VT acc[T];
+#pragma unroll
+            for (int i = 0; i < T; ++i) vzero(acc[i]);
+            for (int32_t q = 0; q < len; q += U) {
+                int32_t col[U];
+                float val[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const bool ok = q + u < len;
+                    col[u] = ok ? __ldg(a.ci + start + q + u) : 0;
+                    val[u] = ok ? __ldg(a.vals + start + q + u) : 0.f;
+                }
+                VT xv[U][T];
+#pragma unroll
+                for (int u = 0; u < U; ++u)
+#pragma unroll
+                    for (int i = 0; i < T; ++i) {
+                        const int32_t c = cc + li + i * L;
+                        if (q + u < len && c < FV)
+                            xv[u][i] = ldx(X + (int64_t)col[u] * FV + c);
+                        else
+                            vzero(xv[u][i]);
+                    }
+#pragma unroll
+                for (int u = 0; u < U; ++u)
+#pragma unroll
+                    for (int i = 0; i < T; ++i) vfma(acc[i], val[u], xv[u][i]);
+            }
+#pragma unroll
+            for (int i = 0; i < T; ++i) {
+                const int32_t c = cc + li + i * L;
+                if (c < FV) {
+                    if (whole)
+                        sty(Y + (int64_t)row * FV + c, acc[i]);
+                    else
+                        vatomic(Y + (int64_t)row * FV + c, acc[i]);
+                }
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------- dispatch
+struct Shape {
+    int L, T;
+};
+
+// Combined-warp shape: L lanes (power of two) x T vectors per lane cover FV vectors in one
+// pass if FV <= 128 (fewest lane slots, then fewest vectors per lane); wider rows loop over
+// column chunks of 32 x 4 vectors.
+Shape pick_shape(int32_t FV) {
+    if (FV > 128) return {32, 4};
+    Shape best{32, 4};
+    int best_slots = 1 << 30;
+    for (int T = 1; T <= 4; ++T)
+        for (int L = 1; L <= 32; L <<= 1)
+            if (L * T >= FV) {
+                int slots = L * T;
+                if (slots < best_slots) {
+                    best_slots = slots;
+                    best = {L, T};
+                }
+                break;
+            }
+    return best;
+}
+
+int g_num_sms = 0;
+std::once_flag g_sms_once;
+
+template <int L, int T, bool V4>
+void launch_block(const BlockArgs& a, cudaStream_t s, size_t smem) {
+    constexpr int U = 4;
+    auto kern = k_spmm_block<L, T, V4, U>;
+    static int occ = -1;        // per instantiation, for the last shared-memory size
+    static size_t occ_smem = 0;
+    if (occ < 0 || occ_smem != smem) {
+        AGCN_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        AGCN_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kCtaThreads, smem));
+        if (occ < 1) occ = 1;
+        occ_smem = smem;
+    }
+    const int64_t work = std::max<int64_t>(a.nblocks, (a.n_zero + 31) / 32);
+    const int64_t want = (work + kWarpsPerCta - 1) / kWarpsPerCta;
+    const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)num_sms() * occ));
+    kern<<<(unsigned)grid, kCtaThreads, smem, s>>>(a);
+    post_launch();
+}
+
+template <int L, int T, bool V4>
+void launch_warp(const WarpArgs& a, cudaStream_t s) {
+    auto kern = k_spmm_warp<L, T, V4, 4>;
+    static int occ = -1;
+    if (occ < 0) {
+        AGCN_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kCtaThreads, 0));
+        if (occ < 1) occ = 1;
+    }
+    constexpr int G = 32 / L;
+    const int64_t want = (a.ntasks + kWarpsPerCta * G - 1) / (kWarpsPerCta * G);
+    const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)num_sms() * occ));
+    kern<<<(unsigned)grid, kCtaThreads, 0, s>>>(a);
+    post_launch();
+}
+
+#define AGCN_DISPATCH_LT(SHAPE, FN, ...)                                             \
+    do {                                                                             \
+        switch ((SHAPE).L * 8 + (SHAPE).T) {                                         \
+            case 1 * 8 + 1: FN<1, 1>(__VA_ARGS__); break;                            \
+            case 1 * 8 + 2: FN<1, 2>(__VA_ARGS__); break;                            \
+            case 1 * 8 + 3: FN<1, 3>(__VA_ARGS__); break;                            \
+            case 1 * 8 + 4: FN<1, 4>(__VA_ARGS__); break;                            \
+            case 2 * 8 + 1: FN<2, 1>(__VA_ARGS__); break;                            \
+            case 2 * 8 + 2: FN<2, 2>(__VA_ARGS__); break;                            \
+            case 2 * 8 + 3: FN<2, 3>(__VA_ARGS__); break;                            \
+            case 2 * 8 + 4: FN<2, 4>(__VA_ARGS__); break;                            \
+            case 4 * 8 + 1: FN<4, 1>(__VA_ARGS__); break;                            \
+            case 4 * 8 + 2: FN<4, 2>(__VA_ARGS__); break;                            \
+            case 4 * 8 + 3: FN<4, 3>(__VA_ARGS__); break;                            \
+            case 4 * 8 + 4: FN<4, 4>(__VA_ARGS__); break;                            \
+            case 8 * 8 + 1: FN<8, 1>(__VA_ARGS__); break;                            \
+            case 8 * 8 + 2: FN<8, 2>(__VA_ARGS__); break;                            \
+            case 8 * 8 + 3: FN<8, 3>(__VA_ARGS__); break;                            \
+            case 8 * 8 + 4: FN<8, 4>(__VA_ARGS__); break;                            \
+            case 16 * 8 + 1: FN<16, 1>(__VA_ARGS__); break;                          \
+            case 16 * 8 + 2: FN<16, 2>(__VA_ARGS__); break;                          \
+            case 16 * 8 + 3: FN<16, 3>(__VA_ARGS__); break;                          \
+            case 16 * 8 + 4: FN<16, 4>(__VA_ARGS__); break;                          \
+            case 32 * 8 + 1: FN<32, 1>(__VA_ARGS__); break;                          \
+            case 32 * 8 + 2: FN<32, 2>(__VA_ARGS__); break;                          \
+            case 32 * 8 + 3: FN<32, 3>(__VA_ARGS__); break;                          \
+            case 32 * 8 + 4: FN<32, 4>(__VA_ARGS__); break;                          \
+            default: throw Error{AGCN_ERR_CUDA, "internal: bad combined-warp shape"}; \
+        }                                                                            \
+    } while (0)
+
+template <int L, int T>
+void block_v4(const BlockArgs& a, cudaStream_t s, size_t smem) { launch_block<L, T, true>(a, s, smem); }
+template <int L, int T>
+void block_v1(const BlockArgs& a, cudaStream_t s, size_t smem) { launch_block<L, T, false>(a, s, smem); }
+template <int L, int T>
+void warp_v4(const WarpArgs& a, cudaStream_t s) { launch_warp<L, T, true>(a, s); }
+template <int L, int T>
+void warp_v1(const WarpArgs& a, cudaStream_t s) { launch_warp<L, T, false>(a, s); }
+
+inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+}  // namespace
+
+int num_sms() {
+    std::call_once(g_sms_once, [] {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+        if (g_num_sms <= 0) g_num_sms = 148;
+    });
+    return g_num_sms;
+}
+
+void spmm_launch(agcn_plan_s* p, const float* vals, const float* X, int32_t F, float* Y,
+                 cudaStream_t s) {
+    if (p->n == 0) return;
+    const bool v4 = (F % 4 == 0) && aligned16(X) && aligned16(Y);
+    const int32_t FV = v4 ? F / 4 : F;
+    const Shape sh = pick_shape(FV);
+    if (p->partition == AGCN_PARTITION_WARP) {
+        AGCN_CUDA(cudaMemsetAsync(Y, 0, sizeof(float) * (size_t)p->n * F, s));
+        if (p->ntasks == 0) return;
+        WarpArgs a{p->tasks, p->ntasks, p->rowptr_copy, p->colidx_copy, vals + p->rp_base, X, Y, FV};
+        if (v4)
+            AGCN_DISPATCH_LT(sh, warp_v4, a, s);
+        else
+            AGCN_DISPATCH_LT(sh, warp_v1, a, s);
+        return;
+    }
+    // oversized-row partial buffer (grows, stream-ordered)
+    const size_t need = (size_t)p->ov_chunks * (size_t)F;
+    if (need > p->ov_partial_floats) {
+        if (p->ov_partial) AGCN_CUDA(cudaFreeAsync(p->ov_partial, s));
+        p->ov_partial = nullptr;
+        p->ov_partial_floats = 0;
+        AGCN_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p->ov_partial), need * sizeof(float), s));
+        p->ov_partial_floats = need;
+    }
+    BlockArgs a;
+    a.desc = p->desc;
+    a.nblocks = p->nblocks;
+    a.first_ov = p->nb_small;
+    a.db = p->deg_bound;
+    a.stage = (p->deg_bound + 3) & ~3;
+    a.scol = p->sorted_colidx;
+    a.srp = p->sorted_rowptr;
+    a.rso = p->row_src_off;
+    a.perm = p->perm;
+    a.vals = vals + p->rp_base;
+    a.X = X;
+    a.Y = Y;
+    a.ovp = p->ov_partial;
+    a.n_zero = p->n_zero;
+    a.FV = FV;
+    const size_t elt = v4 ? sizeof(float4) : sizeof(float);
+    const size_t smem = (size_t)kWarpsPerCta * (2 * a.stage * 4 + 64 * sh.T * elt);
+    if (v4)
+        AGCN_DISPATCH_LT(sh, block_v4, a, s, smem);
+    else
+        AGCN_DISPATCH_LT(sh, block_v1, a, s, smem);
+    if (p->n_ov > 0) {
+        const int64_t wpc = 8;
+        const unsigned grid = (unsigned)((p->n_ov + wpc - 1) / wpc);
+        if (v4)
+            k_ov_reduce<true><<<grid, 32 * wpc, 0, s>>>(p->ov_partial, p->ov_chunk_start, p->perm,
+                                                        p->ov_start, p->n_ov, Y, FV);
+        else
+            k_ov_reduce<false><<<grid, 32 * wpc, 0, s>>>(p->ov_partial, p->ov_chunk_start, p->perm,
+                                                         p->ov_start, p->n_ov, Y, FV);
+        post_launch();
+    }
+}
+
+}  // namespace agcn

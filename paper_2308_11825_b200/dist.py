@@ -1,0 +1,96 @@
+"""Multi-GPU row sharding for stacked propagation layers (BASELINE.json north_star).
+
+A is split into contiguous row shards with balanced nnz (agcn_shard_bounds); X is
+replicated.  Rank p owns rows [b_p, b_{p+1}); its plan relabels columns into the padded
+layout j -> q*S + (j - b_q) (q = owner of j, S = max shard rows), so one in-place
+``all_gather_into_tensor`` of the S-row slots (NCCL over NVLink) IS the next layer's X.
+No other collective is on the data path.
+
+This module holds the host-side bookkeeping only; the SpMM is the C-ABI call.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+
+@dataclass
+class ShardLayout:
+    bounds: np.ndarray   # int64 [P+1]
+    rank: int
+
+    @property
+    def P(self) -> int:
+        return int(self.bounds.size - 1)
+
+    @property
+    def slot_rows(self) -> int:
+        """S = max shard rows (every rank's slot in the padded layout has S rows)."""
+        return int(np.diff(self.bounds).max()) if self.P > 0 else 0
+
+    @property
+    def lo(self) -> int:
+        return int(self.bounds[self.rank])
+
+    @property
+    def hi(self) -> int:
+        return int(self.bounds[self.rank + 1])
+
+    @property
+    def rows(self) -> int:
+        return self.hi - self.lo
+
+    @property
+    def padded_rows(self) -> int:
+        return self.P * self.slot_rows
+
+    def slot(self, buf, q: int | None = None):
+        """Rows of rank q's slot in a padded [P*S, F] buffer (default: this rank)."""
+        q = self.rank if q is None else q
+        S = self.slot_rows
+        return buf[q * S:(q + 1) * S]
+
+    def own_rows(self, buf):
+        """The rows this rank computes (first `rows` rows of its slot)."""
+        return self.slot(buf)[:self.rows]
+
+    def pad(self, X, out):
+        """Copy a full [n, F] matrix into the padded layout `out` ([P*S, F])."""
+        S = self.slot_rows
+        for q in range(self.P):
+            a, b = int(self.bounds[q]), int(self.bounds[q + 1])
+            out[q * S:q * S + (b - a)] = X[a:b]
+        return out
+
+    def unpad(self, buf):
+        """Padded [P*S, F] -> the [n, F] rows in original order (a copy)."""
+        S = self.slot_rows
+        parts = [buf[q * S:q * S + int(self.bounds[q + 1] - self.bounds[q])] for q in range(self.P)]
+        if hasattr(buf, "new_empty"):  # torch
+            import torch
+            return torch.cat(parts, 0)
+        return np.concatenate(parts, 0)
+
+    def relabel(self, colidx: np.ndarray) -> np.ndarray:
+        """Host reference of the plan's column relabel (the CUDA path does it on device)."""
+        q = np.searchsorted(self.bounds, colidx, side="right") - 1
+        return (q * self.slot_rows + (colidx - self.bounds[q])).astype(np.int64)
+
+
+def propagate(layout: ShardLayout, spmm, X0, bufs, layers: int, all_gather=None):
+    """Run `layers` propagation layers.
+
+    spmm(Xin_padded, out_rows) computes this rank's rows of A.Xin into out_rows (a view of
+    this rank's slot); all_gather(full_buf, slot_view) fills every slot (in place).
+    bufs: list of padded buffers to rotate through (>= 1, must not include X0).
+    Returns the padded buffer holding the last layer's output.
+    """
+    cur = X0
+    for layer in range(layers):
+        nxt = bufs[layer % len(bufs)]
+        spmm(cur, layout.own_rows(nxt))
+        if all_gather is not None and layout.P > 1:
+            all_gather(nxt, layout.slot(nxt))
+        cur = nxt
+    return cur

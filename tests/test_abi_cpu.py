@@ -1,0 +1,80 @@
+"""CPU-only checks of the C-ABI library: it builds for sm_100a, loads, exports every symbol
+declared in include/agcn.h, and rejects bad arguments before touching a device."""
+import ctypes
+import os
+import re
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _declared():
+    src = open(os.path.join(ROOT, "include", "agcn.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(agcn_[a-z_]+)\s*\(", src)))
+
+
+def test_header_declares_the_boundary():
+    names = _declared()
+    for want in ("agcn_plan", "agcn_spmm", "agcn_plan_ex", "agcn_plan_destroy", "agcn_plan_stats",
+                 "agcn_plan_copy", "agcn_shard_bounds", "agcn_propagate_host", "agcn_last_error"):
+        assert want in names
+
+
+def test_library_exports_every_declared_symbol():
+    from paper_2308_11825_b200 import _lib
+    L = _lib.lib()
+    out = subprocess.run(["nm", "-D", "--defined-only", L._name], capture_output=True, text=True).stdout
+    exported = set(re.findall(r" T (agcn_\w+)", out))
+    missing = [n for n in _declared() if n not in exported]
+    assert not missing, missing
+    assert set(_lib.EXPORTS) == set(_declared())
+
+
+def test_library_is_sm100a():
+    from paper_2308_11825_b200 import _lib
+    L = _lib.lib()
+    out = subprocess.run(["cuobjdump", "--list-elf", L._name], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_version_and_counter():
+    import paper_2308_11825_b200 as A
+    assert "sm_100a" in A.version()
+    assert A.launch_count() >= 0
+
+
+def test_argument_errors_without_device():
+    from paper_2308_11825_b200 import _lib
+    L = _lib.lib()
+    assert not L.agcn_plan(None, None, -1, 0)
+    assert L.agcn_last_status() == 1            # AGCN_ERR_INVALID_ARG
+    assert b"n and nnz" in L.agcn_last_error()
+    assert not L.agcn_plan(None, None, 4, 3)
+    assert L.agcn_last_status() == 1            # rowptr NULL
+    assert not L.agcn_plan(ctypes.c_void_p(16), ctypes.c_void_p(16), 4, 1 << 31)
+    assert L.agcn_last_status() == 1            # nnz >= 2^31
+    o = _lib.Opts()
+    L.agcn_default_opts(ctypes.byref(o))
+    assert (o.max_block_warps, o.max_warp_nzs, o.partition, o.validate) == (12, 32, 0, 1)
+    o.max_block_warps, o.max_warp_nzs = 64, 64                     # deg_bound 4096 > 2048
+    assert not L.agcn_plan_ex(ctypes.c_void_p(16), ctypes.c_void_p(16), 4, 4, ctypes.byref(o))
+    assert L.agcn_last_status() == 6                               # AGCN_ERR_UNSUPPORTED
+    o.max_block_warps = 70000                                      # 16-bit info half overflows
+    assert not L.agcn_plan_ex(ctypes.c_void_p(16), ctypes.c_void_p(16), 4, 4, ctypes.byref(o))
+    assert L.agcn_last_status() == 5                               # AGCN_ERR_OVERFLOW
+    assert L.agcn_spmm(None, None, None, 4, None, None) == 1
+    assert L.agcn_plan_destroy(None) == 0
+
+
+def test_product_package_does_not_import_oracle():
+    pkg = os.path.join(ROOT, "paper_2308_11825_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".h", ".cuh", ".cpp")):
+                txt = open(os.path.join(dirpath, f)).read()
+                assert not re.search(r"^\s*(import|from)\s+oracle\b", txt, re.M), f
+                assert not re.search(r"#include\s+[<\"].*oracle", txt), f
+                assert "liboracle" not in txt and "agcn_inputs" not in txt, f

@@ -1,0 +1,294 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle.
+
+Integer metadata (degree order, sorted CSR, descriptors, warp tasks, shard bounds) must be
+bit-exact.  fp32 output must satisfy |y - y_ref| <= 1e-5 * sum|a x| + 1e-7 per element
+(BASELINE.json north_star), checked by oracle.spmm_check.
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+import agcn_inputs as gen
+import oracle
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # pragma: no cover - CPU container
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_2308_11825_b200 as A  # noqa: E402
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+DEV = torch.device("cuda:0")
+
+
+def cu(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).to(DEV)
+
+
+def make_plan(rowptr, colidx, **kw):
+    return A.Plan(cu(rowptr.astype(np.int32)), cu(colidx.astype(np.int32)), **kw)
+
+
+def check_plan_vs_oracle(rowptr, colidx, mbw=12, mwn=32, n_cols=None):
+    p = make_plan(rowptr, colidx, max_block_warps=mbw, max_warp_nzs=mwn, n_cols=n_cols)
+    o = oracle.plan(rowptr, colidx, mbw, mwn)
+    assert np.array_equal(p.copy("perm"), o["perm"])
+    assert np.array_equal(p.copy("sorted_rowptr"), o["sorted_rowptr"])
+    assert np.array_equal(p.copy("row_src_off"), o["row_src_off"])
+    assert np.array_equal(p.copy("sorted_colidx"), o["sorted_colidx"])
+    assert np.array_equal(p.copy("blocks"), o["blocks"])
+    st = p.stats()
+    assert st["nblocks"] == o["blocks"].shape[0]
+    assert st["n_zero_rows"] == int((o["sorted_deg"] == 0).sum())
+    assert st["n_oversized_rows"] == int((o["sorted_deg"] > mbw * mwn).sum())
+    return p
+
+
+def check_spmm(p, rowptr, colidx, vals, X, Y=None):
+    if Y is None:
+        Y = p.spmm(cu(vals), cu(X)).cpu().numpy()
+    r = oracle.spmm_check(rowptr, colidx, vals, X, Y)
+    assert r["nfail"] == 0, r
+    return Y
+
+
+# ---------------------------------------------------------------- metadata
+def test_fig3_golden_on_gpu():
+    g = json.load(open(os.path.join(GOLD, "fig3.json")))
+    rowptr, colidx = np.array(g["rowptr"], np.int32), np.array(g["colidx"], np.int32)
+    p = make_plan(rowptr, colidx, max_block_warps=2, max_warp_nzs=2, n_cols=g["n_cols"])
+    assert p.copy("perm").tolist() == g["perm"]
+    assert p.copy("blocks").tolist() == g["blocks"]
+    w = make_plan(rowptr, colidx, max_block_warps=2, max_warp_nzs=2, n_cols=4, partition="warp")
+    t = w.copy("tasks")
+    assert t.shape[0] == g["n_warp_tasks"] and t[0].tolist() == g["warp_tasks_first"]
+
+
+@pytest.mark.parametrize("name", ["c1", "c2", "c3"])
+def test_metadata_bit_exact_configs(name):
+    w = gen.make_config(name)
+    check_plan_vs_oracle(w.rowptr, w.colidx)
+
+
+@pytest.mark.parametrize("seed", range(60))
+def test_metadata_bit_exact_random(seed):
+    rng = np.random.default_rng(seed)
+    mbw, mwn = [(1, 1), (2, 2), (12, 32), (16, 64), (3, 5), (12, 1), (4, 7)][seed % 7]
+    n = int(rng.integers(1, 3000))
+    nc = int(rng.integers(1, 3000))
+    rowptr, colidx = gen.random_csr(n, nc, seed, max_deg=int(rng.choice([8, 100, 1500, 2500])),
+                                    dup=bool(seed % 2))
+    check_plan_vs_oracle(rowptr, colidx, mbw, mwn, n_cols=nc)
+
+
+def _rows_csr(degs, n_cols, seed=0):
+    rng = np.random.default_rng(seed)
+    rowptr = np.concatenate([[0], np.cumsum(degs)]).astype(np.int32)
+    colidx = rng.integers(0, n_cols, size=int(rowptr[-1])).astype(np.int32)
+    return rowptr, colidx
+
+
+@pytest.mark.parametrize("degs", [
+    [384], [383], [385], [768], [769], [384 * 5, 1, 0, 384 * 5 + 7],   # around deg_bound
+    [0, 0, 0], [0], [70000, 3, 0, 65536, 65537],                        # zero rows, deg >= 2^16
+    [1] * 5000 + [2] * 3000 + [33] * 100,                               # many full blocks
+])
+def test_metadata_edge_cases(degs):
+    rowptr, colidx = _rows_csr(np.array(degs), 1000)
+    p = check_plan_vs_oracle(rowptr, colidx, n_cols=1000)
+    vals = gen.uniform_f32(3, colidx.size)
+    X = gen.uniform_f32(4, (1000, 64))
+    check_spmm(p, rowptr, colidx, vals, X)
+
+
+def test_empty_plans():
+    for rowptr in (np.zeros(1, np.int32), np.zeros(5, np.int32)):
+        p = make_plan(rowptr, np.zeros(0, np.int32), n_cols=3)
+        assert p.stats()["nblocks"] == 0
+        Y = p.spmm(cu(np.zeros(0, np.float32)), cu(np.ones((3, 8), np.float32))).cpu().numpy()
+        assert Y.shape == (rowptr.size - 1, 8) and not Y.any()
+
+
+def test_warp_tasks_bit_exact():
+    for seed in range(10):
+        rowptr, colidx = gen.random_csr(2000, 500, seed, max_deg=300)
+        for mwn in (1, 2, 32):
+            p = make_plan(rowptr, colidx, partition="warp", max_warp_nzs=mwn, n_cols=500)
+            assert np.array_equal(p.copy("tasks"), oracle.warp_partition(rowptr, mwn))
+
+
+# ---------------------------------------------------------------- SpMM parity
+def test_spmm_c1_all_F():
+    w = gen.make_config("c1")
+    p = make_plan(w.rowptr, w.colidx)
+    for F in range(1, 129):
+        X = w.X(F)
+        check_spmm(p, w.rowptr, w.colidx, w.vals, X)
+
+
+@pytest.mark.parametrize("F", [16, 32, 64, 128, 96, 100, 3, 256, 520])
+def test_spmm_c2_F(F):
+    w = gen.make_config("c2", vals_kind="uniform")
+    p = make_plan(w.rowptr, w.colidx)
+    check_spmm(p, w.rowptr, w.colidx, w.vals, w.X(F))
+
+
+def test_spmm_c3_both_partitions():
+    w = gen.make_config("c3")
+    X = w.X()
+    Yb = check_spmm(make_plan(w.rowptr, w.colidx), w.rowptr, w.colidx, w.vals, X)
+    Yw = check_spmm(make_plan(w.rowptr, w.colidx, partition="warp"), w.rowptr, w.colidx, w.vals, X)
+    assert Yb.shape == Yw.shape
+
+
+@pytest.mark.parametrize("seed", range(40))
+def test_spmm_random(seed):
+    rng = np.random.default_rng(100 + seed)
+    mbw, mwn = [(12, 32), (2, 2), (1, 1), (16, 64), (3, 5), (6, 8)][seed % 6]
+    n, nc = int(rng.integers(1, 1500)), int(rng.integers(1, 1500))
+    F = int(rng.choice([1, 2, 4, 7, 16, 24, 33, 64, 96, 128, 200]))
+    rowptr, colidx = gen.random_csr(n, nc, seed, max_deg=int(rng.choice([10, 400, 1400])),
+                                    dup=bool(seed % 3 == 0))
+    vals = rng.uniform(-1, 1, colidx.size).astype(np.float32)
+    X = rng.uniform(-1, 1, (nc, F)).astype(np.float32)
+    part = "warp" if seed % 4 == 3 else "block"
+    p = make_plan(rowptr, colidx, max_block_warps=mbw, max_warp_nzs=mwn, n_cols=nc, partition=part)
+    check_spmm(p, rowptr, colidx, vals, X)
+
+
+def test_spmm_integer_exact_and_deterministic():
+    rng = np.random.default_rng(5)
+    rowptr, colidx = _rows_csr(np.array([0, 1, 5, 40, 384, 385, 2000, 3, 900]), 300, 5)
+    vals = rng.integers(-4, 5, colidx.size).astype(np.float32)
+    X = rng.integers(-4, 5, (300, 64)).astype(np.float32)
+    p = make_plan(rowptr, colidx, n_cols=300)
+    Y1 = p.spmm(cu(vals), cu(X)).cpu().numpy()
+    Y2 = p.spmm(cu(vals), cu(X)).cpu().numpy()
+    y, _ = oracle.spmm(rowptr, colidx, vals, X)
+    assert np.array_equal(Y1.astype(np.float64), y)    # exact: |partial sums| < 2^24
+    assert np.array_equal(Y1, Y2)                      # deterministic order, bitwise
+
+
+def test_spmm_unaligned_scalar_path():
+    w = gen.make_config("c1")
+    p = make_plan(w.rowptr, w.colidx)
+    Xbig = cu(w.X(65))
+    X = Xbig[:, 1:]                                    # stride 65: not contiguous -> copy
+    Xs = torch.empty(w.n * 64 + 1, device=DEV)[1:].view(w.n, 64)   # 4-byte offset
+    Xs.copy_(X)
+    out = torch.empty(w.n * 64 + 1, device=DEV)[1:].view(w.n, 64)
+    p.spmm(cu(w.vals), Xs, out=out)
+    check_spmm(p, w.rowptr, w.colidx, w.vals, Xs.cpu().numpy(), out.cpu().numpy())
+
+
+# ---------------------------------------------------------------- full BASELINE sizes (sampled)
+def _sample_rows(rowptr, k, seed):
+    deg = np.diff(rowptr)
+    rng = np.random.default_rng(seed)
+    top = np.argsort(deg, kind="stable")[-16:]
+    zero = np.flatnonzero(deg == 0)[:8]
+    rnd = rng.choice(deg.size, size=min(k, deg.size), replace=False)
+    return np.unique(np.concatenate([top, zero, rnd])).astype(np.int64)
+
+
+@pytest.mark.parametrize("name", ["c4", "c5"])
+def test_full_size_sampled(name):
+    w = gen.make_config(name)
+    rp, ci, va = cu(w.rowptr), cu(w.colidx), cu(w.vals)
+    p = A.Plan(rp, ci)
+    o_perm = oracle.degree_sort(w.rowptr)
+    assert np.array_equal(p.copy("perm"), o_perm)
+    X = w.X()
+    Xd = cu(X)
+    rows = _sample_rows(w.rowptr, 3000, 1)
+    Y = p.spmm(va, Xd)
+    r = oracle.spmm_check(w.rowptr, w.colidx, w.vals, X, Y[cu(rows)].cpu().numpy(), rows=rows)
+    assert r["nfail"] == 0, r
+    if w.layers > 1:                                   # layer 2 on the GPU's own layer-1 output
+        Y1 = Y.cpu().numpy()
+        Y2 = p.spmm(va, Y)
+        r = oracle.spmm_check(w.rowptr, w.colidx, w.vals, Y1, Y2[cu(rows)].cpu().numpy(), rows=rows)
+        assert r["nfail"] == 0, r
+    # properties at full size: all-ones X gives row sums of vals
+    ones = torch.ones((w.n, 4), device=DEV)
+    Ys = p.spmm(va, ones).cpu().numpy()
+    rs = np.add.reduceat(w.vals.astype(np.float64), w.rowptr[:-1].clip(max=w.nnz - 1))
+    rs[np.diff(w.rowptr) == 0] = 0.0
+    s_abs = np.add.reduceat(np.abs(w.vals).astype(np.float64), w.rowptr[:-1].clip(max=w.nnz - 1))
+    s_abs[np.diff(w.rowptr) == 0] = 0.0
+    assert np.all(np.abs(Ys[:, 0] - rs) <= 1e-5 * s_abs + 1e-7)
+
+
+# ---------------------------------------------------------------- shards, relabel, host API
+def test_shard_bounds_and_sharded_plans():
+    w = gen.make_config("c3")
+    rp = cu(w.rowptr)
+    X = w.X(32)
+    Y_full, _ = oracle.spmm(w.rowptr, w.colidx, w.vals, X, with_abs=False)
+    ci, va, Xd = cu(w.colidx), cu(w.vals), cu(X)
+    for P in (1, 2, 3, 8):
+        b = A.shard_bounds(rp, P)
+        assert b.tolist() == oracle.shard_bounds(w.rowptr, P).tolist()
+        outs = []
+        for q in range(P):
+            lo, hi = int(b[q]), int(b[q + 1])
+            sub = rp[lo:hi + 1].contiguous()
+            ps = A.Plan(sub, ci, n_cols=w.n)
+            o = oracle.plan(w.rowptr[lo:hi + 1], w.colidx)
+            assert np.array_equal(ps.copy("blocks"), o["blocks"])
+            assert np.array_equal(ps.copy("row_src_off"), o["row_src_off"])
+            outs.append(ps.spmm(va, Xd).cpu().numpy())
+        Y = np.concatenate(outs)
+        r = oracle.spmm_check(w.rowptr, w.colidx, w.vals, X, Y)
+        assert r["nfail"] == 0
+
+
+def test_padded_column_relabel():
+    w = gen.make_config("c2")
+    P = 3
+    b = oracle.shard_bounds(w.rowptr, P)
+    slot = int(np.diff(b).max()) + 5
+    X = w.X(16)
+    Xpad = np.zeros((P * slot, 16), np.float32)
+    for q in range(P):
+        Xpad[q * slot:q * slot + b[q + 1] - b[q]] = X[b[q]:b[q + 1]]
+    p = A.Plan(cu(w.rowptr), cu(w.colidx), col_bounds=b, col_slot_rows=slot)
+    Y = p.spmm(cu(w.vals), cu(Xpad)).cpu().numpy()
+    check_spmm(p, w.rowptr, w.colidx, w.vals, X, Y)
+
+
+def test_propagate_host_two_layers():
+    w = gen.make_config("c3")
+    X = w.X(16)
+    Y2 = A.propagate_host(w.rowptr, w.colidx, w.vals, X, layers=2)
+    Y1 = A.propagate_host(w.rowptr, w.colidx, w.vals, X, layers=1)
+    check_spmm(A.Plan(cu(w.rowptr), cu(w.colidx)), w.rowptr, w.colidx, w.vals, X, Y1)
+    r = oracle.spmm_check(w.rowptr, w.colidx, w.vals, Y1, Y2)
+    assert r["nfail"] == 0
+
+
+def test_bad_csr_is_reported():
+    rowptr = np.array([0, 3, 2, 5], np.int32)
+    with pytest.raises(A.AgcnError) as e:
+        make_plan(rowptr, np.zeros(5, np.int32))
+    assert e.value.status == "AGCN_ERR_BAD_CSR"
+    with pytest.raises(A.AgcnError) as e:
+        make_plan(np.array([0, 1, 2], np.int32), np.array([0, 7], np.int32), n_cols=3)
+    assert e.value.status == "AGCN_ERR_BAD_CSR"
+    p = make_plan(np.array([0, 1, 2], np.int32), np.array([0, 1], np.int32))
+    X = cu(np.ones((2, 4), np.float32))
+    with pytest.raises(A.AgcnError) as e:
+        A.agcn_spmm(p, cu(np.ones(2, np.float32)), X, 4, X)
+    assert e.value.status == "AGCN_ERR_INVALID_ARG"
+
+
+def test_launch_counter_moves():
+    w = gen.make_config("c1")
+    p = make_plan(w.rowptr, w.colidx)
+    c0 = A.launch_count()
+    p.spmm(cu(w.vals), cu(w.X()))
+    assert A.launch_count() > c0
