@@ -97,9 +97,14 @@ void agcn_default_opts(agcn_opts_t* opts);
  *   colidx: DEVICE int32, entries rowptr[0] .. rowptr[n]-1 are read; 0 <= colidx < n_cols.
  *   n, nnz: rows of A and rowptr[n] - rowptr[0]; 0 <= n, 0 <= nnz < 2^31.
  * Degree order is ascending and stable (ties keep original row order); degree-0 rows come
- * first and get no descriptor.  The plan copies everything it needs: the caller may free
- * rowptr/colidx after return.  Synchronises the plan stream (reads the bucket counts and
- * the validation flag).  Limits: deg_bound = max_block_warps*max_warp_nzs <= 2048,
+ * first and get no descriptor.  Step (3) of P:295 is the O(n) row-pointer update: the plan
+ * stores the degree-sorted row pointer and, per sorted row, where its entries start in the
+ * caller's arrays; it does NOT copy colidx.  Ownership: rowptr may be freed after return;
+ * colidx is BORROWED and must stay valid and unchanged until agcn_plan_destroy (like a
+ * cuSPARSE CSR descriptor).  The AGCN_PARTITION_WARP plan copies colidx.  Synchronises the
+ * plan stream once mid-way (bucket counts, validation flags); the last kernels run
+ * asynchronously on opts.stream, and agcn_spmm on another stream waits for them (event).
+ * Limits: deg_bound = max_block_warps*max_warp_nzs <= 2048,
  * max_block_warps < 65536 and max_warp_nzs < 65536 (16-bit info halves) -> otherwise
  * AGCN_ERR_UNSUPPORTED / AGCN_ERR_OVERFLOW.  Returns NULL on error.
  */

@@ -121,6 +121,7 @@ class Plan:
         if not h:
             _raise_last()
         self._h = h
+        self._colidx = colidx  # the plan borrows colidx (read by every spmm): keep it alive
         self.partition = partition
         st = self.stats()
         self.n, self.n_cols, self.nnz = st["n"], st["n_cols"], st["nnz"]

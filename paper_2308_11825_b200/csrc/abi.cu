@@ -33,6 +33,7 @@ agcn_status_t cuda_status(cudaError_t e) {
 agcn_plan_s* build_plan(const int32_t* rowptr, const int32_t* colidx, int64_t n, int64_t nnz,
                         const agcn_opts_t& o);
 void free_plan_arrays(agcn_plan_s* p);
+void plan_copy_sorted_colidx(agcn_plan_s* p, int32_t* host_dst);
 
 namespace {
 
@@ -171,7 +172,7 @@ agcn_status_t agcn_plan_copy(agcn_plan_t plan, int32_t field, void* host_dst, si
         switch (field) {
             case AGCN_FIELD_PERM: src = plan->perm; want = 4 * (size_t)plan->n; break;
             case AGCN_FIELD_BLOCKS: src = plan->desc; want = 16 * (size_t)plan->nblocks; break;
-            case AGCN_FIELD_SORTED_COLIDX: src = plan->sorted_colidx; want = 4 * (size_t)plan->nnz; break;
+            case AGCN_FIELD_SORTED_COLIDX: src = plan->perm; want = 4 * (size_t)plan->nnz; break;
             case AGCN_FIELD_ROW_SRC_OFF: src = plan->row_src_off; want = 4 * (size_t)plan->n; break;
             case AGCN_FIELD_TASKS: src = plan->tasks; want = 16 * (size_t)plan->ntasks; break;
             case AGCN_FIELD_SORTED_ROWPTR: src = plan->sorted_rowptr; want = 4 * (size_t)(plan->n + 1); break;
@@ -181,6 +182,10 @@ agcn_status_t agcn_plan_copy(agcn_plan_t plan, int32_t field, void* host_dst, si
         AGCN_CHECK(is_task ? !blk : blk, AGCN_ERR_INVALID_ARG, "field not present for this partition");
         AGCN_CHECK(bytes == want, AGCN_ERR_INVALID_ARG,
                    "bytes must equal the field size (" + std::to_string(want) + ")");
+        if (field == AGCN_FIELD_SORTED_COLIDX) {  // not stored: materialised on demand
+            plan_copy_sorted_colidx(plan, static_cast<int32_t*>(host_dst));
+            return;
+        }
         if (want) AGCN_CUDA(cudaMemcpy(host_dst, src, want, cudaMemcpyDeviceToHost));
     });
 }

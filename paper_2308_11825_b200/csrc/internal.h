@@ -8,6 +8,7 @@
 #include <string>
 
 #include "../../include/agcn.h"
+#include "colmap.cuh"
 
 namespace agcn {
 
@@ -87,9 +88,10 @@ struct agcn_plan_s {
     int64_t nblocks = 0, nb_small = 0, n_zero = 0, n_ov = 0, ov_start = 0, ov_chunks = 0;
     int64_t max_deg = 0;
     int32_t* perm = nullptr;           // [n]   sorted position -> original row
-    int32_t* sorted_rowptr = nullptr;  // [n+1]
-    int32_t* sorted_colidx = nullptr;  // [nnz + 4] (padded for aligned bulk reads)
-    int32_t* row_src_off = nullptr;    // [n]
+    int32_t* sorted_rowptr = nullptr;  // [n+1] row pointer of the degree-sorted CSR (P:295 (3))
+    int32_t* row_src_off = nullptr;    // [n]   rowptr[perm[k]] - rowptr[0]
+    const int32_t* colidx = nullptr;   // BORROWED caller colidx (indexed by rowptr values)
+    agcn::ColMap cmap{};               // optional padded-layout column relabel
     int4* desc = nullptr;              // [nblocks]
     int32_t* ov_chunk_start = nullptr; // [n_ov + 1]
 
@@ -104,7 +106,8 @@ struct agcn_plan_s {
     size_t ov_partial_floats = 0;
 
     size_t device_bytes = 0;
-    cudaStream_t stream = nullptr;  // stream used for plan-owned allocations
+    cudaStream_t stream = nullptr;  // stream the plan was built on
+    cudaEvent_t ready = nullptr;    // recorded on `stream` when the plan is complete
 };
 
 namespace agcn {

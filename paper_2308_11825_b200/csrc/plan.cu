@@ -25,25 +25,7 @@ constexpr int kWarps = kThreads / 32;
 constexpr int kSubTile = 256;                 // rows per warp per tile
 constexpr int kTile = kWarps * kSubTile;      // rows per CTA tile
 constexpr int kMaxDegBound = 2048;
-constexpr int kMaxColParts = 64;
 
-struct ColMap {                               // optional padded-layout column relabel
-    int32_t nparts;
-    int32_t slot_rows;
-    int64_t n_cols;
-    int64_t bounds[kMaxColParts + 1];
-};
-
-__device__ __forceinline__ int32_t map_col(int32_t j, const ColMap& cm, int32_t* bad) {
-    if (j < 0 || (int64_t)j >= cm.n_cols) {
-        *bad = 1;
-        return 0;
-    }
-    if (cm.nparts <= 0) return j;
-    int p = 0;
-    while (p + 1 < cm.nparts && (int64_t)j >= cm.bounds[p + 1]) ++p;
-    return (int32_t)(p * (int64_t)cm.slot_rows + (j - cm.bounds[p]));
-}
 
 __device__ __forceinline__ int32_t row_key(const int32_t* rowptr, int64_t i, int32_t db) {
     int32_t d = rowptr[i + 1] - rowptr[i];
@@ -212,46 +194,28 @@ __device__ __forceinline__ int32_t bin_search(const int32_t* a, int32_t db, int3
     return lo - 1;
 }
 
-// sorted_colidx for rows of degree 1..db: one thread per nonzero, bucket found by binary
-// search of the bucket nnz starts (shared memory); row = row_start + off / d.
-__global__ void __launch_bounds__(kThreads) k_gather_small(
-    int64_t nnz_small, int32_t db, const int32_t* __restrict__ g_nnz_start,
-    const int32_t* __restrict__ g_row_start, const int32_t* __restrict__ perm,
-    const int32_t* __restrict__ rowptr, const int32_t* __restrict__ colidx,
-    int32_t* __restrict__ sorted_colidx, ColMap cm, PlanFlags* __restrict__ flags) {
-    extern __shared__ int32_t sm[];
-    int32_t* nnz_start = sm;
-    int32_t* row_start = sm + db + 2;
-    for (int d = threadIdx.x; d < db + 2; d += kThreads) {
-        nnz_start[d] = g_nnz_start[d];
-        row_start[d] = g_row_start[d];
-    }
-    __syncthreads();
+// Colidx validation (0 <= colidx < n_cols), one flat coalesced pass over the nonzeros.
+__global__ void k_validate_cols(const int32_t* __restrict__ colidx, int64_t nnz, int64_t n_cols,
+                                PlanFlags* __restrict__ flags) {
     int32_t bad = 0;
-    for (int64_t q = (int64_t)blockIdx.x * kThreads + threadIdx.x; q < nnz_small;
-         q += (int64_t)gridDim.x * kThreads) {
-        int32_t d = bin_search(nnz_start, db, (int32_t)q);
-        int32_t off = (int32_t)q - nnz_start[d];
-        int32_t k = row_start[d] + off / d;
-        int32_t j = off - (off / d) * d;
-        int32_t r = perm[k];
-        sorted_colidx[q] = map_col(colidx[rowptr[r] + j], cm, &bad);
+    for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < nnz;
+         q += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t j = __ldcs(colidx + q);
+        bad |= (j < 0) | ((int64_t)j >= n_cols);
     }
     if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) flags->bad_colidx = 1;
 }
 
-// sorted_colidx for oversized rows: one CTA per row, strided copy.
-__global__ void __launch_bounds__(kThreads) k_gather_ov(
-    int64_t ov_start, const int32_t* __restrict__ sorted_rowptr, const int32_t* __restrict__ perm,
-    const int32_t* __restrict__ rowptr, const int32_t* __restrict__ colidx,
-    int32_t* __restrict__ sorted_colidx, ColMap cm, PlanFlags* __restrict__ flags) {
-    const int64_t k = ov_start + blockIdx.x;
-    const int32_t dst = sorted_rowptr[k], d = sorted_rowptr[k + 1] - dst;
-    const int32_t src = rowptr[perm[k]];
-    int32_t bad = 0;
-    for (int32_t j = threadIdx.x; j < d; j += kThreads)
-        sorted_colidx[dst + j] = map_col(colidx[src + j], cm, &bad);
-    if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) flags->bad_colidx = 1;
+// Introspection only (agcn_plan_copy(AGCN_FIELD_SORTED_COLIDX)): materialise the colidx of the
+// degree-sorted CSR, one warp per sorted row.  Not on the plan / SpMM path.
+__global__ void k_gather_sorted_cols(int64_t n, const int32_t* __restrict__ sorted_rowptr,
+                                     const int32_t* __restrict__ rso,
+                                     const int32_t* __restrict__ colidx, ColMap cm,
+                                     int32_t* __restrict__ out) {
+    const int64_t k = (int64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+    if (k >= n) return;
+    const int32_t dst = sorted_rowptr[k], d = sorted_rowptr[k + 1] - dst, src = rso[k];
+    for (int32_t j = threadIdx.x & 31; j < d; j += 32) out[dst + j] = map_col(colidx[src + j], cm);
 }
 
 // ---------------------------------------------------------------- (5) Algorithm 2 emission
@@ -323,12 +287,10 @@ __global__ void k_rowptr_check(const int32_t* __restrict__ rowptr, int64_t n, in
 }
 
 __global__ void k_copy_cols(const int32_t* __restrict__ colidx, int64_t nnz, int32_t* __restrict__ out,
-                            ColMap cm, PlanFlags* __restrict__ flags) {
-    int32_t bad = 0;
+                            ColMap cm) {
     for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < nnz;
          q += (int64_t)gridDim.x * blockDim.x)
-        out[q] = map_col(colidx[q], cm, &bad);
-    if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) flags->bad_colidx = 1;
+        out[q] = map_col(colidx[q], cm);
 }
 
 // Fig. 3(b): row i -> tasks {i, c, min(mwn, d - c), 0} for c = 0, mwn, 2 mwn, ...
@@ -357,6 +319,8 @@ void host_patterns(int32_t mbw, int32_t mwn, std::vector<int32_t>& br, std::vect
     }
 }
 
+}  // namespace
+
 ColMap make_colmap(const agcn_opts_t& o, int64_t n_cols) {
     ColMap cm{};
     cm.n_cols = n_cols;
@@ -378,6 +342,8 @@ ColMap make_colmap(const agcn_opts_t& o, int64_t n_cols) {
     return cm;
 }
 
+namespace {
+
 void read_flags(PlanFlags* d_flags, PlanFlags* h, cudaStream_t s) {
     AGCN_CUDA(cudaMemcpyAsync(h, d_flags, sizeof(PlanFlags), cudaMemcpyDeviceToHost, s));
     AGCN_CUDA(cudaStreamSynchronize(s));
@@ -389,13 +355,22 @@ void check_csr_flags(const PlanFlags& f, int64_t nnz) {
                "rowptr[n] - rowptr[0] != nnz");
 }
 
+// First phase shared by both partitions: validate colidx (optional, flat pass) then read the
+// flags once.  This is the plan's only host synchronisation.
+void validate_cols(const int32_t* colidx, int64_t nnz, int64_t n_cols, PlanFlags* d_flags,
+                   cudaStream_t s) {
+    if (nnz == 0) return;
+    const unsigned g = (unsigned)std::min<int64_t>(blocks_for(nnz, 256), 148 * 16);
+    k_validate_cols<<<g, 256, 0, s>>>(colidx, nnz, n_cols, d_flags);
+    post_launch();
+}
+
 // ---------------------------------------------------------------- block-partition plan
 void build_block_plan(agcn_plan_s* p, const int32_t* rowptr, const int32_t* colidx,
                       const agcn_opts_t& o, cudaStream_t s) {
     const int64_t n = p->n, nnz = p->nnz;
     const int32_t db = p->deg_bound, nbins = db + 2;
     const int64_t ntiles = std::max<int64_t>(1, (n + kTile - 1) / kTile);
-    ColMap cm = make_colmap(o, p->n_cols);
 
     PlanFlags* d_flags = dalloc<PlanFlags>(1, s);
     int32_t* bin_cnt = dalloc<int32_t>(nbins, s);
@@ -403,17 +378,24 @@ void build_block_plan(agcn_plan_s* p, const int32_t* rowptr, const int32_t* coli
     AGCN_CUDA(cudaMemsetAsync(d_flags, 0, sizeof(PlanFlags), s));
     AGCN_CUDA(cudaMemsetAsync(bin_cnt, 0, sizeof(int32_t) * nbins, s));
 
-    // (1)+(2a) per-tile bucket histograms, bucket totals, max degree, validation
+    // (1)+(2a) per-tile bucket histograms, bucket totals, max degree, rowptr validation
     k_deg_hist<<<(unsigned)ntiles, kThreads, nbins * sizeof(int32_t), s>>>(rowptr, n, db, nbins, ntiles,
                                                                          table, bin_cnt, d_flags);
     post_launch();
+    if (o.validate) {
+        int32_t first = 0;  // colidx is indexed by rowptr values; the run starts at rowptr[0]
+        AGCN_CUDA(cudaMemcpyAsync(&first, rowptr, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+        AGCN_CUDA(cudaStreamSynchronize(s));
+        validate_cols(colidx + first, nnz, p->n_cols, d_flags, s);
+    }
     exclusive_scan_i32(table, table, (int64_t)nbins * ntiles, s);
 
     std::vector<int32_t> h_cnt(nbins);
     PlanFlags hf{};
     AGCN_CUDA(cudaMemcpyAsync(h_cnt.data(), bin_cnt, sizeof(int32_t) * nbins, cudaMemcpyDeviceToHost, s));
-    read_flags(d_flags, &hf, s);  // the plan's one mid-course synchronisation
+    read_flags(d_flags, &hf, s);  // the plan's mid-course synchronisation (bucket counts)
     check_csr_flags(hf, nnz);
+    AGCN_CHECK(!hf.bad_colidx, AGCN_ERR_BAD_CSR, "colidx out of [0, n_cols)");
     p->rp_base = hf.rowptr_first;
 
     // host-side bucket bookkeeping (tiny: deg_bound + 2 entries)
@@ -448,19 +430,16 @@ void build_block_plan(agcn_plan_s* p, const int32_t* rowptr, const int32_t* coli
     p->max_deg = hf.max_deg;
     p->nb_small = blk;
     p->nblocks = blk + hf.ov_chunks;
-    const int64_t nnz_small = loc;
     AGCN_CHECK(p->nblocks < (1ll << 31), AGCN_ERR_OVERFLOW, "too many descriptors");
 
-    // plan-owned arrays
+    // plan-owned arrays (colidx is borrowed: the SpMM reads it through row_src_off)
     p->perm = dalloc<int32_t>(n, s);
     p->sorted_rowptr = dalloc<int32_t>(n + 1, s);
-    p->sorted_colidx = dalloc<int32_t>(nnz + 4, s);
     p->row_src_off = dalloc<int32_t>(n, s);
     p->desc = dalloc<int4>(p->nblocks, s);
     p->ov_chunk_start = dalloc<int32_t>(p->n_ov + 1, s);
-    p->device_bytes = sizeof(int32_t) * (size_t)(3 * n + 1 + nnz + 4 + p->n_ov + 1) +
+    p->device_bytes = sizeof(int32_t) * (size_t)(3 * n + 1 + p->n_ov + 1) +
                       sizeof(int4) * (size_t)p->nblocks;
-    AGCN_CUDA(cudaMemsetAsync(p->sorted_colidx + nnz, 0, 4 * sizeof(int32_t), s));
 
     // (2b) stable scatter into bucket order
     const size_t scat_smem = (size_t)kWarps * nbins * sizeof(int32_t);
@@ -501,7 +480,9 @@ void build_block_plan(agcn_plan_s* p, const int32_t* rowptr, const int32_t* coli
         dfree(ka, s); dfree(va, s); dfree(kb, s); dfree(vb, s); dfree(rt, s);
     }
 
-    // (3) sorted degrees -> sorted_rowptr (scan), row_src_off, sorted_colidx
+    // (3) "updating the row pointer array to reflect the new row order", O(n):
+    // sorted degrees -> sorted_rowptr (scan) and row_src_off (where each sorted row starts in
+    // the caller's colidx / vals).  Column indices are not copied.
     if (n > 0) {
         k_sorted_rows<<<blocks_for(n, 256), 256, 0, s>>>(p->perm, rowptr, n, p->sorted_rowptr,
                                                           p->row_src_off);
@@ -509,22 +490,9 @@ void build_block_plan(agcn_plan_s* p, const int32_t* rowptr, const int32_t* coli
     }
     exclusive_scan_i32(p->sorted_rowptr, p->sorted_rowptr, n, s);
 
+    // (4)+(5) Algorithm 1/2 descriptors
     int32_t* d_tab = dalloc<int32_t>(6 * W, s);
     AGCN_CUDA(cudaMemcpyAsync(d_tab, tab.data(), sizeof(int32_t) * 6 * W, cudaMemcpyHostToDevice, s));
-    if (nnz_small > 0) {
-        unsigned g = (unsigned)std::min<int64_t>(blocks_for(nnz_small, kThreads), 148 * 16);
-        k_gather_small<<<g, kThreads, 2 * W * sizeof(int32_t), s>>>(
-            nnz_small, db, d_tab /*nnz_start*/, d_tab + W /*row_start*/, p->perm, rowptr, colidx,
-            p->sorted_colidx, cm, d_flags);
-        post_launch();
-    }
-    if (m > 0) {
-        k_gather_ov<<<(unsigned)m, kThreads, 0, s>>>(p->ov_start, p->sorted_rowptr, p->perm, rowptr,
-                                                      colidx, p->sorted_colidx, cm, d_flags);
-        post_launch();
-    }
-
-    // (4)+(5) Algorithm 1/2 descriptors
     if (p->nb_small > 0) {
         unsigned g = (unsigned)std::min<int64_t>(blocks_for(p->nb_small, kThreads), 148 * 8);
         size_t smem = 6 * W * sizeof(int32_t);
@@ -545,9 +513,6 @@ void build_block_plan(agcn_plan_s* p, const int32_t* rowptr, const int32_t* coli
     } else {
         AGCN_CUDA(cudaMemsetAsync(p->ov_chunk_start, 0, sizeof(int32_t), s));
     }
-
-    read_flags(d_flags, &hf, s);  // completes the plan; reports colidx validation
-    AGCN_CHECK(!hf.bad_colidx, AGCN_ERR_BAD_CSR, "colidx out of [0, n_cols)");
     dfree(d_tab, s); dfree(table, s); dfree(bin_cnt, s); dfree(d_flags, s);
 }
 
@@ -555,7 +520,6 @@ void build_block_plan(agcn_plan_s* p, const int32_t* rowptr, const int32_t* coli
 void build_warp_plan(agcn_plan_s* p, const int32_t* rowptr, const int32_t* colidx,
                      const agcn_opts_t& o, cudaStream_t s) {
     const int64_t n = p->n, nnz = p->nnz;
-    ColMap cm = make_colmap(o, p->n_cols);
     PlanFlags* d_flags = dalloc<PlanFlags>(1, s);
     AGCN_CUDA(cudaMemsetAsync(d_flags, 0, sizeof(PlanFlags), s));
     p->rowptr_copy = dalloc<int32_t>(n + 1, s);
@@ -563,12 +527,17 @@ void build_warp_plan(agcn_plan_s* p, const int32_t* rowptr, const int32_t* colid
     k_rowptr_check<<<blocks_for(n + 1, 256), 256, 0, s>>>(rowptr, n, p->mwn, p->rowptr_copy, tstart,
                                                           d_flags);
     post_launch();
+    int32_t first = 0;
+    AGCN_CUDA(cudaMemcpyAsync(&first, rowptr, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    AGCN_CUDA(cudaStreamSynchronize(s));
+    if (o.validate) validate_cols(colidx + first, nnz, p->n_cols, d_flags, s);
     exclusive_scan_i32(tstart, tstart, n, s);
     int32_t ntasks = 0;
     AGCN_CUDA(cudaMemcpyAsync(&ntasks, tstart + n, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
     PlanFlags hf{};
     read_flags(d_flags, &hf, s);
     check_csr_flags(hf, nnz);
+    AGCN_CHECK(!hf.bad_colidx, AGCN_ERR_BAD_CSR, "colidx out of [0, n_cols)");
     p->ntasks = ntasks;
     p->max_deg = hf.max_deg;
     p->rp_base = hf.rowptr_first;
@@ -577,26 +546,40 @@ void build_warp_plan(agcn_plan_s* p, const int32_t* rowptr, const int32_t* colid
     p->device_bytes = sizeof(int32_t) * (size_t)(n + 1 + nnz) + sizeof(int4) * (size_t)ntasks;
     if (nnz > 0) {
         k_copy_cols<<<(unsigned)std::min<int64_t>(blocks_for(nnz, 256), 148 * 16), 256, 0, s>>>(
-            colidx + p->rp_base, nnz, p->colidx_copy, cm, d_flags);
+            colidx + p->rp_base, nnz, p->colidx_copy, p->cmap);
         post_launch();
     }
     if (n > 0) {
         k_emit_tasks<<<blocks_for(n, 256), 256, 0, s>>>(p->rowptr_copy, n, p->mwn, tstart, p->tasks);
         post_launch();
     }
-    read_flags(d_flags, &hf, s);
-    AGCN_CHECK(!hf.bad_colidx, AGCN_ERR_BAD_CSR, "colidx out of [0, n_cols)");
     dfree(tstart, s); dfree(d_flags, s);
 }
 
 }  // namespace
 
 void free_plan_arrays(agcn_plan_s* p) {
-    void* ptrs[] = {p->perm,  p->sorted_rowptr, p->sorted_colidx, p->row_src_off, p->desc,
-                    p->ov_chunk_start, p->tasks, p->rowptr_copy, p->colidx_copy, p->ov_partial};
+    void* ptrs[] = {p->perm, p->sorted_rowptr, p->row_src_off, p->desc, p->ov_chunk_start,
+                    p->tasks, p->rowptr_copy, p->colidx_copy, p->ov_partial};
     for (void* q : ptrs)
         if (q) cudaFreeAsync(q, nullptr);  // stream-ordered allocations; legacy stream orders all
+    if (p->ready) cudaEventDestroy(p->ready);
     cudaStreamSynchronize(nullptr);
+}
+
+// Materialise the degree-sorted colidx (introspection for parity tests; not on the path).
+void plan_copy_sorted_colidx(agcn_plan_s* p, int32_t* host_dst) {
+    if (p->nnz == 0) return;
+    cudaStream_t s = p->stream;
+    int32_t* d = dalloc<int32_t>(p->nnz, s);
+    if (p->n > 0) {
+        k_gather_sorted_cols<<<blocks_for(p->n, kWarps), kThreads, 0, s>>>(
+            p->n, p->sorted_rowptr, p->row_src_off, p->colidx + p->rp_base, p->cmap, d);
+        post_launch();
+    }
+    AGCN_CUDA(cudaMemcpyAsync(host_dst, d, sizeof(int32_t) * p->nnz, cudaMemcpyDeviceToHost, s));
+    dfree(d, s);
+    AGCN_CUDA(cudaStreamSynchronize(s));
 }
 
 // Keep freed stream-ordered memory cached in the device pool (plans are rebuilt often).
@@ -630,23 +613,26 @@ agcn_plan_s* build_plan(const int32_t* rowptr, const int32_t* colidx, int64_t n,
     cudaStream_t s = (cudaStream_t)o.stream;
 
     agcn_plan_s* p = new agcn_plan_s();
-    AGCN_CUDA(cudaGetDevice(&p->device));
-    keep_pool_cached(p->device);
-    p->n = n;
-    p->n_cols = n_cols;
-    p->nnz = nnz;
-    p->mbw = o.max_block_warps;
-    p->mwn = o.max_warp_nzs;
-    p->deg_bound = o.max_block_warps * o.max_warp_nzs;
-    p->partition = o.partition;
-    p->x_rows = o.col_nparts > 0 ? (int64_t)o.col_nparts * o.col_slot_rows : n_cols;
-    p->stream = s;
     try {
+        p->cmap = make_colmap(o, n_cols);
+        AGCN_CUDA(cudaGetDevice(&p->device));
+        keep_pool_cached(p->device);
+        p->n = n;
+        p->n_cols = n_cols;
+        p->nnz = nnz;
+        p->mbw = o.max_block_warps;
+        p->mwn = o.max_warp_nzs;
+        p->deg_bound = o.max_block_warps * o.max_warp_nzs;
+        p->partition = o.partition;
+        p->x_rows = o.col_nparts > 0 ? (int64_t)o.col_nparts * o.col_slot_rows : n_cols;
+        p->stream = s;
+        p->colidx = colidx;
         if (o.partition == AGCN_PARTITION_BLOCK)
             build_block_plan(p, rowptr, colidx, o, s);
         else
             build_warp_plan(p, rowptr, colidx, o, s);
-        AGCN_CUDA(cudaStreamSynchronize(s));
+        AGCN_CUDA(cudaEventCreateWithFlags(&p->ready, cudaEventDisableTiming));
+        AGCN_CUDA(cudaEventRecord(p->ready, s));
     } catch (...) {
         cudaStreamSynchronize(s);
         free_plan_arrays(p);

@@ -18,6 +18,7 @@
 //    a second kernel (replaces global atomics).
 //  * Rows are restored to the original order in the store: Y[perm[row]] (reading S:142-150).
 #include <algorithm>
+#include <cstdlib>
 #include <mutex>
 
 #include "internal.h"
@@ -57,13 +58,22 @@ __device__ __forceinline__ void vadd(float4& a, const float4& b) {
 }
 __device__ __forceinline__ void vadd(float& a, float b) { a += b; }
 
-// X rows: read-only path, keep in L1 (hot rows are re-read across descriptors)
-__device__ __forceinline__ float4 ldx(const float4* p) { return __ldg(p); }
-__device__ __forceinline__ float ldx(const float* p) { return __ldg(p); }
+// X rows: read-only, no L1 allocation (C5 L1 hit rate was 4 %: the gather streams through L2)
+__device__ __forceinline__ float4 ldx(const float4* p) {
+    float4 v;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0, %1, %2, %3}, [%4];"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ float ldx(const float* p) {
+    float v;
+    asm volatile("ld.global.nc.L1::no_allocate.f32 %0, [%1];" : "=f"(v) : "l"(p));
+    return v;
+}
 // Y / partial stores: streaming (written once)
 __device__ __forceinline__ void sty(float4* p, const float4& v) { __stcs(p, v); }
 __device__ __forceinline__ void sty(float* p, float v) { __stcs(p, v); }
-// CSR streams: read once
+// CSR streams: read once (evict-first)
 __device__ __forceinline__ int32_t ldcs_i(const int32_t* p) { return __ldcs(p); }
 __device__ __forceinline__ float ldcs_f(const float* p) { return __ldcs(p); }
 
@@ -72,8 +82,9 @@ struct BlockArgs {
     int64_t nblocks;
     int64_t first_ov;       // descriptor index of the first oversized chunk (== nb_small)
     int32_t db;             // deg_bound
-    int32_t stage;          // shared-memory entries per warp (>= db, multiple of 4)
-    const int32_t* scol;    // sorted colidx
+    int32_t stage;          // shared-memory entries per warp (>= db + 8, multiple of 4)
+    int32_t rso_stage;      // shared-memory row offsets per warp (>= max_block_warps)
+    const int32_t* colidx;  // caller colidx, already offset by rowptr[0] (borrowed)
     const int32_t* srp;     // sorted rowptr
     const int32_t* rso;     // row_src_off
     const int32_t* perm;    // sorted -> original row
@@ -83,18 +94,21 @@ struct BlockArgs {
     float* ovp;             // oversized partials [ov_chunks][FV]
     int64_t n_zero;         // sorted rows [0, n_zero) have degree 0
     int32_t FV;             // vectors per row (F/4 on the float4 path, F otherwise)
+    ColMap cmap;            // padded-layout column relabel (nparts == 0: identity)
 };
 
 template <int L, int T, bool V4, int U>
-__global__ void __launch_bounds__(kCtaThreads) k_spmm_block(const BlockArgs a) {
+__global__ void __launch_bounds__(kCtaThreads, 4) k_spmm_block(const __grid_constant__ BlockArgs a) {
     using VT = typename VecT<V4>::T;
     constexpr int G = 32 / L;
+    static_assert(U % 4 == 0, "U must be a multiple of 4 (LDS.128 of staged colidx / vals)");
     extern __shared__ __align__(16) unsigned char smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int s = lane / L, li = lane % L;
-    int32_t* s_col = reinterpret_cast<int32_t*>(smem) + warp * 2 * a.stage;
+    int32_t* s_col = reinterpret_cast<int32_t*>(smem) + warp * (2 * a.stage + a.rso_stage);
     float* s_val = reinterpret_cast<float*>(s_col + a.stage);
-    VT* s_part = reinterpret_cast<VT*>(smem + (size_t)kWarpsPerCta * 2 * a.stage * 4) +
+    int32_t* s_rso = s_col + 2 * a.stage;
+    VT* s_part = reinterpret_cast<VT*>(smem + (size_t)kWarpsPerCta * (2 * a.stage + a.rso_stage) * 4) +
                  warp * (G * 2 * T * L);
     const VT* __restrict__ X = reinterpret_cast<const VT*>(a.X);
     VT* __restrict__ Y = reinterpret_cast<VT*>(a.Y);
@@ -111,26 +125,37 @@ __global__ void __launch_bounds__(kCtaThreads) k_spmm_block(const BlockArgs a) {
         for (int32_t c = li; c < FV; c += L) sty(Y + orow * FV + c, z);
     }
 
+    int4 m_next = gw < a.nblocks ? __ldg(a.desc + gw) : make_int4(0, 0, 0, 0);
     for (int64_t b = gw; b < a.nblocks; b += W) {
-        const int4 m = __ldg(a.desc + b);
+        const int4 m = m_next;
+        if (b + W < a.nblocks) m_next = __ldg(a.desc + b + W);  // prefetch the next descriptor
         const bool ov = m.x > a.db;
         const int32_t d = m.x, loc = m.y, row0 = m.z;
-        const int32_t total = ov ? m.w : (m.w & 0xffff) * d;
+        const int32_t R = ov ? 1 : (m.w & 0xffff);
+        const int32_t total = ov ? m.w : R * d;
         const int32_t seg = ov ? total : d;  // row-segment length inside the descriptor
 
-        // ---- stage colidx / vals of the descriptor in shared memory
+        // ---- stage colidx / vals of the descriptor in shared memory.  Rows are read from the
+        // caller's CSR through row_src_off (the O(n) row-pointer update of P:295 (3)).
         __syncwarp();
-        const int32_t vbase0 = ov ? a.rso[row0] + (loc - a.srp[row0]) : 0;
+        int32_t vbase0 = 0;
+        if (ov) {
+            vbase0 = __ldg(a.rso + row0) + (loc - __ldg(a.srp + row0));
+        } else {
+            for (int32_t r = lane; r < R; r += 32) s_rso[r] = __ldg(a.rso + row0 + r);
+            __syncwarp();
+        }
+#pragma unroll 4
         for (int32_t e = lane; e < total; e += 32) {
-            s_col[e] = ldcs_i(a.scol + loc + e);
-            int32_t voff;
+            int32_t off;
             if (ov) {
-                voff = vbase0 + e;
+                off = vbase0 + e;
             } else {
                 const int32_t r = e / d;
-                voff = a.rso[row0 + r] + (e - r * d);
+                off = s_rso[r] + (e - r * d);
             }
-            s_val[e] = ldcs_f(a.vals + voff);
+            s_col[e] = map_col(ldcs_i(a.colidx + off), a.cmap);
+            s_val[e] = ldcs_f(a.vals + off);
         }
         __syncwarp();
 
@@ -148,38 +173,27 @@ __global__ void __launch_bounds__(kCtaThreads) k_spmm_block(const BlockArgs a) {
             int32_t fin_rs = 0;
 
             auto store_row = [&](int32_t rstart, VT* v) {
-                if (ov) {
-                    VT* dst = OVP + (b - a.first_ov) * (int64_t)FV;
+                VT* dst;
+                if (ov)
+                    dst = OVP + (b - a.first_ov) * (int64_t)FV;
+                else
+                    dst = Y + (int64_t)a.perm[row0 + rstart / seg] * FV;
 #pragma unroll
-                    for (int t = 0; t < T; ++t) {
-                        const int32_t c = cc + li + t * L;
-                        if (c < FV) sty(dst + c, v[t]);
-                    }
-                } else {
-                    const int64_t orow = a.perm[row0 + rstart / seg];
-                    VT* dst = Y + orow * FV;
-#pragma unroll
-                    for (int t = 0; t < T; ++t) {
-                        const int32_t c = cc + li + t * L;
-                        if (c < FV) sty(dst + c, v[t]);
-                    }
+                for (int t = 0; t < T; ++t) {
+                    const int32_t c = cc + li + t * L;
+                    if (c < FV) sty(dst + c, v[t]);
                 }
             };
 
             for (int32_t q = q0; q < q1; q += U) {
                 int32_t col[U];
                 float val[U];
-                if constexpr (U == 4) {
-                    const int4 c4 = *reinterpret_cast<const int4*>(s_col + q);
-                    const float4 v4 = *reinterpret_cast<const float4*>(s_val + q);
-                    col[0] = c4.x; col[1] = c4.y; col[2] = c4.z; col[3] = c4.w;
-                    val[0] = v4.x; val[1] = v4.y; val[2] = v4.z; val[3] = v4.w;
-                } else {
 #pragma unroll
-                    for (int u = 0; u < U; ++u) {
-                        col[u] = s_col[q + u];
-                        val[u] = s_val[q + u];
-                    }
+                for (int u = 0; u < U; u += 4) {
+                    const int4 c4 = *reinterpret_cast<const int4*>(s_col + q + u);
+                    const float4 v4 = *reinterpret_cast<const float4*>(s_val + q + u);
+                    col[u] = c4.x; col[u + 1] = c4.y; col[u + 2] = c4.z; col[u + 3] = c4.w;
+                    val[u] = v4.x; val[u + 1] = v4.y; val[u + 2] = v4.z; val[u + 3] = v4.w;
                 }
                 VT xv[U][T];
 #pragma unroll
@@ -239,33 +253,48 @@ __global__ void __launch_bounds__(kCtaThreads) k_spmm_block(const BlockArgs a) {
     }
 }
 
-// Level-3 merge: oversized row k gets the sum of its chunk partials in chunk order.
+// Level-3 merge: oversized row k gets the sum of its chunk partials.  One CTA per row:
+// thread (g, c) sums chunks c0+g, c0+g+NG, ... of vector column c in order, then thread
+// (0, c) adds the NG group sums in group order -> fixed summation order (deterministic).
+constexpr int kReduceThreads = 128;
 template <bool V4>
-__global__ void k_ov_reduce(const float* __restrict__ ovp_f, const int32_t* __restrict__ chunk_start,
-                            const int32_t* __restrict__ perm, int64_t ov_start, int64_t n_ov,
-                            float* __restrict__ Y_f, int32_t FV) {
+__global__ void __launch_bounds__(kReduceThreads) k_ov_reduce(
+    const float* __restrict__ ovp_f, const int32_t* __restrict__ chunk_start,
+    const int32_t* __restrict__ perm, int64_t ov_start, float* __restrict__ Y_f, int32_t FV) {
     using VT = typename VecT<V4>::T;
+    __shared__ VT part[kReduceThreads];
     const VT* ovp = reinterpret_cast<const VT*>(ovp_f);
     VT* Y = reinterpret_cast<VT*>(Y_f);
-    const int64_t k = (int64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
-    if (k >= n_ov) return;
-    const int lane = threadIdx.x & 31;
+    const int64_t k = blockIdx.x;
     const int32_t c0 = chunk_start[k], c1 = chunk_start[k + 1];
     const int64_t orow = perm[ov_start + k];
-    for (int32_t c = lane; c < FV; c += 32) {
+    const int FVc = FV < kReduceThreads ? FV : kReduceThreads;   // columns per pass
+    const int NG = kReduceThreads / FVc;                         // chunk groups
+    const int g = threadIdx.x / FVc, cl = threadIdx.x % FVc;
+    for (int32_t cb = 0; cb < FV; cb += FVc) {
+        const int32_t c = cb + cl;
         VT acc;
         vzero(acc);
-        int32_t j = c0;
-        for (; j + 4 <= c1; j += 4) {
-            VT x0 = ovp[(int64_t)j * FV + c], x1 = ovp[(int64_t)(j + 1) * FV + c];
-            VT x2 = ovp[(int64_t)(j + 2) * FV + c], x3 = ovp[(int64_t)(j + 3) * FV + c];
-            vadd(acc, x0);
-            vadd(acc, x1);
-            vadd(acc, x2);
-            vadd(acc, x3);
+        if (g < NG && c < FV) {
+            int32_t j = c0 + g;
+            for (; j + 3 * NG < c1; j += 4 * NG) {
+                VT x0 = ovp[(int64_t)j * FV + c], x1 = ovp[(int64_t)(j + NG) * FV + c];
+                VT x2 = ovp[(int64_t)(j + 2 * NG) * FV + c], x3 = ovp[(int64_t)(j + 3 * NG) * FV + c];
+                vadd(acc, x0);
+                vadd(acc, x1);
+                vadd(acc, x2);
+                vadd(acc, x3);
+            }
+            for (; j < c1; j += NG) vadd(acc, ovp[(int64_t)j * FV + c]);
         }
-        for (; j < c1; ++j) vadd(acc, ovp[(int64_t)j * FV + c]);
-        sty(Y + orow * FV + c, acc);
+        part[threadIdx.x] = acc;
+        __syncthreads();
+        if (g == 0 && c < FV) {
+            VT sum = part[cl];
+            for (int gg = 1; gg < NG; ++gg) vadd(sum, part[gg * FVc + cl]);
+            sty(Y + orow * FV + c, sum);
+        }
+        __syncthreads();
     }
 }
 
@@ -372,14 +401,19 @@ Shape pick_shape(int32_t FV) {
 int g_num_sms = 0;
 std::once_flag g_sms_once;
 
-template <int L, int T, bool V4>
-void launch_block(const BlockArgs& a, cudaStream_t s, size_t smem) {
-    constexpr int U = 4;
+int env_int(const char* name, int dflt) {
+    const char* v = getenv(name);
+    return v ? atoi(v) : dflt;
+}
+
+template <int L, int T, bool V4, int U>
+void launch_block_u(const BlockArgs& a, cudaStream_t s, size_t smem) {
     auto kern = k_spmm_block<L, T, V4, U>;
     static int occ = -1;        // per instantiation, for the last shared-memory size
     static size_t occ_smem = 0;
     if (occ < 0 || occ_smem != smem) {
         AGCN_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        AGCN_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
         AGCN_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kCtaThreads, smem));
         if (occ < 1) occ = 1;
         occ_smem = smem;
@@ -389,6 +423,16 @@ void launch_block(const BlockArgs& a, cudaStream_t s, size_t smem) {
     const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)num_sms() * occ));
     kern<<<(unsigned)grid, kCtaThreads, smem, s>>>(a);
     post_launch();
+}
+
+// X-row loads in flight per lane: 8 for one vector per lane (T == 1), else 4 (register budget).
+template <int L, int T, bool V4>
+void launch_block(const BlockArgs& a, cudaStream_t s, size_t smem) {
+    static const int u_env = env_int("AGCN_SPMM_U", 8);
+    if (T == 1 && u_env == 8)
+        launch_block_u<L, T, V4, 8>(a, s, smem);
+    else
+        launch_block_u<L, T, V4, 4>(a, s, smem);
 }
 
 template <int L, int T, bool V4>
@@ -463,6 +507,7 @@ int num_sms() {
 void spmm_launch(agcn_plan_s* p, const float* vals, const float* X, int32_t F, float* Y,
                  cudaStream_t s) {
     if (p->n == 0) return;
+    if (s != p->stream) AGCN_CUDA(cudaStreamWaitEvent(s, p->ready, 0));  // plan built on another stream
     const bool v4 = (F % 4 == 0) && aligned16(X) && aligned16(Y);
     const int32_t FV = v4 ? F / 4 : F;
     const Shape sh = pick_shape(FV);
@@ -490,8 +535,10 @@ void spmm_launch(agcn_plan_s* p, const float* vals, const float* X, int32_t F, f
     a.nblocks = p->nblocks;
     a.first_ov = p->nb_small;
     a.db = p->deg_bound;
-    a.stage = (p->deg_bound + 3) & ~3;
-    a.scol = p->sorted_colidx;
+    a.stage = ((p->deg_bound + 3) & ~3) + 8;
+    a.rso_stage = (p->mbw + 3) & ~3;
+    a.colidx = p->colidx + p->rp_base;
+    a.cmap = p->cmap;
     a.srp = p->sorted_rowptr;
     a.rso = p->row_src_off;
     a.perm = p->perm;
@@ -502,20 +549,19 @@ void spmm_launch(agcn_plan_s* p, const float* vals, const float* X, int32_t F, f
     a.n_zero = p->n_zero;
     a.FV = FV;
     const size_t elt = v4 ? sizeof(float4) : sizeof(float);
-    const size_t smem = (size_t)kWarpsPerCta * (2 * a.stage * 4 + 64 * sh.T * elt);
+    const size_t smem = (size_t)kWarpsPerCta * ((2 * a.stage + a.rso_stage) * 4 + 64 * sh.T * elt);
     if (v4)
         AGCN_DISPATCH_LT(sh, block_v4, a, s, smem);
     else
         AGCN_DISPATCH_LT(sh, block_v1, a, s, smem);
     if (p->n_ov > 0) {
-        const int64_t wpc = 8;
-        const unsigned grid = (unsigned)((p->n_ov + wpc - 1) / wpc);
+        const unsigned grid = (unsigned)p->n_ov;
         if (v4)
-            k_ov_reduce<true><<<grid, 32 * wpc, 0, s>>>(p->ov_partial, p->ov_chunk_start, p->perm,
-                                                        p->ov_start, p->n_ov, Y, FV);
+            k_ov_reduce<true><<<grid, kReduceThreads, 0, s>>>(p->ov_partial, p->ov_chunk_start, p->perm,
+                                                              p->ov_start, Y, FV);
         else
-            k_ov_reduce<false><<<grid, 32 * wpc, 0, s>>>(p->ov_partial, p->ov_chunk_start, p->perm,
-                                                         p->ov_start, p->n_ov, Y, FV);
+            k_ov_reduce<false><<<grid, kReduceThreads, 0, s>>>(p->ov_partial, p->ov_chunk_start,
+                                                               p->perm, p->ov_start, Y, FV);
         post_launch();
     }
 }

@@ -1,0 +1,31 @@
+#!/bin/bash
+# One gpurun session: build, smoke, GPU tests, bench, ncu launch list + full capture.
+# usage: tools/gpu_run.sh TAG [stages...]   stages: smoke tests bench ncu_list ncu_full
+TAG=${1:-r01}; shift
+STAGES=${*:-"smoke tests bench ncu_list ncu_full"}
+cd "${GRAFT_REPO_ROOT:-$(dirname "$0")/..}"
+OUT=gpurun_out/$TAG
+mkdir -p "$OUT"
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,clocks.mem,power.limit --format=csv > "$OUT/nvsmi.txt" 2>&1
+python -c "import __graft_entry__ as g; g.build()" > "$OUT/build.log" 2>&1 || { echo BUILD FAILED; tail -30 "$OUT/build.log"; exit 1; }
+for st in $STAGES; do
+  case $st in
+    smoke) timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > "$OUT/smoke.log" 2>&1; echo "smoke rc=$?"; tail -3 "$OUT/smoke.log";;
+    tests) timeout 1500 python -m pytest tests -q -m gpu -x > "$OUT/pytest_gpu.log" 2>&1; echo "pytest rc=$?"; tail -15 "$OUT/pytest_gpu.log";;
+    quicktests) timeout 900 python -m pytest tests -q -m gpu -x -k "not full_size" > "$OUT/pytest_gpu.log" 2>&1; echo "pytest rc=$?"; tail -15 "$OUT/pytest_gpu.log";;
+    bench) timeout 900 python bench.py --steps 10 --warmup 3 > "$OUT/bench_c5.log" 2>&1; echo "bench rc=$?"; tail -2 "$OUT/bench_c5.log";;
+    bench_all)
+      for c in c3 c4; do timeout 600 python bench.py --config $c --steps 10 --warmup 3 --no-cpu-baseline --no-e2e > "$OUT/bench_$c.log" 2>&1; echo "bench $c rc=$?"; tail -1 "$OUT/bench_$c.log"; done
+      for F in 16 32 64 128; do timeout 300 python bench.py --config c2 --F $F --steps 20 --warmup 3 --no-cpu-baseline --no-e2e > "$OUT/bench_c2_F$F.log" 2>&1; tail -1 "$OUT/bench_c2_F$F.log"; done
+      timeout 600 python bench.py --config c3 --partition warp --steps 10 --warmup 3 --no-cpu-baseline --no-e2e > "$OUT/bench_c3_warp.log" 2>&1; tail -1 "$OUT/bench_c3_warp.log";;
+    ncu_list)
+      timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv \
+        --log-file "$OUT/launches_c5.csv" python bench.py --profile --steps 2 --warmup 1 > "$OUT/ncu_list.log" 2>&1; echo "ncu_list rc=$?";;
+    ncu_full)
+      for c in c5 c4 c3; do
+        timeout 1200 ncu --set full --clock-control none --import-source on -k regex:k_spmm_block -s 3 -c 1 \
+          -o "$OUT/prof_$c" -f python bench.py --profile --config $c --steps 1 --warmup 1 > "$OUT/ncu_full_$c.log" 2>&1; echo "ncu_full $c rc=$?"
+      done;;
+  esac
+done
+ls -la "$OUT"
