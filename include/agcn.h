@@ -127,7 +127,9 @@ agcn_plan_t agcn_plan_ex(const int32_t* rowptr, const int32_t* colidx, int64_t n
 agcn_status_t agcn_spmm(agcn_plan_t plan, const float* vals, const float* X, int32_t F, float* Y,
                         agcn_stream_t stream);
 
-/* Release the plan's device memory (synchronises the device first).  NULL is a no-op. */
+/* Release the plan's device memory, stream-ordered on the plan's stream (after its own work
+   and after the most recent agcn_spmm issued on another stream); never synchronises the host.
+   Work on further streams must be ordered by the caller.  NULL is a no-op. */
 agcn_status_t agcn_plan_destroy(agcn_plan_t plan);
 
 /* Plan statistics (host struct, filled without device synchronisation). */

@@ -135,8 +135,7 @@ agcn_status_t agcn_plan_destroy(agcn_plan_t plan) {
         int cur = 0;
         cudaGetDevice(&cur);
         if (cur != plan->device) cudaSetDevice(plan->device);
-        cudaDeviceSynchronize();
-        free_plan_arrays(plan);
+        free_plan_arrays(plan);  // stream-ordered: no host synchronisation
         if (cur != plan->device) cudaSetDevice(cur);
         delete plan;
     });

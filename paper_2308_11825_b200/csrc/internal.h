@@ -108,6 +108,7 @@ struct agcn_plan_s {
     size_t device_bytes = 0;
     cudaStream_t stream = nullptr;  // stream the plan was built on
     cudaEvent_t ready = nullptr;    // recorded on `stream` when the plan is complete
+    cudaEvent_t last_use = nullptr; // recorded after an SpMM issued on a stream != `stream`
 };
 
 namespace agcn {

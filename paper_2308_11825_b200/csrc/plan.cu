@@ -561,10 +561,13 @@ void build_warp_plan(agcn_plan_s* p, const int32_t* rowptr, const int32_t* colid
 void free_plan_arrays(agcn_plan_s* p) {
     void* ptrs[] = {p->perm, p->sorted_rowptr, p->row_src_off, p->desc, p->ov_chunk_start,
                     p->tasks, p->rowptr_copy, p->colidx_copy, p->ov_partial};
+    // Stream-ordered release on the plan's stream, after the last SpMM that used the plan on
+    // another stream (p->last_use); no host synchronisation.
+    if (p->last_use) cudaStreamWaitEvent(p->stream, p->last_use, 0);
     for (void* q : ptrs)
-        if (q) cudaFreeAsync(q, nullptr);  // stream-ordered allocations; legacy stream orders all
+        if (q) cudaFreeAsync(q, p->stream);
     if (p->ready) cudaEventDestroy(p->ready);
-    cudaStreamSynchronize(nullptr);
+    if (p->last_use) cudaEventDestroy(p->last_use);
 }
 
 // Materialise the degree-sorted colidx (introspection for parity tests; not on the path).

@@ -27,6 +27,11 @@ namespace agcn {
 namespace {
 
 constexpr int kWarpsPerCta = 8;
+
+int env_int(const char* name, int dflt) {  // experiment switches
+    const char* v = getenv(name);
+    return v ? atoi(v) : dflt;
+}
 constexpr int kCtaThreads = kWarpsPerCta * 32;
 
 template <bool V4>
@@ -58,17 +63,43 @@ __device__ __forceinline__ void vadd(float4& a, const float4& b) {
 }
 __device__ __forceinline__ void vadd(float& a, float b) { a += b; }
 
-// X rows: read-only, no L1 allocation (C5 L1 hit rate was 4 %: the gather streams through L2)
-__device__ __forceinline__ float4 ldx(const float4* p) {
+// X-row gather loads, read-only path.  Flavour (uniform per launch):
+//   bit 0: L1::no_allocate     bit 1: L2::cache_hint with an evict_last policy
+__device__ __forceinline__ float4 ldx(const float4* p, int mode, uint64_t pol) {
     float4 v;
-    asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0, %1, %2, %3}, [%4];"
-                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p));
+    switch (mode) {
+        case 1:
+            asm("ld.global.nc.L1::no_allocate.v4.f32 {%0, %1, %2, %3}, [%4];"
+                : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p));
+            break;
+        case 2:
+            asm("ld.global.nc.L2::cache_hint.v4.f32 {%0, %1, %2, %3}, [%4], %5;"
+                : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p), "l"(pol));
+            break;
+        case 3:
+            asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.f32 {%0, %1, %2, %3}, [%4], %5;"
+                : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p), "l"(pol));
+            break;
+        default: v = __ldg(p);
+    }
     return v;
 }
-__device__ __forceinline__ float ldx(const float* p) {
+__device__ __forceinline__ float ldx(const float* p, int mode, uint64_t pol) {
     float v;
-    asm volatile("ld.global.nc.L1::no_allocate.f32 %0, [%1];" : "=f"(v) : "l"(p));
+    switch (mode) {
+        case 1: asm("ld.global.nc.L1::no_allocate.f32 %0, [%1];" : "=f"(v) : "l"(p)); break;
+        case 2: asm("ld.global.nc.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(p), "l"(pol)); break;
+        case 3:
+            asm("ld.global.nc.L1::no_allocate.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(p), "l"(pol));
+            break;
+        default: v = __ldg(p);
+    }
     return v;
+}
+__device__ __forceinline__ uint64_t policy_evict_last() {
+    uint64_t pol;
+    asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
 }
 // Y / partial stores: streaming (written once)
 __device__ __forceinline__ void sty(float4* p, const float4& v) { __stcs(p, v); }
@@ -95,6 +126,7 @@ struct BlockArgs {
     int64_t n_zero;         // sorted rows [0, n_zero) have degree 0
     int32_t FV;             // vectors per row (F/4 on the float4 path, F otherwise)
     ColMap cmap;            // padded-layout column relabel (nparts == 0: identity)
+    int32_t xmode;          // X-load flavour (see ldx)
 };
 
 template <int L, int T, bool V4, int U>
@@ -116,6 +148,8 @@ __global__ void __launch_bounds__(kCtaThreads, 4) k_spmm_block(const __grid_cons
     const int32_t FV = a.FV;
     const int64_t gw = (int64_t)blockIdx.x * kWarpsPerCta + warp;
     const int64_t W = (int64_t)gridDim.x * kWarpsPerCta;
+    const int xmode = a.xmode;
+    const uint64_t pol = policy_evict_last();
 
     // degree-0 rows: Y row = 0 (reading Q16)
     for (int64_t r = gw * G + s; r < a.n_zero; r += W * G) {
@@ -203,7 +237,7 @@ __global__ void __launch_bounds__(kCtaThreads, 4) k_spmm_block(const __grid_cons
                     for (int t = 0; t < T; ++t) {
                         const int32_t c = cc + li + t * L;
                         if (ok && c < FV)
-                            xv[u][t] = ldx(X + (int64_t)col[u] * FV + c);
+                            xv[u][t] = ldx(X + (int64_t)col[u] * FV + c, xmode, pol);
                         else
                             vzero(xv[u][t]);
                     }
@@ -350,7 +384,7 @@ __global__ void __launch_bounds__(kCtaThreads) k_spmm_warp(const WarpArgs a) {
                     for (int i = 0; i < T; ++i) {
                         const int32_t c = cc + li + i * L;
                         if (q + u < len && c < FV)
-                            xv[u][i] = ldx(X + (int64_t)col[u] * FV + c);
+                            xv[u][i] = ldx(X + (int64_t)col[u] * FV + c, 0, 0);
                         else
                             vzero(xv[u][i]);
                     }
@@ -401,11 +435,6 @@ Shape pick_shape(int32_t FV) {
 int g_num_sms = 0;
 std::once_flag g_sms_once;
 
-int env_int(const char* name, int dflt) {
-    const char* v = getenv(name);
-    return v ? atoi(v) : dflt;
-}
-
 template <int L, int T, bool V4, int U>
 void launch_block_u(const BlockArgs& a, cudaStream_t s, size_t smem) {
     auto kern = k_spmm_block<L, T, V4, U>;
@@ -413,7 +442,8 @@ void launch_block_u(const BlockArgs& a, cudaStream_t s, size_t smem) {
     static size_t occ_smem = 0;
     if (occ < 0 || occ_smem != smem) {
         AGCN_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-        AGCN_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+        static const int carve = env_int("AGCN_CARVEOUT", -1);
+        if (carve >= 0) AGCN_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, carve));
         AGCN_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kCtaThreads, smem));
         if (occ < 1) occ = 1;
         occ_smem = smem;
@@ -428,7 +458,7 @@ void launch_block_u(const BlockArgs& a, cudaStream_t s, size_t smem) {
 // X-row loads in flight per lane: 8 for one vector per lane (T == 1), else 4 (register budget).
 template <int L, int T, bool V4>
 void launch_block(const BlockArgs& a, cudaStream_t s, size_t smem) {
-    static const int u_env = env_int("AGCN_SPMM_U", 8);
+    static const int u_env = env_int("AGCN_SPMM_U", 4);
     if (T == 1 && u_env == 8)
         launch_block_u<L, T, V4, 8>(a, s, smem);
     else
@@ -507,7 +537,15 @@ int num_sms() {
 void spmm_launch(agcn_plan_s* p, const float* vals, const float* X, int32_t F, float* Y,
                  cudaStream_t s) {
     if (p->n == 0) return;
-    if (s != p->stream) AGCN_CUDA(cudaStreamWaitEvent(s, p->ready, 0));  // plan built on another stream
+    const bool foreign = s != p->stream;
+    if (foreign) {  // plan built on another stream: wait for it; remember this use for destroy
+        AGCN_CUDA(cudaStreamWaitEvent(s, p->ready, 0));
+        if (!p->last_use) AGCN_CUDA(cudaEventCreateWithFlags(&p->last_use, cudaEventDisableTiming));
+    }
+    struct Rec {  // record last_use after the launches below, on every exit path
+        agcn_plan_s* p; cudaStream_t s; bool on;
+        ~Rec() { if (on) cudaEventRecord(p->last_use, s); }
+    } rec{p, s, foreign};
     const bool v4 = (F % 4 == 0) && aligned16(X) && aligned16(Y);
     const int32_t FV = v4 ? F / 4 : F;
     const Shape sh = pick_shape(FV);
@@ -539,6 +577,8 @@ void spmm_launch(agcn_plan_s* p, const float* vals, const float* X, int32_t F, f
     a.rso_stage = (p->mbw + 3) & ~3;
     a.colidx = p->colidx + p->rp_base;
     a.cmap = p->cmap;
+    static const int xmode = env_int("AGCN_XMODE", 0);
+    a.xmode = xmode;
     a.srp = p->sorted_rowptr;
     a.rso = p->row_src_off;
     a.perm = p->perm;

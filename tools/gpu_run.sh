@@ -18,13 +18,29 @@ for st in $STAGES; do
       for c in c3 c4; do timeout 600 python bench.py --config $c --steps 10 --warmup 3 --no-cpu-baseline --no-e2e > "$OUT/bench_$c.log" 2>&1; echo "bench $c rc=$?"; tail -1 "$OUT/bench_$c.log"; done
       for F in 16 32 64 128; do timeout 300 python bench.py --config c2 --F $F --steps 20 --warmup 3 --no-cpu-baseline --no-e2e > "$OUT/bench_c2_F$F.log" 2>&1; tail -1 "$OUT/bench_c2_F$F.log"; done
       timeout 600 python bench.py --config c3 --partition warp --steps 10 --warmup 3 --no-cpu-baseline --no-e2e > "$OUT/bench_c3_warp.log" 2>&1; tail -1 "$OUT/bench_c3_warp.log";;
+    ab)  # A/B of kernel variants selected by environment (AB_VAR=values, e.g. AGCN_SPMM_U=4,8)
+      for c in ${AB_CONFIGS:-c5 c4}; do for v in ${AB_VALUES//,/ }; do
+        env ${AB_VAR}=$v timeout 600 python bench.py --config $c --steps 10 --warmup 3 --no-cpu-baseline --no-e2e --no-cusparse > "$OUT/ab_${c}_${AB_VAR}_$v.log" 2>&1
+        echo "ab $c $AB_VAR=$v: $(python -c "import json,sys; d=json.loads(open(sys.argv[1]).read().strip().splitlines()[-1]); print(round(d['ms_per_step'],3), 'spmm', round(d['spmm_only']['ms_per_layer'],3), 'plan', round(d['plan_ms'],3))" "$OUT/ab_${c}_${AB_VAR}_$v.log" 2>&1 | tail -1)"
+      done; done;;
     ncu_list)
       timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv \
         --log-file "$OUT/launches_c5.csv" python bench.py --profile --steps 2 --warmup 1 > "$OUT/ncu_list.log" 2>&1; echo "ncu_list rc=$?";;
+    ncu_ab)  # full ncu capture of the SpMM kernel per config x variant (AB_VAR/AB_VALUES)
+      for c in ${AB_CONFIGS:-c5 c4}; do for v in ${AB_VALUES//,/ }; do
+        env ${AB_VAR}=$v timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_spmm_block -s 3 -c 1 \
+          -o "$OUT/prof_${c}_${AB_VAR}_$v" -f python bench.py --profile --config $c --steps 1 --warmup 1 > "$OUT/ncu_${c}_$v.log" 2>&1; echo "ncu $c $v rc=$?"
+        python tools/ncu_summary.py "$OUT/sum_${c}_${AB_VAR}_$v" "$OUT/prof_${c}_${AB_VAR}_$v.ncu-rep" | tail -1
+        python tools/ncu_stalls.py "$OUT/prof_${c}_${AB_VAR}_$v.ncu-rep" 30 > "$OUT/stalls_${c}_${AB_VAR}_$v.txt"
+        [ -n "$KEEP_REP" ] || rm -f "$OUT/prof_${c}_${AB_VAR}_$v.ncu-rep"
+      done; done;;
     ncu_full)
       for c in c5 c4 c3; do
         timeout 1200 ncu --set full --clock-control none --import-source on -k regex:k_spmm_block -s 3 -c 1 \
           -o "$OUT/prof_$c" -f python bench.py --profile --config $c --steps 1 --warmup 1 > "$OUT/ncu_full_$c.log" 2>&1; echo "ncu_full $c rc=$?"
+        python tools/ncu_summary.py "$OUT/sum_$c" "$OUT/prof_$c.ncu-rep" | tail -1
+        python tools/ncu_stalls.py "$OUT/prof_$c.ncu-rep" 30 > "$OUT/stalls_$c.txt"
+        [ -n "$KEEP_REP" ] || rm -f "$OUT/prof_$c.ncu-rep"
       done;;
   esac
 done
