@@ -287,6 +287,144 @@ __global__ void __launch_bounds__(kCtaThreads, 4) k_spmm_block(const __grid_cons
     }
 }
 
+// ---------------------------------------------------------------- lean fast path
+// Same mapping and results as k_spmm_block for the common shape (float4 path, one vector
+// per lane: F % 4 == 0, F <= 128), written for occupancy: the gather of X rows is latency
+// bound and B200 sustains ~18 TB/s of L2->SM gather only with ~64 resident warps/SM
+// (tools/gather_probe.cu), so the hot loop keeps only the 4 in-flight rows, the accumulator
+// and a countdown to the end of the current row segment in registers; everything per-row
+// happens in the cold flush path.
+struct LeanArgs {
+    const int4* desc;
+    int64_t nblocks;
+    int64_t first_ov;
+    int64_t n_zero;
+    const int32_t* colidx;  // caller colidx, offset by rowptr[0]
+    const int32_t* srp;
+    const int32_t* rso;
+    const int32_t* perm;
+    const float* vals;      // caller vals, offset by rowptr[0]
+    const float4* X;
+    float4* Y;
+    float4* ovp;
+    int32_t db, stage, rso_stage, FV;
+    ColMap cmap;
+};
+
+template <int L, bool RELABEL>
+__global__ void __launch_bounds__(kCtaThreads, 6) k_spmm_lean(const __grid_constant__ LeanArgs a) {
+    constexpr int G = 32 / L;
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int s = lane / L, li = lane % L;
+    const int per_warp = 2 * a.stage + a.rso_stage;
+    int32_t* s_col = reinterpret_cast<int32_t*>(smem) + warp * per_warp;
+    float* s_val = reinterpret_cast<float*>(s_col + a.stage);
+    int32_t* s_rso = s_col + 2 * a.stage;
+    float4* s_part = reinterpret_cast<float4*>(smem + (size_t)kWarpsPerCta * per_warp * 4) + warp * (2 * 32);
+    const int32_t FV = a.FV;
+    const bool lane_on = li < FV;
+    const int64_t gw = (int64_t)blockIdx.x * kWarpsPerCta + warp;
+    const int64_t W = (int64_t)gridDim.x * kWarpsPerCta;
+
+    for (int64_t r = gw * G + s; r < a.n_zero; r += W * G)  // degree-0 rows (Q16)
+        if (lane_on) sty(a.Y + (int64_t)a.perm[r] * FV + li, vzero4());
+
+    const float4* __restrict__ Xl = a.X + li;
+    for (int64_t b = gw; b < a.nblocks; b += W) {
+        const int4 m = __ldg(a.desc + b);
+        const bool ov = m.x > a.db;
+        const int32_t d = m.x, loc = m.y, row0 = m.z;
+        const int32_t total = ov ? m.w : (m.w & 0xffff) * d;
+        const int32_t seg = ov ? total : d;
+
+        __syncwarp();
+        int32_t vbase0 = 0;
+        if (ov) {
+            vbase0 = __ldg(a.rso + row0) + (loc - __ldg(a.srp + row0));
+        } else {
+            for (int32_t r = lane; r < (m.w & 0xffff); r += 32) s_rso[r] = __ldg(a.rso + row0 + r);
+            __syncwarp();
+        }
+        for (int32_t e = lane; e < total; e += 32) {
+            int32_t off;
+            if (ov) {
+                off = vbase0 + e;
+            } else {
+                const int32_t r = e / d;
+                off = s_rso[r] + (e - r * d);
+            }
+            const int32_t c = ldcs_i(a.colidx + off);
+            s_col[e] = RELABEL ? map_col(c, a.cmap) : c;
+            s_val[e] = ldcs_f(a.vals + off);
+        }
+        __syncwarp();
+
+        const int32_t Q = (((total + G - 1) / G) + 3) & ~3;
+        const int32_t q0 = min(s * Q, total), q1 = min(q0 + Q, total);
+        float4 acc = vzero4();
+        int32_t left = seg - (q0 % seg);  // entries left in the current row segment
+
+        // cold path: a row segment ends at q_end
+        auto flush = [&](int32_t q_end) {
+            const int32_t rstart = q_end + 1 - seg;
+            if (rstart >= q0) {
+                if (lane_on) {
+                    float4* dst = ov ? a.ovp + (b - a.first_ov) * (int64_t)FV
+                                     : a.Y + (int64_t)a.perm[row0 + rstart / seg] * FV;
+                    sty(dst + li, acc);
+                }
+            } else {
+                s_part[s * 2 * L + li] = acc;  // head partial: finished below
+            }
+            acc = vzero4();
+            left = seg;
+        };
+
+        for (int32_t q = q0; q < q1; q += 4) {
+            const int4 c = *reinterpret_cast<const int4*>(s_col + q);
+            const float4 z = vzero4();
+            const float4 x0 = (lane_on) ? __ldg(Xl + (int64_t)c.x * FV) : z;
+            const float4 x1 = (lane_on && q + 1 < q1) ? __ldg(Xl + (int64_t)c.y * FV) : z;
+            const float4 x2 = (lane_on && q + 2 < q1) ? __ldg(Xl + (int64_t)c.z * FV) : z;
+            const float4 x3 = (lane_on && q + 3 < q1) ? __ldg(Xl + (int64_t)c.w * FV) : z;
+            const float4 v = *reinterpret_cast<const float4*>(s_val + q);
+            vfma(acc, v.x, x0);
+            if (--left == 0) flush(q);
+            if (q + 1 < q1) {
+                vfma(acc, v.y, x1);
+                if (--left == 0) flush(q + 1);
+            }
+            if (q + 2 < q1) {
+                vfma(acc, v.z, x2);
+                if (--left == 0) flush(q + 2);
+            }
+            if (q + 3 < q1) {
+                vfma(acc, v.w, x3);
+                if (--left == 0) flush(q + 3);
+            }
+        }
+        if (q1 > q0 && left < seg) {  // range ends inside a row: tail (1) or middle (0) partial
+            const int32_t cs = q1 - (seg - left);
+            s_part[(s * 2 + (cs >= q0 ? 1 : 0)) * L + li] = acc;
+        }
+        __syncwarp();
+        const int32_t h = q0 % seg;
+        if (q1 > q0 && h != 0 && q0 - h + seg <= q1) {  // we finish a row begun earlier
+            const int32_t fin_rs = q0 - h;
+            const int s_first = fin_rs / Q;
+            float4 sum = s_part[(s_first * 2 + 1) * L + li];
+            for (int s2 = s_first + 1; s2 <= s; ++s2) vadd(sum, s_part[(s2 * 2) * L + li]);
+            if (lane_on) {
+                float4* dst = ov ? a.ovp + (b - a.first_ov) * (int64_t)FV
+                                 : a.Y + (int64_t)a.perm[row0 + fin_rs / seg] * FV;
+                sty(dst + li, sum);
+            }
+        }
+        __syncwarp();
+    }
+}
+
 // Level-3 merge: oversized row k gets the sum of its chunk partials.  One CTA per row:
 // thread (g, c) sums chunks c0+g, c0+g+NG, ... of vector column c in order, then thread
 // (0, c) adds the NG group sums in group order -> fixed summation order (deterministic).
@@ -511,6 +649,34 @@ void launch_warp(const WarpArgs& a, cudaStream_t s) {
         }                                                                            \
     } while (0)
 
+template <int L, bool RELABEL>
+void launch_lean_t(const LeanArgs& a, cudaStream_t s, size_t smem) {
+    auto kern = k_spmm_lean<L, RELABEL>;
+    static int occ = -1;
+    static size_t occ_smem = 0;
+    if (occ < 0 || occ_smem != smem) {
+        AGCN_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        static const int carve = env_int("AGCN_CARVEOUT", -1);
+        if (carve >= 0) AGCN_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, carve));
+        AGCN_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kCtaThreads, smem));
+        if (occ < 1) occ = 1;
+        occ_smem = smem;
+    }
+    const int64_t work = std::max<int64_t>(a.nblocks, (a.n_zero + 31) / 32);
+    const int64_t want = (work + kWarpsPerCta - 1) / kWarpsPerCta;
+    const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)num_sms() * occ));
+    kern<<<(unsigned)grid, kCtaThreads, smem, s>>>(a);
+    post_launch();
+}
+
+template <int L>
+void launch_lean(const LeanArgs& a, cudaStream_t s, size_t smem) {
+    if (a.cmap.nparts > 0)
+        launch_lean_t<L, true>(a, s, smem);
+    else
+        launch_lean_t<L, false>(a, s, smem);
+}
+
 template <int L, int T>
 void block_v4(const BlockArgs& a, cudaStream_t s, size_t smem) { launch_block<L, T, true>(a, s, smem); }
 template <int L, int T>
@@ -590,7 +756,20 @@ void spmm_launch(agcn_plan_s* p, const float* vals, const float* X, int32_t F, f
     a.FV = FV;
     const size_t elt = v4 ? sizeof(float4) : sizeof(float);
     const size_t smem = (size_t)kWarpsPerCta * ((2 * a.stage + a.rso_stage) * 4 + 64 * sh.T * elt);
-    if (v4)
+    static const int lean_env = env_int("AGCN_LEAN", 1);
+    if (v4 && sh.T == 1 && lean_env) {
+        LeanArgs la{a.desc, a.nblocks, a.first_ov, a.n_zero, a.colidx, a.srp, a.rso, a.perm, a.vals,
+                    reinterpret_cast<const float4*>(X), reinterpret_cast<float4*>(Y),
+                    reinterpret_cast<float4*>(p->ov_partial), a.db, a.stage, a.rso_stage, FV, a.cmap};
+        switch (sh.L) {
+            case 1: launch_lean<1>(la, s, smem); break;
+            case 2: launch_lean<2>(la, s, smem); break;
+            case 4: launch_lean<4>(la, s, smem); break;
+            case 8: launch_lean<8>(la, s, smem); break;
+            case 16: launch_lean<16>(la, s, smem); break;
+            default: launch_lean<32>(la, s, smem); break;
+        }
+    } else if (v4)
         AGCN_DISPATCH_LT(sh, block_v4, a, s, smem);
     else
         AGCN_DISPATCH_LT(sh, block_v1, a, s, smem);
