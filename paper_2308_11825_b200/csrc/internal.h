@@ -91,6 +91,9 @@ struct agcn_plan_s {
     int32_t* sorted_rowptr = nullptr;  // [n+1] row pointer of the degree-sorted CSR (P:295 (3))
     int32_t* row_src_off = nullptr;    // [n]   rowptr[perm[k]] - rowptr[0]
     const int32_t* colidx = nullptr;   // BORROWED caller colidx (indexed by rowptr values)
+    int32_t* sorted_colidx = nullptr;  // [nnz + 8] degree-sorted colidx (relabelled), heat class
+                                       // in bits 29-30 when `heat` (a SpMM cache hint)
+    bool heat = false;
     agcn::ColMap cmap{};               // optional padded-layout column relabel
     int4* desc = nullptr;              // [nblocks]
     int32_t* ov_chunk_start = nullptr; // [n_ov + 1]

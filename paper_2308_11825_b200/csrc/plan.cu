@@ -267,6 +267,81 @@ __global__ void k_emit_ov(const int32_t* __restrict__ sorted_rowptr, int64_t ov_
         desc[nb_small + c0 + j] = make_int4(d, loc + j * db, row, min(db, d - j * db));
 }
 
+// ---------------------------------------------------------------- column heat (L2 hint)
+// Not part of the paper's metadata: a B200 cache-residency hint for the SpMM.  Columns are
+// ranked by (sampled) in-degree; the top K3 < K2 < K1 columns get heat class 3 / 2 / 1, stored
+// in bits 29-30 of the plan's degree-sorted colidx.  agcn_spmm keeps rows of hot classes in L2
+// with an evict_last policy (how many classes depends on F: the hot rows must fit in L2).
+constexpr int kHeatSample = 8;   // count every 8th nonzero
+constexpr int kHeatBins = 4096;  // sampled counts are capped into this many bins
+constexpr int kHeatShift = 29;
+__device__ __constant__ int64_t kHeatK[3] = {384 * 1024, 192 * 1024, 96 * 1024};
+
+__global__ void k_col_count(const int32_t* __restrict__ colidx, int64_t nnz, int32_t* __restrict__ cnt) {
+    for (int64_t q = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * kHeatSample; q < nnz;
+         q += (int64_t)gridDim.x * blockDim.x * kHeatSample)
+        atomicAdd(&cnt[__ldcs(colidx + q)], 1);
+}
+
+__global__ void k_count_hist(const int32_t* __restrict__ cnt, int64_t n_cols, int32_t* __restrict__ hist) {
+    __shared__ int32_t h[kHeatBins];
+    for (int b = threadIdx.x; b < kHeatBins; b += blockDim.x) h[b] = 0;
+    __syncthreads();
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n_cols; j += (int64_t)gridDim.x * blockDim.x)
+        atomicAdd(&h[min(cnt[j], kHeatBins - 1)], 1);
+    __syncthreads();
+    for (int b = threadIdx.x; b < kHeatBins; b += blockDim.x)
+        if (h[b]) atomicAdd(&hist[b], h[b]);
+}
+
+// thr[k] = lowest count c >= 1 such that #columns with count >= c is <= kHeatK[k]
+__global__ void k_heat_thresholds(const int32_t* __restrict__ hist, int32_t* __restrict__ thr) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    int64_t acc = 0;
+    int32_t t[3] = {kHeatBins, kHeatBins, kHeatBins};
+    for (int b = kHeatBins - 1; b >= 1; --b) {
+        acc += hist[b];
+        for (int k = 0; k < 3; ++k)
+            if (acc <= kHeatK[k]) t[k] = b;
+    }
+    for (int k = 0; k < 3; ++k) thr[k] = t[k];
+}
+
+// Degree-sorted colidx (relabelled, heat class in bits 29-30), one warp per descriptor: the
+// descriptor's nonzeros are contiguous in the sorted order, its rows start at row_src_off.
+__global__ void __launch_bounds__(kThreads) k_gather_cols(
+    const int4* __restrict__ desc, int64_t nblocks, int32_t db, const int32_t* __restrict__ rso,
+    const int32_t* __restrict__ srp, const int32_t* __restrict__ colidx, ColMap cm,
+    const int32_t* __restrict__ cnt, const int32_t* __restrict__ thr, int32_t* __restrict__ out) {
+    const int lane = threadIdx.x & 31;
+    int32_t t0 = 0, t1 = 0, t2 = 0;
+    if (cnt) { t0 = thr[0]; t1 = thr[1]; t2 = thr[2]; }
+    for (int64_t b = (int64_t)blockIdx.x * kWarps + (threadIdx.x >> 5); b < nblocks;
+         b += (int64_t)gridDim.x * kWarps) {
+        const int4 m = desc[b];
+        const bool ov = m.x > db;
+        const int32_t d = m.x, loc = m.y, row0 = m.z;
+        const int32_t total = ov ? m.w : (m.w & 0xffff) * d;
+        const int32_t vbase0 = ov ? rso[row0] + (loc - srp[row0]) : 0;
+        for (int32_t e = lane; e < total; e += 32) {
+            int32_t off;
+            if (ov) {
+                off = vbase0 + e;
+            } else {
+                const int32_t r = e / d;
+                off = rso[row0 + r] + (e - r * d);
+            }
+            const int32_t c = __ldcs(colidx + off);
+            int32_t v = map_col(c, cm);
+            if (cnt) {
+                const int32_t k = __ldg(cnt + c);
+                v |= ((k >= t0) + (k >= t1) + (k >= t2)) << kHeatShift;
+            }
+            out[loc + e] = v;
+        }
+    }
+}
+
 // ---------------------------------------------------------------- warp-level partition
 __global__ void k_rowptr_check(const int32_t* __restrict__ rowptr, int64_t n, int32_t mwn,
                                int32_t* __restrict__ rp_copy, int32_t* __restrict__ ntask,
@@ -513,6 +588,35 @@ void build_block_plan(agcn_plan_s* p, const int32_t* rowptr, const int32_t* coli
     } else {
         AGCN_CUDA(cudaMemsetAsync(p->ov_chunk_start, 0, sizeof(int32_t), s));
     }
+
+    // Degree-sorted colidx for the SpMM's contiguous staging, with column heat classes.
+    p->sorted_colidx = dalloc<int32_t>(nnz + 8, s);
+    p->device_bytes += sizeof(int32_t) * (size_t)(nnz + 8);
+    AGCN_CUDA(cudaMemsetAsync(p->sorted_colidx + nnz, 0, 8 * sizeof(int32_t), s));
+    p->heat = p->x_rows < (1ll << kHeatShift) && nnz > 0;
+    int32_t *cnt = nullptr, *hist = nullptr, *thr = nullptr;
+    if (p->heat) {
+        cnt = dalloc<int32_t>(p->n_cols, s);
+        hist = dalloc<int32_t>(kHeatBins, s);
+        thr = dalloc<int32_t>(3, s);
+        AGCN_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int32_t) * p->n_cols, s));
+        AGCN_CUDA(cudaMemsetAsync(hist, 0, sizeof(int32_t) * kHeatBins, s));
+        const unsigned g = (unsigned)std::min<int64_t>(blocks_for(nnz / kHeatSample + 1, 256), 148 * 8);
+        k_col_count<<<g, 256, 0, s>>>(colidx + p->rp_base, nnz, cnt);
+        post_launch();
+        k_count_hist<<<(unsigned)std::min<int64_t>(blocks_for(p->n_cols, 256), 148 * 2), 256, 0, s>>>(
+            cnt, p->n_cols, hist);
+        post_launch();
+        k_heat_thresholds<<<1, 32, 0, s>>>(hist, thr);
+        post_launch();
+    }
+    if (p->nblocks > 0) {
+        const unsigned g = (unsigned)std::min<int64_t>(blocks_for(p->nblocks, kWarps), 148 * 16);
+        k_gather_cols<<<g, kThreads, 0, s>>>(p->desc, p->nblocks, db, p->row_src_off, p->sorted_rowptr,
+                                              colidx + p->rp_base, p->cmap, cnt, thr, p->sorted_colidx);
+        post_launch();
+    }
+    dfree(cnt, s); dfree(hist, s); dfree(thr, s);
     dfree(d_tab, s); dfree(table, s); dfree(bin_cnt, s); dfree(d_flags, s);
 }
 
@@ -559,8 +663,8 @@ void build_warp_plan(agcn_plan_s* p, const int32_t* rowptr, const int32_t* colid
 }  // namespace
 
 void free_plan_arrays(agcn_plan_s* p) {
-    void* ptrs[] = {p->perm, p->sorted_rowptr, p->row_src_off, p->desc, p->ov_chunk_start,
-                    p->tasks, p->rowptr_copy, p->colidx_copy, p->ov_partial};
+    void* ptrs[] = {p->perm,  p->sorted_rowptr, p->row_src_off, p->desc,       p->ov_chunk_start,
+                    p->tasks, p->rowptr_copy,   p->colidx_copy, p->ov_partial, p->sorted_colidx};
     // Stream-ordered release on the plan's stream, after the last SpMM that used the plan on
     // another stream (p->last_use); no host synchronisation.
     if (p->last_use) cudaStreamWaitEvent(p->stream, p->last_use, 0);
@@ -570,11 +674,19 @@ void free_plan_arrays(agcn_plan_s* p) {
     if (p->last_use) cudaEventDestroy(p->last_use);
 }
 
-// Materialise the degree-sorted colidx (introspection for parity tests; not on the path).
+// Degree-sorted colidx for introspection (parity tests): the plan's array without heat bits.
 void plan_copy_sorted_colidx(agcn_plan_s* p, int32_t* host_dst) {
     if (p->nnz == 0) return;
     cudaStream_t s = p->stream;
-    int32_t* d = dalloc<int32_t>(p->nnz, s);
+    if (p->sorted_colidx) {
+        AGCN_CUDA(cudaMemcpyAsync(host_dst, p->sorted_colidx, sizeof(int32_t) * p->nnz,
+                                  cudaMemcpyDeviceToHost, s));
+        AGCN_CUDA(cudaStreamSynchronize(s));
+        if (p->heat)
+            for (int64_t i = 0; i < p->nnz; ++i) host_dst[i] &= (1 << kHeatShift) - 1;
+        return;
+    }
+    int32_t* d = dalloc<int32_t>(p->nnz, s);  // warp partition: gather in degree order
     if (p->n > 0) {
         k_gather_sorted_cols<<<blocks_for(p->n, kWarps), kThreads, 0, s>>>(
             p->n, p->sorted_rowptr, p->row_src_off, p->colidx + p->rp_base, p->cmap, d);

@@ -115,7 +115,7 @@ struct BlockArgs {
     int32_t db;             // deg_bound
     int32_t stage;          // shared-memory entries per warp (>= db + 8, multiple of 4)
     int32_t rso_stage;      // shared-memory row offsets per warp (>= max_block_warps)
-    const int32_t* colidx;  // caller colidx, already offset by rowptr[0] (borrowed)
+    const int32_t* scol;    // plan's degree-sorted colidx (relabelled; heat class in bits 29-30)
     const int32_t* srp;     // sorted rowptr
     const int32_t* rso;     // row_src_off
     const int32_t* perm;    // sorted -> original row
@@ -125,7 +125,6 @@ struct BlockArgs {
     float* ovp;             // oversized partials [ov_chunks][FV]
     int64_t n_zero;         // sorted rows [0, n_zero) have degree 0
     int32_t FV;             // vectors per row (F/4 on the float4 path, F otherwise)
-    ColMap cmap;            // padded-layout column relabel (nparts == 0: identity)
     int32_t xmode;          // X-load flavour (see ldx)
 };
 
@@ -188,7 +187,7 @@ __global__ void __launch_bounds__(kCtaThreads, 4) k_spmm_block(const __grid_cons
                 const int32_t r = e / d;
                 off = s_rso[r] + (e - r * d);
             }
-            s_col[e] = map_col(ldcs_i(a.colidx + off), a.cmap);
+            s_col[e] = ldcs_i(a.scol + loc + e) & ((1 << 29) - 1);
             s_val[e] = ldcs_f(a.vals + off);
         }
         __syncwarp();
@@ -299,7 +298,7 @@ struct LeanArgs {
     int64_t nblocks;
     int64_t first_ov;
     int64_t n_zero;
-    const int32_t* colidx;  // caller colidx, offset by rowptr[0]
+    const int32_t* scol;    // plan's degree-sorted colidx (relabelled; heat class in bits 29-30)
     const int32_t* srp;
     const int32_t* rso;
     const int32_t* perm;
@@ -308,19 +307,33 @@ struct LeanArgs {
     float4* Y;
     float4* ovp;
     int32_t db, stage, rso_stage, FV;
-    ColMap cmap;
+    int32_t min_cls;        // heat class from which X rows are kept in L2 (evict_last); 4: none
 };
 
-template <int L, bool RELABEL>
+// X-row load with the L2 residency hint: hot rows evict_last, the rest default priority.
+__device__ __forceinline__ float4 ldx_heat(const float4* p, bool hot, uint64_t pol) {
+    float4 v;
+    if (hot)
+        asm("ld.global.nc.L2::cache_hint.v4.f32 {%0, %1, %2, %3}, [%4], %5;"
+            : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p), "l"(pol));
+    else
+        v = __ldg(p);
+    return v;
+}
+
+template <int L>
 __global__ void __launch_bounds__(kCtaThreads, 6) k_spmm_lean(const __grid_constant__ LeanArgs a) {
     constexpr int G = 32 / L;
+    constexpr int32_t kColMask = (1 << 29) - 1;
     extern __shared__ __align__(16) unsigned char smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int s = lane / L, li = lane % L;
-    const int per_warp = 2 * a.stage + a.rso_stage;
+    const int per_warp = 2 * a.stage + 2 * a.rso_stage;
     int32_t* s_col = reinterpret_cast<int32_t*>(smem) + warp * per_warp;
     float* s_val = reinterpret_cast<float*>(s_col + a.stage);
     int32_t* s_rso = s_col + 2 * a.stage;
+    int32_t* s_perm = s_rso + a.rso_stage;
+    const uint64_t pol = policy_evict_last();
     float4* s_part = reinterpret_cast<float4*>(smem + (size_t)kWarpsPerCta * per_warp * 4) + warp * (2 * 32);
     const int32_t FV = a.FV;
     const bool lane_on = li < FV;
@@ -338,15 +351,21 @@ __global__ void __launch_bounds__(kCtaThreads, 6) k_spmm_lean(const __grid_const
         const int32_t total = ov ? m.w : (m.w & 0xffff) * d;
         const int32_t seg = ov ? total : d;
 
+        // ---- stage: colidx contiguous from the plan's sorted array; vals through row_src_off;
+        // perm of the descriptor's rows (for the stores)
         __syncwarp();
         int32_t vbase0 = 0;
         if (ov) {
             vbase0 = __ldg(a.rso + row0) + (loc - __ldg(a.srp + row0));
         } else {
-            for (int32_t r = lane; r < (m.w & 0xffff); r += 32) s_rso[r] = __ldg(a.rso + row0 + r);
+            for (int32_t r = lane; r < (m.w & 0xffff); r += 32) {
+                s_rso[r] = __ldg(a.rso + row0 + r);
+                s_perm[r] = __ldg(a.perm + row0 + r);
+            }
             __syncwarp();
         }
         for (int32_t e = lane; e < total; e += 32) {
+            s_col[e] = ldcs_i(a.scol + loc + e);
             int32_t off;
             if (ov) {
                 off = vbase0 + e;
@@ -354,8 +373,6 @@ __global__ void __launch_bounds__(kCtaThreads, 6) k_spmm_lean(const __grid_const
                 const int32_t r = e / d;
                 off = s_rso[r] + (e - r * d);
             }
-            const int32_t c = ldcs_i(a.colidx + off);
-            s_col[e] = RELABEL ? map_col(c, a.cmap) : c;
             s_val[e] = ldcs_f(a.vals + off);
         }
         __syncwarp();
@@ -371,7 +388,7 @@ __global__ void __launch_bounds__(kCtaThreads, 6) k_spmm_lean(const __grid_const
             if (rstart >= q0) {
                 if (lane_on) {
                     float4* dst = ov ? a.ovp + (b - a.first_ov) * (int64_t)FV
-                                     : a.Y + (int64_t)a.perm[row0 + rstart / seg] * FV;
+                                     : a.Y + (int64_t)s_perm[rstart / seg] * FV;
                     sty(dst + li, acc);
                 }
             } else {
@@ -384,10 +401,11 @@ __global__ void __launch_bounds__(kCtaThreads, 6) k_spmm_lean(const __grid_const
         for (int32_t q = q0; q < q1; q += 4) {
             const int4 c = *reinterpret_cast<const int4*>(s_col + q);
             const float4 z = vzero4();
-            const float4 x0 = (lane_on) ? __ldg(Xl + (int64_t)c.x * FV) : z;
-            const float4 x1 = (lane_on && q + 1 < q1) ? __ldg(Xl + (int64_t)c.y * FV) : z;
-            const float4 x2 = (lane_on && q + 2 < q1) ? __ldg(Xl + (int64_t)c.z * FV) : z;
-            const float4 x3 = (lane_on && q + 3 < q1) ? __ldg(Xl + (int64_t)c.w * FV) : z;
+            const int32_t mc = a.min_cls;
+            const float4 x0 = (lane_on) ? ldx_heat(Xl + (int64_t)(c.x & kColMask) * FV, (c.x >> 29) >= mc, pol) : z;
+            const float4 x1 = (lane_on && q + 1 < q1) ? ldx_heat(Xl + (int64_t)(c.y & kColMask) * FV, (c.y >> 29) >= mc, pol) : z;
+            const float4 x2 = (lane_on && q + 2 < q1) ? ldx_heat(Xl + (int64_t)(c.z & kColMask) * FV, (c.z >> 29) >= mc, pol) : z;
+            const float4 x3 = (lane_on && q + 3 < q1) ? ldx_heat(Xl + (int64_t)(c.w & kColMask) * FV, (c.w >> 29) >= mc, pol) : z;
             const float4 v = *reinterpret_cast<const float4*>(s_val + q);
             vfma(acc, v.x, x0);
             if (--left == 0) flush(q);
@@ -417,7 +435,7 @@ __global__ void __launch_bounds__(kCtaThreads, 6) k_spmm_lean(const __grid_const
             for (int s2 = s_first + 1; s2 <= s; ++s2) vadd(sum, s_part[(s2 * 2) * L + li]);
             if (lane_on) {
                 float4* dst = ov ? a.ovp + (b - a.first_ov) * (int64_t)FV
-                                 : a.Y + (int64_t)a.perm[row0 + fin_rs / seg] * FV;
+                                 : a.Y + (int64_t)s_perm[fin_rs / seg] * FV;
                 sty(dst + li, sum);
             }
         }
@@ -649,9 +667,9 @@ void launch_warp(const WarpArgs& a, cudaStream_t s) {
         }                                                                            \
     } while (0)
 
-template <int L, bool RELABEL>
-void launch_lean_t(const LeanArgs& a, cudaStream_t s, size_t smem) {
-    auto kern = k_spmm_lean<L, RELABEL>;
+template <int L>
+void launch_lean(const LeanArgs& a, cudaStream_t s, size_t smem) {
+    auto kern = k_spmm_lean<L>;
     static int occ = -1;
     static size_t occ_smem = 0;
     if (occ < 0 || occ_smem != smem) {
@@ -667,14 +685,6 @@ void launch_lean_t(const LeanArgs& a, cudaStream_t s, size_t smem) {
     const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)num_sms() * occ));
     kern<<<(unsigned)grid, kCtaThreads, smem, s>>>(a);
     post_launch();
-}
-
-template <int L>
-void launch_lean(const LeanArgs& a, cudaStream_t s, size_t smem) {
-    if (a.cmap.nparts > 0)
-        launch_lean_t<L, true>(a, s, smem);
-    else
-        launch_lean_t<L, false>(a, s, smem);
 }
 
 template <int L, int T>
@@ -741,8 +751,7 @@ void spmm_launch(agcn_plan_s* p, const float* vals, const float* X, int32_t F, f
     a.db = p->deg_bound;
     a.stage = ((p->deg_bound + 3) & ~3) + 8;
     a.rso_stage = (p->mbw + 3) & ~3;
-    a.colidx = p->colidx + p->rp_base;
-    a.cmap = p->cmap;
+    a.scol = p->sorted_colidx;
     static const int xmode = env_int("AGCN_XMODE", 0);
     a.xmode = xmode;
     a.srp = p->sorted_rowptr;
@@ -758,16 +767,20 @@ void spmm_launch(agcn_plan_s* p, const float* vals, const float* X, int32_t F, f
     const size_t smem = (size_t)kWarpsPerCta * ((2 * a.stage + a.rso_stage) * 4 + 64 * sh.T * elt);
     static const int lean_env = env_int("AGCN_LEAN", 1);
     if (v4 && sh.T == 1 && lean_env) {
-        LeanArgs la{a.desc, a.nblocks, a.first_ov, a.n_zero, a.colidx, a.srp, a.rso, a.perm, a.vals,
+        // rows of heat class >= min_cls are kept in L2: ~100 MB of hot rows (plan.cu kHeatK)
+        static const int heat_env = env_int("AGCN_HEAT", 1);
+        const int min_cls = !p->heat || !heat_env ? 4 : F <= 64 ? 1 : F <= 128 ? 2 : F <= 256 ? 3 : 4;
+        LeanArgs la{a.desc, a.nblocks, a.first_ov, a.n_zero, a.scol, a.srp, a.rso, a.perm, a.vals,
                     reinterpret_cast<const float4*>(X), reinterpret_cast<float4*>(Y),
-                    reinterpret_cast<float4*>(p->ov_partial), a.db, a.stage, a.rso_stage, FV, a.cmap};
+                    reinterpret_cast<float4*>(p->ov_partial), a.db, a.stage, a.rso_stage, FV, min_cls};
+        const size_t lsmem = (size_t)kWarpsPerCta * ((2 * a.stage + 2 * a.rso_stage) * 4 + 64 * 16);
         switch (sh.L) {
-            case 1: launch_lean<1>(la, s, smem); break;
-            case 2: launch_lean<2>(la, s, smem); break;
-            case 4: launch_lean<4>(la, s, smem); break;
-            case 8: launch_lean<8>(la, s, smem); break;
-            case 16: launch_lean<16>(la, s, smem); break;
-            default: launch_lean<32>(la, s, smem); break;
+            case 1: launch_lean<1>(la, s, lsmem); break;
+            case 2: launch_lean<2>(la, s, lsmem); break;
+            case 4: launch_lean<4>(la, s, lsmem); break;
+            case 8: launch_lean<8>(la, s, lsmem); break;
+            case 16: launch_lean<16>(la, s, lsmem); break;
+            default: launch_lean<32>(la, s, lsmem); break;
         }
     } else if (v4)
         AGCN_DISPATCH_LT(sh, block_v4, a, s, smem);

@@ -41,6 +41,50 @@ __global__ void __launch_bounds__(256) k_ldg(const float4* __restrict__ X, const
     out[blockIdx.x * 256 + threadIdx.x] = acc.x + acc.y + acc.z + acc.w;
 }
 
+// 256-bit gathers (LDG.E.256): 8 lanes x 32 B per row at F = 64.  HINT: 0 normal; 1 evict_last
+// for rows flagged hot (bit 31 of the index), evict_first otherwise; 2 all evict_first.
+struct f8 { float v[8]; };
+template <int HINT>
+__device__ __forceinline__ f8 ld256(const float* p, bool hot) {
+    f8 r;
+    if (HINT == 1 && hot)
+        asm volatile("ld.global.nc.L2::evict_last.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                     : "=f"(r.v[0]), "=f"(r.v[1]), "=f"(r.v[2]), "=f"(r.v[3]), "=f"(r.v[4]), "=f"(r.v[5]),
+                       "=f"(r.v[6]), "=f"(r.v[7]) : "l"(p));
+    else if (HINT >= 1)
+        asm volatile("ld.global.nc.L2::evict_first.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                     : "=f"(r.v[0]), "=f"(r.v[1]), "=f"(r.v[2]), "=f"(r.v[3]), "=f"(r.v[4]), "=f"(r.v[5]),
+                       "=f"(r.v[6]), "=f"(r.v[7]) : "l"(p));
+    else
+        asm volatile("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                     : "=f"(r.v[0]), "=f"(r.v[1]), "=f"(r.v[2]), "=f"(r.v[3]), "=f"(r.v[4]), "=f"(r.v[5]),
+                       "=f"(r.v[6]), "=f"(r.v[7]) : "l"(p));
+    return r;
+}
+template <int U, int HINT>
+__global__ void __launch_bounds__(256) k_ldg256(const float* __restrict__ X, const int* __restrict__ idx, long n_idx,
+                                                float* __restrict__ out) {
+    constexpr int LP = F / 8;  // lanes per row
+    const int lane = threadIdx.x & 31, s = lane / LP, li = lane % LP;
+    constexpr int G = 32 / LP;
+    const long gw = (long)blockIdx.x * 8 + (threadIdx.x >> 5), W = (long)gridDim.x * 8;
+    float acc = 0.f;
+    for (long base = gw * G * U; base < n_idx; base += W * G * U) {
+        f8 v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            long q = base + s * U + u;
+            int r = q < n_idx ? __ldg(idx + q) : 0;
+            v[u] = ld256<HINT>(X + (long)(r & 0x7fffffff) * F + li * 8, r < 0);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+            for (int j = 0; j < 8; ++j) acc += v[u].v[j];
+    }
+    out[blockIdx.x * 256 + threadIdx.x] = acc;
+}
+
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
 // TMA gather: each warp owns a ring of S stages; a stage = 32 rows (8 gather4) = 8 KB.
@@ -162,6 +206,39 @@ int main(int argc, char** argv) {
         timeit(occ == 4 ? "ldg U=8 grid=148x4" : "ldg U=8 grid=148x8",
                [&] { k_ldg<8><<<sms * occ, 256>>>(reinterpret_cast<float4*>(X), idx, n_idx, out); });
     }
+    // 256-bit loads, and the hot/cold eviction policy: flag the most frequent rows (hot set of
+    // ~100 MB = 390K rows at F = 64) in bit 31 of the index.
+    {
+        std::vector<int> cnt(n_rows, 0);
+        for (auto x : h) cnt[x]++;
+        std::vector<int> order(n_rows);
+        for (long i = 0; i < n_rows; ++i) order[i] = (int)i;
+        long K = std::min<long>(n_rows, 390000);
+        std::nth_element(order.begin(), order.begin() + K, order.end(),
+                         [&](int a, int b) { return cnt[a] > cnt[b]; });
+        std::vector<char> hot(n_rows, 0);
+        for (long i = 0; i < K; ++i) hot[order[i]] = 1;
+        long hot_refs = 0;
+        std::vector<int> hf(n_idx);
+        for (long i = 0; i < n_idx; ++i) { hf[i] = hot[h[i]] ? (int)(h[i] | 0x80000000u) : h[i]; hot_refs += hot[h[i]]; }
+        printf("hot set %ld rows (%.0f MB) receives %.1f%% of refs\n", K, K * ROWB / 1e6, 100.0 * hot_refs / n_idx);
+        int* idxf;
+        CK(cudaMalloc(&idxf, sizeof(int) * n_idx));
+        CK(cudaMemcpy(idxf, hf.data(), sizeof(int) * n_idx, cudaMemcpyHostToDevice));
+        for (int occ : {4, 8}) {
+            char name[64];
+            snprintf(name, sizeof(name), "ldg256 U=4 normal x%d", occ);
+            timeit(name, [&] { k_ldg256<4, 0><<<sms * occ, 256>>>(X, idxf, n_idx, out); });
+            snprintf(name, sizeof(name), "ldg256 U=4 hot/cold x%d", occ);
+            timeit(name, [&] { k_ldg256<4, 1><<<sms * occ, 256>>>(X, idxf, n_idx, out); });
+            snprintf(name, sizeof(name), "ldg256 U=2 hot/cold x%d", occ);
+            timeit(name, [&] { k_ldg256<2, 1><<<sms * occ, 256>>>(X, idxf, n_idx, out); });
+            snprintf(name, sizeof(name), "ldg256 U=4 all-first x%d", occ);
+            timeit(name, [&] { k_ldg256<4, 2><<<sms * occ, 256>>>(X, idxf, n_idx, out); });
+        }
+        cudaFree(idxf);
+    }
+    if (getenv("PROBE_NO_TMA")) return 0;
     // TMA tensor map: 2D {F, n_rows} fp32, box {F, 1}
     EncodeFn enc = nullptr;
     cudaDriverEntryPointQueryResult q;

@@ -28,7 +28,7 @@ for st in $STAGES; do
         --log-file "$OUT/launches_c5.csv" python bench.py --profile --steps 2 --warmup 1 > "$OUT/ncu_list.log" 2>&1; echo "ncu_list rc=$?";;
     ncu_ab)  # full ncu capture of the SpMM kernel per config x variant (AB_VAR/AB_VALUES)
       for c in ${AB_CONFIGS:-c5 c4}; do for v in ${AB_VALUES//,/ }; do
-        env ${AB_VAR}=$v timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_spmm_block -s 3 -c 1 \
+        env ${AB_VAR}=$v timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_spmm_ -s 3 -c 1 \
           -o "$OUT/prof_${c}_${AB_VAR}_$v" -f python bench.py --profile --config $c --steps 1 --warmup 1 > "$OUT/ncu_${c}_$v.log" 2>&1; echo "ncu $c $v rc=$?"
         python tools/ncu_summary.py "$OUT/sum_${c}_${AB_VAR}_$v" "$OUT/prof_${c}_${AB_VAR}_$v.ncu-rep" | tail -1
         python tools/ncu_stalls.py "$OUT/prof_${c}_${AB_VAR}_$v.ncu-rep" 30 > "$OUT/stalls_${c}_${AB_VAR}_$v.txt"
@@ -36,7 +36,7 @@ for st in $STAGES; do
       done; done;;
     ncu_full)
       for c in c5 c4 c3; do
-        timeout 1200 ncu --set full --clock-control none --import-source on -k regex:k_spmm_block -s 3 -c 1 \
+        timeout 1200 ncu --set full --clock-control none --import-source on -k regex:k_spmm_ -s 3 -c 1 \
           -o "$OUT/prof_$c" -f python bench.py --profile --config $c --steps 1 --warmup 1 > "$OUT/ncu_full_$c.log" 2>&1; echo "ncu_full $c rc=$?"
         python tools/ncu_summary.py "$OUT/sum_$c" "$OUT/prof_$c.ncu-rep" | tail -1
         python tools/ncu_stalls.py "$OUT/prof_$c.ncu-rep" 30 > "$OUT/stalls_$c.txt"
