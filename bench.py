@@ -40,6 +40,8 @@ def parse():
     ap.add_argument("--F", type=int, default=None)
     ap.add_argument("--layers", type=int, default=None)
     ap.add_argument("--partition", choices=["block", "warp"], default="block")
+    ap.add_argument("--kernel", choices=["auto", "general", "wide"], default="auto")
+    ap.add_argument("--l2-hint", type=int, default=None, help="None: auto; 0: never; 1: always")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="CPU-oracle sample budget")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -61,7 +63,10 @@ def load_peaks():
 
 def load_traffic(config: str, F: int):
     """dram bytes per agcn_spmm launch from the committed ncu --set full summary, if any."""
-    for name in sorted(os.listdir(os.path.join(ROOT, "profiles")), reverse=True):
+    pdir = os.path.join(ROOT, "profiles")
+    if not os.path.isdir(pdir):
+        return None, None
+    for name in sorted(os.listdir(pdir), reverse=True):
         if name.startswith("ncu_traffic") and name.endswith(".json"):
             d = json.load(open(os.path.join(ROOT, "profiles", name)))
             key = f"{config}_F{F}"
@@ -234,7 +239,7 @@ def main():
         def spmm(Xin, out_rows):
             s0, s1 = ev(), ev()
             s0.record(stream)
-            plan.spmm(va_d, Xin, out=out_rows)
+            plan.spmm(va_d, Xin, out=out_rows, kernel=args.kernel, l2_hint=args.l2_hint)
             s1.record(stream)
             if record:
                 rec["spmm"].append((s0, s1))
@@ -304,7 +309,7 @@ def main():
             "scaling": "strong" if P > 1 else "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic",
             "config": {"workload": w.meta["desc"], "name": w.name, "n": n, "nnz": nnz, "F": F,
-                       "layers": layers, "partition": args.partition, "parallelism": f"row-shard{P}",
+                       "layers": layers, "partition": args.partition, "kernel": args.kernel, "parallelism": f"row-shard{P}",
                        "max_block_warps": 12, "max_warp_nzs": 32,
                        "l2": "inputs larger than L2 (CSR + X > 126 MB)" if
                              (8 * nnz + 4 * n * F) > 126e6 else "inputs fit in L2 (warm)",

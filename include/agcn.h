@@ -127,6 +127,33 @@ agcn_plan_t agcn_plan_ex(const int32_t* rowptr, const int32_t* colidx, int64_t n
 agcn_status_t agcn_spmm(agcn_plan_t plan, const float* vals, const float* X, int32_t F, float* Y,
                         agcn_stream_t stream);
 
+/* SpMM kernel variants (all compute the same Y within the tolerance; AUTO picks per F). */
+typedef enum {
+    AGCN_KERNEL_AUTO = 0,    /* WIDE when applicable, else GENERAL */
+    AGCN_KERNEL_GENERAL = 1, /* any F: float4 (F % 4 == 0, 16-B aligned X/Y) or scalar lanes;
+                                shared-memory staging of each descriptor's colidx / vals */
+    AGCN_KERNEL_WIDE = 3     /* F in {8,16,32,64,128,256}, 32-B aligned X/Y, max_block_warps
+                                <= 32: one 256-bit row slice per lane, shuffle-broadcast CSR */
+} agcn_kernel_t;
+
+typedef struct {
+    int32_t kernel;   /* agcn_kernel_t; default AGCN_KERNEL_AUTO */
+    int32_t l2_hint;  /* X-row L2 residency: -1 (default) evict_last hints when X fits in L2
+                         (<= 128 MiB), 0 never, 1 always */
+    int32_t reserved[6];
+} agcn_spmm_opts_t;
+
+/* Fill *opts with the defaults above. */
+void agcn_default_spmm_opts(agcn_spmm_opts_t* opts);
+
+/*
+ * agcn_spmm with an explicit kernel choice (same contract as agcn_spmm; opts may be NULL).
+ * A kernel that cannot run this F / alignment / plan returns AGCN_ERR_UNSUPPORTED.
+ * AGCN_PARTITION_WARP plans ignore opts.kernel (they have their own kernel).
+ */
+agcn_status_t agcn_spmm_ex(agcn_plan_t plan, const float* vals, const float* X, int32_t F,
+                           float* Y, agcn_stream_t stream, const agcn_spmm_opts_t* opts);
+
 /* Release the plan's device memory, stream-ordered on the plan's stream (after its own work
    and after the most recent agcn_spmm issued on another stream); never synchronises the host.
    Work on further streams must be ordered by the caller.  NULL is a no-op. */

@@ -17,7 +17,7 @@ import numpy as np
 from . import _lib
 from ._lib import FIELDS, STATUS
 
-__all__ = ["Plan", "AgcnError", "agcn_plan", "agcn_spmm", "shard_bounds", "propagate_host",
+__all__ = ["Plan", "AgcnError", "agcn_plan", "agcn_spmm", "agcn_spmm_ex", "shard_bounds", "propagate_host",
            "launch_count", "version", "library_path"]
 
 
@@ -149,8 +149,12 @@ class Plan:
                                          out.ctypes.data or None, out.nbytes))
         return out
 
-    def spmm(self, vals, X, out=None, stream=None):
-        """Y = A.X (asynchronous on `stream`, default the current torch stream)."""
+    def spmm(self, vals, X, out=None, stream=None, kernel: str = "auto", l2_hint: int | None = None):
+        """Y = A.X (asynchronous on `stream`, default the current torch stream).
+
+        kernel: "auto" | "general" | "wide" (agcn_kernel_t); l2_hint: None (auto: evict_last
+        hints on X rows when X fits in L2), 0 (never) or 1 (always).
+        """
         torch = _torch()
         F = X.shape[1] if X.dim() == 2 else 1
         if out is None:
@@ -162,8 +166,8 @@ class Plan:
         v = _dev_ptr(vals, "float32", "vals") if vals.numel() else 0
         x = _dev_ptr(X, "float32", "X") if X.numel() else 0
         y = _dev_ptr(out, "float32", "out") if out.numel() else 0
-        _check(_lib.lib().agcn_spmm(self.handle, v or None, x or None, int(F), y or None,
-                                    _stream_handle(stream)))
+        _check(_lib.lib().agcn_spmm_ex(self.handle, v or None, x or None, int(F), y or None,
+                                       _stream_handle(stream), _spmm_opts(kernel, l2_hint)))
         return out
 
     def close(self):
@@ -184,6 +188,14 @@ class Plan:
         self.close()
 
 
+def _spmm_opts(kernel: str = "auto", l2_hint: int | None = None):
+    o = _lib.SpmmOpts()
+    _lib.lib().agcn_default_spmm_opts(ctypes.byref(o))
+    o.kernel = _lib.KERNELS[kernel]
+    o.l2_hint = -1 if l2_hint is None else int(l2_hint)
+    return ctypes.byref(o)
+
+
 # ---------------------------------------------------------------- C-ABI-named functions
 def agcn_plan(rowptr, colidx, n: int, nnz: int) -> Plan:
     return Plan(rowptr, colidx, n, nnz)
@@ -195,6 +207,15 @@ def agcn_spmm(plan: Plan, vals, X, F: int, Y, stream=None) -> None:
     y = _dev_ptr(Y, "float32", "Y") if Y.numel() else 0
     _check(_lib.lib().agcn_spmm(plan.handle, v or None, x or None, int(F), y or None,
                                 _stream_handle(stream)))
+
+
+def agcn_spmm_ex(plan: Plan, vals, X, F: int, Y, stream=None, kernel: str = "auto",
+                 l2_hint: int | None = None) -> None:
+    v = _dev_ptr(vals, "float32", "vals") if vals.numel() else 0
+    x = _dev_ptr(X, "float32", "X") if X.numel() else 0
+    y = _dev_ptr(Y, "float32", "Y") if Y.numel() else 0
+    _check(_lib.lib().agcn_spmm_ex(plan.handle, v or None, x or None, int(F), y or None,
+                                   _stream_handle(stream), _spmm_opts(kernel, l2_hint)))
 
 
 def shard_bounds(rowptr, nranks: int, stream=None) -> np.ndarray:

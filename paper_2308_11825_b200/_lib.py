@@ -22,6 +22,13 @@ class Opts(ctypes.Structure):
                 ("col_slot_rows", c_i64)]
 
 
+KERNELS = {"auto": 0, "general": 1, "wide": 3}
+
+
+class SpmmOpts(ctypes.Structure):
+    _fields_ = [("kernel", c_i32), ("l2_hint", c_i32), ("reserved", c_i32 * 6)]
+
+
 class Stats(ctypes.Structure):
     _fields_ = [("n", c_i64), ("n_cols", c_i64), ("nnz", c_i64), ("nblocks", c_i64),
                 ("ntasks", c_i64), ("deg_bound", c_i64), ("max_deg", c_i64),
@@ -52,6 +59,10 @@ def lib():
     L.agcn_plan_ex.restype = c_vp
     L.agcn_spmm.argtypes = [c_vp, c_vp, c_vp, c_i32, c_vp, c_vp]
     L.agcn_spmm.restype = c_i32
+    L.agcn_default_spmm_opts.argtypes = [ctypes.POINTER(SpmmOpts)]
+    L.agcn_default_spmm_opts.restype = None
+    L.agcn_spmm_ex.argtypes = [c_vp, c_vp, c_vp, c_i32, c_vp, c_vp, ctypes.POINTER(SpmmOpts)]
+    L.agcn_spmm_ex.restype = c_i32
     L.agcn_plan_destroy.argtypes = [c_vp]
     L.agcn_plan_destroy.restype = c_i32
     L.agcn_plan_stats.argtypes = [c_vp, ctypes.POINTER(Stats)]
@@ -75,6 +86,7 @@ def lib():
     return L
 
 
-EXPORTS = ["agcn_default_opts", "agcn_plan", "agcn_plan_ex", "agcn_spmm", "agcn_plan_destroy",
+EXPORTS = ["agcn_default_opts", "agcn_plan", "agcn_plan_ex", "agcn_spmm", "agcn_default_spmm_opts",
+           "agcn_spmm_ex", "agcn_plan_destroy",
            "agcn_plan_stats", "agcn_plan_copy", "agcn_shard_bounds", "agcn_propagate_host",
            "agcn_last_status", "agcn_last_error", "agcn_launch_count", "agcn_version"]

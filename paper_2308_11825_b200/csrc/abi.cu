@@ -108,11 +108,23 @@ agcn_plan_t agcn_plan(const int32_t* rowptr, const int32_t* colidx, int64_t n, i
     return agcn_plan_ex(rowptr, colidx, n, nnz, nullptr);
 }
 
-agcn_status_t agcn_spmm(agcn_plan_t plan, const float* vals, const float* X, int32_t F, float* Y,
-                        agcn_stream_t stream) {
+void agcn_default_spmm_opts(agcn_spmm_opts_t* o) {
+    if (!o) return;
+    std::memset(o, 0, sizeof(*o));
+    o->kernel = AGCN_KERNEL_AUTO;
+    o->l2_hint = -1;
+}
+
+agcn_status_t agcn_spmm_ex(agcn_plan_t plan, const float* vals, const float* X, int32_t F, float* Y,
+                           agcn_stream_t stream, const agcn_spmm_opts_t* opts) {
     return guarded([&] {
         AGCN_CHECK(plan != nullptr, AGCN_ERR_INVALID_ARG, "plan is NULL");
         AGCN_CHECK(F > 0, AGCN_ERR_INVALID_ARG, "F must be > 0");
+        agcn_spmm_opts_t o;
+        if (opts) o = *opts; else agcn_default_spmm_opts(&o);
+        AGCN_CHECK(o.kernel == AGCN_KERNEL_AUTO || o.kernel == AGCN_KERNEL_GENERAL ||
+                       o.kernel == AGCN_KERNEL_WIDE, AGCN_ERR_INVALID_ARG, "unknown kernel");
+        AGCN_CHECK(o.l2_hint >= -1 && o.l2_hint <= 1, AGCN_ERR_INVALID_ARG, "l2_hint must be -1, 0 or 1");
         if (plan->n == 0) return;
         AGCN_CHECK(Y != nullptr, AGCN_ERR_INVALID_ARG, "Y is NULL");
         AGCN_CHECK(plan->nnz == 0 || (vals != nullptr && X != nullptr), AGCN_ERR_INVALID_ARG,
@@ -125,8 +137,13 @@ agcn_status_t agcn_spmm(agcn_plan_t plan, const float* vals, const float* X, int
             const size_t ny = sizeof(float) * (size_t)plan->n * F;
             AGCN_CHECK(!ranges_overlap(X, nx, Y, ny), AGCN_ERR_INVALID_ARG, "X and Y overlap");
         }
-        spmm_launch(plan, vals, X, F, Y, (cudaStream_t)stream);
+        spmm_launch(plan, vals, X, F, Y, (cudaStream_t)stream, o);
     });
+}
+
+agcn_status_t agcn_spmm(agcn_plan_t plan, const float* vals, const float* X, int32_t F, float* Y,
+                        agcn_stream_t stream) {
+    return agcn_spmm_ex(plan, vals, X, F, Y, stream, nullptr);
 }
 
 agcn_status_t agcn_plan_destroy(agcn_plan_t plan) {
@@ -194,11 +211,11 @@ agcn_status_t agcn_shard_bounds(const int32_t* rowptr, int64_t n, int32_t nranks
     return guarded([&] {
         AGCN_CHECK(rowptr && bounds_host && n >= 0 && nranks >= 1, AGCN_ERR_INVALID_ARG, "bad argument");
         cudaStream_t s = (cudaStream_t)stream;
-        int64_t* d = dalloc<int64_t>(nranks + 1, s);
+        Scratch tmp(s);
+        int64_t* d = tmp.alloc<int64_t>(nranks + 1);
         k_shard_bounds<<<(nranks + 1 + 127) / 128, 128, 0, s>>>(rowptr, n, nranks, d);
         post_launch();
         AGCN_CUDA(cudaMemcpyAsync(bounds_host, d, sizeof(int64_t) * (nranks + 1), cudaMemcpyDeviceToHost, s));
-        dfree(d, s);
         AGCN_CUDA(cudaStreamSynchronize(s));
     });
 }
@@ -217,42 +234,42 @@ agcn_status_t agcn_propagate_host(const int32_t* rowptr_h, const int32_t* colidx
         AGCN_CHECK(layers == 1 || n_cols == n, AGCN_ERR_INVALID_ARG, "layers > 1 needs a square A");
         cudaStream_t s = (cudaStream_t)o.stream;
         const size_t xb = sizeof(float) * (size_t)n_cols * F, yb = sizeof(float) * (size_t)n * F;
-        int32_t* rp = dalloc<int32_t>(n + 1, s);
-        int32_t* ci = dalloc<int32_t>(nnz, s);
-        float* va = dalloc<float>(nnz, s);
-        float* x = dalloc<float>((size_t)n_cols * F, s);
-        float* y = dalloc<float>((size_t)n * F, s);
-        float* y2 = layers > 1 ? dalloc<float>((size_t)n * F, s) : nullptr;
-        agcn_plan_s* plan = nullptr;
-        try {
-            // colidx_h / vals_h are indexed by rowptr values: copy the [rowptr[0], rowptr[n]) run
-            const int32_t base = rowptr_h[0];
-            AGCN_CUDA(cudaMemcpyAsync(rp, rowptr_h, sizeof(int32_t) * (n + 1), cudaMemcpyHostToDevice, s));
-            if (nnz) {
-                AGCN_CUDA(cudaMemcpyAsync(ci, colidx_h + base, sizeof(int32_t) * nnz, cudaMemcpyHostToDevice, s));
-                AGCN_CUDA(cudaMemcpyAsync(va, vals_h + base, sizeof(float) * nnz, cudaMemcpyHostToDevice, s));
+        struct Sync {       // the call is synchronous, also when it fails half-way (destroyed last)
+            cudaStream_t s;
+            ~Sync() { cudaStreamSynchronize(s); }
+        } sync{s};
+        struct PlanGuard {  // plan arrays + scratch released (stream-ordered) on every exit path
+            agcn_plan_s* p = nullptr;
+            ~PlanGuard() {
+                if (p) { free_plan_arrays(p); delete p; }
             }
-            AGCN_CUDA(cudaMemcpyAsync(x, X_h, xb, cudaMemcpyHostToDevice, s));
-            plan = build_plan(rp, ci - base, n, nnz, o);
-            const float* cur = x;
-            float* out = y;
-            for (int l = 0; l < layers; ++l) {
-                spmm_launch(plan, va - base, cur, F, out, s);
-                cur = out;
-                out = (out == y) ? y2 : y;
-            }
-            AGCN_CUDA(cudaMemcpyAsync(Y_h, cur, yb, cudaMemcpyDeviceToHost, s));
-            AGCN_CUDA(cudaStreamSynchronize(s));
-        } catch (...) {
-            cudaStreamSynchronize(s);
-            if (plan) { free_plan_arrays(plan); delete plan; }
-            dfree(rp, s); dfree(ci, s); dfree(va, s); dfree(x, s); dfree(y, s); dfree(y2, s);
-            cudaStreamSynchronize(s);
-            throw;
+        } pg;
+        Scratch tmp(s);
+        int32_t* rp = tmp.alloc<int32_t>(n + 1);
+        int32_t* ci = tmp.alloc<int32_t>(nnz);
+        float* va = tmp.alloc<float>(nnz);
+        float* x = tmp.alloc<float>((size_t)n_cols * F);
+        float* y = tmp.alloc<float>((size_t)n * F);
+        float* y2 = layers > 1 ? tmp.alloc<float>((size_t)n * F) : nullptr;
+        // colidx_h / vals_h are indexed by rowptr values: copy the [rowptr[0], rowptr[n]) run
+        const int32_t base = rowptr_h[0];
+        AGCN_CUDA(cudaMemcpyAsync(rp, rowptr_h, sizeof(int32_t) * (n + 1), cudaMemcpyHostToDevice, s));
+        if (nnz) {
+            AGCN_CUDA(cudaMemcpyAsync(ci, colidx_h + base, sizeof(int32_t) * nnz, cudaMemcpyHostToDevice, s));
+            AGCN_CUDA(cudaMemcpyAsync(va, vals_h + base, sizeof(float) * nnz, cudaMemcpyHostToDevice, s));
         }
-        free_plan_arrays(plan);
-        delete plan;
-        dfree(rp, s); dfree(ci, s); dfree(va, s); dfree(x, s); dfree(y, s); dfree(y2, s);
+        AGCN_CUDA(cudaMemcpyAsync(x, X_h, xb, cudaMemcpyHostToDevice, s));
+        pg.p = build_plan(rp, ci - base, n, nnz, o);
+        agcn_spmm_opts_t so;
+        agcn_default_spmm_opts(&so);
+        const float* cur = x;
+        float* out = y;
+        for (int l = 0; l < layers; ++l) {
+            spmm_launch(pg.p, va - base, cur, F, out, s, so);
+            cur = out;
+            out = (out == y) ? y2 : y;
+        }
+        AGCN_CUDA(cudaMemcpyAsync(Y_h, cur, yb, cudaMemcpyDeviceToHost, s));
         AGCN_CUDA(cudaStreamSynchronize(s));
     });
 }

@@ -6,6 +6,7 @@
 
 #include <atomic>
 #include <string>
+#include <vector>
 
 #include "../../include/agcn.h"
 #include "colmap.cuh"
@@ -59,6 +60,27 @@ inline void dfree(void* p, cudaStream_t s) {
     if (p) cudaFreeAsync(p, s);
 }
 
+// Temporaries of one call: freed stream-ordered when the scope ends (also on errors).
+class Scratch {
+public:
+    explicit Scratch(cudaStream_t s) : s_(s) {}
+    Scratch(const Scratch&) = delete;
+    Scratch& operator=(const Scratch&) = delete;
+    ~Scratch() {
+        for (void* p : ptrs_) cudaFreeAsync(p, s_);
+    }
+    template <class T>
+    T* alloc(size_t count) {
+        T* p = dalloc<T>(count, s_);
+        ptrs_.push_back(p);
+        return p;
+    }
+
+private:
+    cudaStream_t s_;
+    std::vector<void*> ptrs_;
+};
+
 // ------------------------------------------------------------------ scan (scan.cu)
 // out[i] = sum_{j<i} in[i] for i in [0, n]; out has n+1 entries (out[n] = total).
 // In-place (out == in) is allowed only if in has n+1 entries.  int32 values.
@@ -91,9 +113,9 @@ struct agcn_plan_s {
     int32_t* sorted_rowptr = nullptr;  // [n+1] row pointer of the degree-sorted CSR (P:295 (3))
     int32_t* row_src_off = nullptr;    // [n]   rowptr[perm[k]] - rowptr[0]
     const int32_t* colidx = nullptr;   // BORROWED caller colidx (indexed by rowptr values)
-    int32_t* sorted_colidx = nullptr;  // [nnz + 8] degree-sorted colidx (relabelled), heat class
-                                       // in bits 29-30 when `heat` (a SpMM cache hint)
-    bool heat = false;
+    const int32_t* cols = nullptr;     // what the SpMM reads, indexed like vals (rowptr-relative):
+                                       // colidx + rp_base, or cols_copy when relabelled
+    int32_t* cols_copy = nullptr;      // [nnz] plan-owned relabelled colidx (padded layout only)
     agcn::ColMap cmap{};               // optional padded-layout column relabel
     int4* desc = nullptr;              // [nblocks]
     int32_t* ov_chunk_start = nullptr; // [n_ov + 1]
@@ -102,7 +124,6 @@ struct agcn_plan_s {
     int64_t ntasks = 0;
     int4* tasks = nullptr;             // [ntasks] (row, col, len, 0)
     int32_t* rowptr_copy = nullptr;    // [n+1] (rebased to 0)
-    int32_t* colidx_copy = nullptr;    // [nnz]
 
     // SpMM scratch (oversized-row partial sums, chunk-major [ov_chunks][F])
     float* ov_partial = nullptr;
@@ -116,6 +137,10 @@ struct agcn_plan_s {
 
 namespace agcn {
 void spmm_launch(agcn_plan_s* p, const float* vals, const float* X, int32_t F, float* Y,
-                 cudaStream_t s);
+                 cudaStream_t s, const agcn_spmm_opts_t& o);
+// spmm_wide.cu: 256-bit-per-lane kernel for F in {8,...,256}
+bool wide_supported(const agcn_plan_s* p, const float* X, const float* Y, int32_t F);
+void launch_wide(agcn_plan_s* p, const float* vals, const float* X, int32_t F, float* Y,
+                 bool l2_keep, cudaStream_t s);
 int num_sms();
 }  // namespace agcn

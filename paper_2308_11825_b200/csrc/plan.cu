@@ -195,8 +195,10 @@ __device__ __forceinline__ int32_t bin_search(const int32_t* a, int32_t db, int3
 }
 
 // Colidx validation (0 <= colidx < n_cols), one flat coalesced pass over the nonzeros.
-__global__ void k_validate_cols(const int32_t* __restrict__ colidx, int64_t nnz, int64_t n_cols,
-                                PlanFlags* __restrict__ flags) {
+// colidx is indexed by rowptr values: the run starts at colidx[rowptr[0]] (read on device).
+__global__ void k_validate_cols(const int32_t* __restrict__ rowptr, const int32_t* __restrict__ colidx_g,
+                                int64_t nnz, int64_t n_cols, PlanFlags* __restrict__ flags) {
+    const int32_t* __restrict__ colidx = colidx_g + __ldg(rowptr);
     int32_t bad = 0;
     for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < nnz;
          q += (int64_t)gridDim.x * blockDim.x) {
@@ -207,15 +209,15 @@ __global__ void k_validate_cols(const int32_t* __restrict__ colidx, int64_t nnz,
 }
 
 // Introspection only (agcn_plan_copy(AGCN_FIELD_SORTED_COLIDX)): materialise the colidx of the
-// degree-sorted CSR, one warp per sorted row.  Not on the plan / SpMM path.
+// degree-sorted CSR, one warp per sorted row.  Not on the plan / SpMM path (the SpMM reads
+// the caller's colidx through row_src_off).
 __global__ void k_gather_sorted_cols(int64_t n, const int32_t* __restrict__ sorted_rowptr,
                                      const int32_t* __restrict__ rso,
-                                     const int32_t* __restrict__ colidx, ColMap cm,
-                                     int32_t* __restrict__ out) {
+                                     const int32_t* __restrict__ cols, int32_t* __restrict__ out) {
     const int64_t k = (int64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
     if (k >= n) return;
     const int32_t dst = sorted_rowptr[k], d = sorted_rowptr[k + 1] - dst, src = rso[k];
-    for (int32_t j = threadIdx.x & 31; j < d; j += 32) out[dst + j] = map_col(colidx[src + j], cm);
+    for (int32_t j = threadIdx.x & 31; j < d; j += 32) out[dst + j] = cols[src + j];
 }
 
 // ---------------------------------------------------------------- (5) Algorithm 2 emission
@@ -265,81 +267,6 @@ __global__ void k_emit_ov(const int32_t* __restrict__ sorted_rowptr, int64_t ov_
     const int32_t c0 = chunk_start[k], nc = chunk_start[k + 1] - c0;
     for (int32_t j = threadIdx.x & 31; j < nc; j += 32)
         desc[nb_small + c0 + j] = make_int4(d, loc + j * db, row, min(db, d - j * db));
-}
-
-// ---------------------------------------------------------------- column heat (L2 hint)
-// Not part of the paper's metadata: a B200 cache-residency hint for the SpMM.  Columns are
-// ranked by (sampled) in-degree; the top K3 < K2 < K1 columns get heat class 3 / 2 / 1, stored
-// in bits 29-30 of the plan's degree-sorted colidx.  agcn_spmm keeps rows of hot classes in L2
-// with an evict_last policy (how many classes depends on F: the hot rows must fit in L2).
-constexpr int kHeatSample = 8;   // count every 8th nonzero
-constexpr int kHeatBins = 4096;  // sampled counts are capped into this many bins
-constexpr int kHeatShift = 29;
-__device__ __constant__ int64_t kHeatK[3] = {384 * 1024, 192 * 1024, 96 * 1024};
-
-__global__ void k_col_count(const int32_t* __restrict__ colidx, int64_t nnz, int32_t* __restrict__ cnt) {
-    for (int64_t q = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * kHeatSample; q < nnz;
-         q += (int64_t)gridDim.x * blockDim.x * kHeatSample)
-        atomicAdd(&cnt[__ldcs(colidx + q)], 1);
-}
-
-__global__ void k_count_hist(const int32_t* __restrict__ cnt, int64_t n_cols, int32_t* __restrict__ hist) {
-    __shared__ int32_t h[kHeatBins];
-    for (int b = threadIdx.x; b < kHeatBins; b += blockDim.x) h[b] = 0;
-    __syncthreads();
-    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n_cols; j += (int64_t)gridDim.x * blockDim.x)
-        atomicAdd(&h[min(cnt[j], kHeatBins - 1)], 1);
-    __syncthreads();
-    for (int b = threadIdx.x; b < kHeatBins; b += blockDim.x)
-        if (h[b]) atomicAdd(&hist[b], h[b]);
-}
-
-// thr[k] = lowest count c >= 1 such that #columns with count >= c is <= kHeatK[k]
-__global__ void k_heat_thresholds(const int32_t* __restrict__ hist, int32_t* __restrict__ thr) {
-    if (threadIdx.x != 0 || blockIdx.x != 0) return;
-    int64_t acc = 0;
-    int32_t t[3] = {kHeatBins, kHeatBins, kHeatBins};
-    for (int b = kHeatBins - 1; b >= 1; --b) {
-        acc += hist[b];
-        for (int k = 0; k < 3; ++k)
-            if (acc <= kHeatK[k]) t[k] = b;
-    }
-    for (int k = 0; k < 3; ++k) thr[k] = t[k];
-}
-
-// Degree-sorted colidx (relabelled, heat class in bits 29-30), one warp per descriptor: the
-// descriptor's nonzeros are contiguous in the sorted order, its rows start at row_src_off.
-__global__ void __launch_bounds__(kThreads) k_gather_cols(
-    const int4* __restrict__ desc, int64_t nblocks, int32_t db, const int32_t* __restrict__ rso,
-    const int32_t* __restrict__ srp, const int32_t* __restrict__ colidx, ColMap cm,
-    const int32_t* __restrict__ cnt, const int32_t* __restrict__ thr, int32_t* __restrict__ out) {
-    const int lane = threadIdx.x & 31;
-    int32_t t0 = 0, t1 = 0, t2 = 0;
-    if (cnt) { t0 = thr[0]; t1 = thr[1]; t2 = thr[2]; }
-    for (int64_t b = (int64_t)blockIdx.x * kWarps + (threadIdx.x >> 5); b < nblocks;
-         b += (int64_t)gridDim.x * kWarps) {
-        const int4 m = desc[b];
-        const bool ov = m.x > db;
-        const int32_t d = m.x, loc = m.y, row0 = m.z;
-        const int32_t total = ov ? m.w : (m.w & 0xffff) * d;
-        const int32_t vbase0 = ov ? rso[row0] + (loc - srp[row0]) : 0;
-        for (int32_t e = lane; e < total; e += 32) {
-            int32_t off;
-            if (ov) {
-                off = vbase0 + e;
-            } else {
-                const int32_t r = e / d;
-                off = rso[row0 + r] + (e - r * d);
-            }
-            const int32_t c = __ldcs(colidx + off);
-            int32_t v = map_col(c, cm);
-            if (cnt) {
-                const int32_t k = __ldg(cnt + c);
-                v |= ((k >= t0) + (k >= t1) + (k >= t2)) << kHeatShift;
-            }
-            out[loc + e] = v;
-        }
-    }
 }
 
 // ---------------------------------------------------------------- warp-level partition
@@ -432,12 +359,29 @@ void check_csr_flags(const PlanFlags& f, int64_t nnz) {
 
 // First phase shared by both partitions: validate colidx (optional, flat pass) then read the
 // flags once.  This is the plan's only host synchronisation.
-void validate_cols(const int32_t* colidx, int64_t nnz, int64_t n_cols, PlanFlags* d_flags,
-                   cudaStream_t s) {
+void validate_cols(const int32_t* rowptr, const int32_t* colidx, int64_t nnz, int64_t n_cols,
+                   PlanFlags* d_flags, cudaStream_t s) {
     if (nnz == 0) return;
     const unsigned g = (unsigned)std::min<int64_t>(blocks_for(nnz, 256), 148 * 16);
-    k_validate_cols<<<g, 256, 0, s>>>(colidx, nnz, n_cols, d_flags);
+    k_validate_cols<<<g, 256, 0, s>>>(rowptr, colidx, nnz, n_cols, d_flags);
     post_launch();
+}
+
+// The column array the SpMM reads (indexed like vals, rowptr-relative): the caller's colidx,
+// or -- for a padded multi-GPU layout -- a plan-owned relabelled copy (one flat pass).
+void set_spmm_cols(agcn_plan_s* p, const int32_t* colidx, cudaStream_t s) {
+    if (p->cmap.nparts <= 0) {
+        p->cols = colidx + p->rp_base;
+        return;
+    }
+    p->cols_copy = dalloc<int32_t>(p->nnz, s);
+    p->device_bytes += sizeof(int32_t) * (size_t)p->nnz;
+    if (p->nnz > 0) {
+        k_copy_cols<<<(unsigned)std::min<int64_t>(blocks_for(p->nnz, 256), 148 * 16), 256, 0, s>>>(
+            colidx + p->rp_base, p->nnz, p->cols_copy, p->cmap);
+        post_launch();
+    }
+    p->cols = p->cols_copy;
 }
 
 // ---------------------------------------------------------------- block-partition plan
@@ -447,9 +391,10 @@ void build_block_plan(agcn_plan_s* p, const int32_t* rowptr, const int32_t* coli
     const int32_t db = p->deg_bound, nbins = db + 2;
     const int64_t ntiles = std::max<int64_t>(1, (n + kTile - 1) / kTile);
 
-    PlanFlags* d_flags = dalloc<PlanFlags>(1, s);
-    int32_t* bin_cnt = dalloc<int32_t>(nbins, s);
-    int32_t* table = dalloc<int32_t>((size_t)nbins * ntiles + 1, s);
+    Scratch tmp(s);
+    PlanFlags* d_flags = tmp.alloc<PlanFlags>(1);
+    int32_t* bin_cnt = tmp.alloc<int32_t>(nbins);
+    int32_t* table = tmp.alloc<int32_t>((size_t)nbins * ntiles + 1);
     AGCN_CUDA(cudaMemsetAsync(d_flags, 0, sizeof(PlanFlags), s));
     AGCN_CUDA(cudaMemsetAsync(bin_cnt, 0, sizeof(int32_t) * nbins, s));
 
@@ -457,12 +402,7 @@ void build_block_plan(agcn_plan_s* p, const int32_t* rowptr, const int32_t* coli
     k_deg_hist<<<(unsigned)ntiles, kThreads, nbins * sizeof(int32_t), s>>>(rowptr, n, db, nbins, ntiles,
                                                                          table, bin_cnt, d_flags);
     post_launch();
-    if (o.validate) {
-        int32_t first = 0;  // colidx is indexed by rowptr values; the run starts at rowptr[0]
-        AGCN_CUDA(cudaMemcpyAsync(&first, rowptr, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
-        AGCN_CUDA(cudaStreamSynchronize(s));
-        validate_cols(colidx + first, nnz, p->n_cols, d_flags, s);
-    }
+    if (o.validate) validate_cols(rowptr, colidx, nnz, p->n_cols, d_flags, s);
     exclusive_scan_i32(table, table, (int64_t)nbins * ntiles, s);
 
     std::vector<int32_t> h_cnt(nbins);
@@ -532,11 +472,11 @@ void build_block_plan(agcn_plan_s* p, const int32_t* rowptr, const int32_t* coli
         int passes = 0;
         for (int64_t v = p->max_deg; v > 0; v >>= 8) ++passes;
         const int64_t mt = (m + kTile - 1) / kTile;
-        int32_t* ka = dalloc<int32_t>(m, s);
-        int32_t* va = dalloc<int32_t>(m, s);
-        int32_t* kb = dalloc<int32_t>(m, s);
-        int32_t* vb = dalloc<int32_t>(m, s);
-        int32_t* rt = dalloc<int32_t>(256 * mt + 1, s);
+        int32_t* ka = tmp.alloc<int32_t>(m);
+        int32_t* va = tmp.alloc<int32_t>(m);
+        int32_t* kb = tmp.alloc<int32_t>(m);
+        int32_t* vb = tmp.alloc<int32_t>(m);
+        int32_t* rt = tmp.alloc<int32_t>(256 * mt + 1);
         k_ov_init<<<blocks_for(m, 256), 256, 0, s>>>(p->perm + p->ov_start, rowptr, m, ka, va);
         post_launch();
         for (int pass = 0; pass < passes; ++pass) {
@@ -552,7 +492,6 @@ void build_block_plan(agcn_plan_s* p, const int32_t* rowptr, const int32_t* coli
         }
         AGCN_CUDA(cudaMemcpyAsync(p->perm + p->ov_start, va, sizeof(int32_t) * m,
                                   cudaMemcpyDeviceToDevice, s));
-        dfree(ka, s); dfree(va, s); dfree(kb, s); dfree(vb, s); dfree(rt, s);
     }
 
     // (3) "updating the row pointer array to reflect the new row order", O(n):
@@ -566,7 +505,7 @@ void build_block_plan(agcn_plan_s* p, const int32_t* rowptr, const int32_t* coli
     exclusive_scan_i32(p->sorted_rowptr, p->sorted_rowptr, n, s);
 
     // (4)+(5) Algorithm 1/2 descriptors
-    int32_t* d_tab = dalloc<int32_t>(6 * W, s);
+    int32_t* d_tab = tmp.alloc<int32_t>(6 * W);
     AGCN_CUDA(cudaMemcpyAsync(d_tab, tab.data(), sizeof(int32_t) * 6 * W, cudaMemcpyHostToDevice, s));
     if (p->nb_small > 0) {
         unsigned g = (unsigned)std::min<int64_t>(blocks_for(p->nb_small, kThreads), 148 * 8);
@@ -589,52 +528,22 @@ void build_block_plan(agcn_plan_s* p, const int32_t* rowptr, const int32_t* coli
         AGCN_CUDA(cudaMemsetAsync(p->ov_chunk_start, 0, sizeof(int32_t), s));
     }
 
-    // Degree-sorted colidx for the SpMM's contiguous staging, with column heat classes.
-    p->sorted_colidx = dalloc<int32_t>(nnz + 8, s);
-    p->device_bytes += sizeof(int32_t) * (size_t)(nnz + 8);
-    AGCN_CUDA(cudaMemsetAsync(p->sorted_colidx + nnz, 0, 8 * sizeof(int32_t), s));
-    p->heat = p->x_rows < (1ll << kHeatShift) && nnz > 0;
-    int32_t *cnt = nullptr, *hist = nullptr, *thr = nullptr;
-    if (p->heat) {
-        cnt = dalloc<int32_t>(p->n_cols, s);
-        hist = dalloc<int32_t>(kHeatBins, s);
-        thr = dalloc<int32_t>(3, s);
-        AGCN_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int32_t) * p->n_cols, s));
-        AGCN_CUDA(cudaMemsetAsync(hist, 0, sizeof(int32_t) * kHeatBins, s));
-        const unsigned g = (unsigned)std::min<int64_t>(blocks_for(nnz / kHeatSample + 1, 256), 148 * 8);
-        k_col_count<<<g, 256, 0, s>>>(colidx + p->rp_base, nnz, cnt);
-        post_launch();
-        k_count_hist<<<(unsigned)std::min<int64_t>(blocks_for(p->n_cols, 256), 148 * 2), 256, 0, s>>>(
-            cnt, p->n_cols, hist);
-        post_launch();
-        k_heat_thresholds<<<1, 32, 0, s>>>(hist, thr);
-        post_launch();
-    }
-    if (p->nblocks > 0) {
-        const unsigned g = (unsigned)std::min<int64_t>(blocks_for(p->nblocks, kWarps), 148 * 16);
-        k_gather_cols<<<g, kThreads, 0, s>>>(p->desc, p->nblocks, db, p->row_src_off, p->sorted_rowptr,
-                                              colidx + p->rp_base, p->cmap, cnt, thr, p->sorted_colidx);
-        post_launch();
-    }
-    dfree(cnt, s); dfree(hist, s); dfree(thr, s);
-    dfree(d_tab, s); dfree(table, s); dfree(bin_cnt, s); dfree(d_flags, s);
+    set_spmm_cols(p, colidx, s);
 }
 
 // ---------------------------------------------------------------- warp-partition plan
 void build_warp_plan(agcn_plan_s* p, const int32_t* rowptr, const int32_t* colidx,
                      const agcn_opts_t& o, cudaStream_t s) {
     const int64_t n = p->n, nnz = p->nnz;
-    PlanFlags* d_flags = dalloc<PlanFlags>(1, s);
+    Scratch tmp(s);
+    PlanFlags* d_flags = tmp.alloc<PlanFlags>(1);
     AGCN_CUDA(cudaMemsetAsync(d_flags, 0, sizeof(PlanFlags), s));
     p->rowptr_copy = dalloc<int32_t>(n + 1, s);
-    int32_t* tstart = dalloc<int32_t>(n + 1, s);
+    int32_t* tstart = tmp.alloc<int32_t>(n + 1);
     k_rowptr_check<<<blocks_for(n + 1, 256), 256, 0, s>>>(rowptr, n, p->mwn, p->rowptr_copy, tstart,
                                                           d_flags);
     post_launch();
-    int32_t first = 0;
-    AGCN_CUDA(cudaMemcpyAsync(&first, rowptr, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
-    AGCN_CUDA(cudaStreamSynchronize(s));
-    if (o.validate) validate_cols(colidx + first, nnz, p->n_cols, d_flags, s);
+    if (o.validate) validate_cols(rowptr, colidx, nnz, p->n_cols, d_flags, s);
     exclusive_scan_i32(tstart, tstart, n, s);
     int32_t ntasks = 0;
     AGCN_CUDA(cudaMemcpyAsync(&ntasks, tstart + n, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
@@ -645,26 +554,20 @@ void build_warp_plan(agcn_plan_s* p, const int32_t* rowptr, const int32_t* colid
     p->ntasks = ntasks;
     p->max_deg = hf.max_deg;
     p->rp_base = hf.rowptr_first;
-    p->colidx_copy = dalloc<int32_t>(nnz, s);
     p->tasks = dalloc<int4>(ntasks, s);
-    p->device_bytes = sizeof(int32_t) * (size_t)(n + 1 + nnz) + sizeof(int4) * (size_t)ntasks;
-    if (nnz > 0) {
-        k_copy_cols<<<(unsigned)std::min<int64_t>(blocks_for(nnz, 256), 148 * 16), 256, 0, s>>>(
-            colidx + p->rp_base, nnz, p->colidx_copy, p->cmap);
-        post_launch();
-    }
+    p->device_bytes = sizeof(int32_t) * (size_t)(n + 1) + sizeof(int4) * (size_t)ntasks;
+    set_spmm_cols(p, colidx, s);
     if (n > 0) {
         k_emit_tasks<<<blocks_for(n, 256), 256, 0, s>>>(p->rowptr_copy, n, p->mwn, tstart, p->tasks);
         post_launch();
     }
-    dfree(tstart, s); dfree(d_flags, s);
 }
 
 }  // namespace
 
 void free_plan_arrays(agcn_plan_s* p) {
     void* ptrs[] = {p->perm,  p->sorted_rowptr, p->row_src_off, p->desc,       p->ov_chunk_start,
-                    p->tasks, p->rowptr_copy,   p->colidx_copy, p->ov_partial, p->sorted_colidx};
+                    p->tasks, p->rowptr_copy,   p->cols_copy,   p->ov_partial};
     // Stream-ordered release on the plan's stream, after the last SpMM that used the plan on
     // another stream (p->last_use); no host synchronisation.
     if (p->last_use) cudaStreamWaitEvent(p->stream, p->last_use, 0);
@@ -674,26 +577,18 @@ void free_plan_arrays(agcn_plan_s* p) {
     if (p->last_use) cudaEventDestroy(p->last_use);
 }
 
-// Degree-sorted colidx for introspection (parity tests): the plan's array without heat bits.
+// Degree-sorted colidx for introspection (parity tests), gathered on demand.
 void plan_copy_sorted_colidx(agcn_plan_s* p, int32_t* host_dst) {
     if (p->nnz == 0) return;
     cudaStream_t s = p->stream;
-    if (p->sorted_colidx) {
-        AGCN_CUDA(cudaMemcpyAsync(host_dst, p->sorted_colidx, sizeof(int32_t) * p->nnz,
-                                  cudaMemcpyDeviceToHost, s));
-        AGCN_CUDA(cudaStreamSynchronize(s));
-        if (p->heat)
-            for (int64_t i = 0; i < p->nnz; ++i) host_dst[i] &= (1 << kHeatShift) - 1;
-        return;
-    }
-    int32_t* d = dalloc<int32_t>(p->nnz, s);  // warp partition: gather in degree order
-    if (p->n > 0) {
+    Scratch tmp(s);
+    int32_t* d = tmp.alloc<int32_t>(p->nnz);
+    if (p->n > 0 && p->sorted_rowptr) {
         k_gather_sorted_cols<<<blocks_for(p->n, kWarps), kThreads, 0, s>>>(
-            p->n, p->sorted_rowptr, p->row_src_off, p->colidx + p->rp_base, p->cmap, d);
+            p->n, p->sorted_rowptr, p->row_src_off, p->cols, d);
         post_launch();
     }
     AGCN_CUDA(cudaMemcpyAsync(host_dst, d, sizeof(int32_t) * p->nnz, cudaMemcpyDeviceToHost, s));
-    dfree(d, s);
     AGCN_CUDA(cudaStreamSynchronize(s));
 }
 

@@ -97,14 +97,14 @@ void exclusive_scan_i32(const int32_t* in, int32_t* out, int64_t n, cudaStream_t
         return;
     }
     const int64_t ntiles = (n + kScanTile - 1) / kScanTile;
-    int32_t* sums = dalloc<int32_t>(ntiles + 1, s);
+    Scratch tmp(s);
+    int32_t* sums = tmp.alloc<int32_t>(ntiles + 1);
     k_tile_reduce<<<(unsigned)ntiles, kScanThreads, 0, s>>>(in, n, sums);
     post_launch();
     k_scan_sums<<<1, kScanThreads, 0, s>>>(sums, ntiles);
     post_launch();
     k_tile_scan<<<(unsigned)ntiles, kScanThreads, 0, s>>>(in, out, n, sums, ntiles);
     post_launch();
-    dfree(sums, s);
 }
 
 }  // namespace agcn

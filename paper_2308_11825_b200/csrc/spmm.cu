@@ -27,6 +27,7 @@ namespace agcn {
 namespace {
 
 constexpr int kWarpsPerCta = 8;
+constexpr double kL2KeepBytes = 128.0 * 1024 * 1024;  // X up to ~L2 size gets evict_last hints
 
 int env_int(const char* name, int dflt) {  // experiment switches
     const char* v = getenv(name);
@@ -63,37 +64,23 @@ __device__ __forceinline__ void vadd(float4& a, const float4& b) {
 }
 __device__ __forceinline__ void vadd(float& a, float b) { a += b; }
 
-// X-row gather loads, read-only path.  Flavour (uniform per launch):
-//   bit 0: L1::no_allocate     bit 1: L2::cache_hint with an evict_last policy
-__device__ __forceinline__ float4 ldx(const float4* p, int mode, uint64_t pol) {
+// X-row gather loads (read-only path); with keep, an L2 evict_last cache-policy hint (X fits
+// in L2).  pol comes from policy_evict_last().
+__device__ __forceinline__ float4 ldx(const float4* p, bool keep, uint64_t pol) {
     float4 v;
-    switch (mode) {
-        case 1:
-            asm("ld.global.nc.L1::no_allocate.v4.f32 {%0, %1, %2, %3}, [%4];"
-                : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p));
-            break;
-        case 2:
-            asm("ld.global.nc.L2::cache_hint.v4.f32 {%0, %1, %2, %3}, [%4], %5;"
-                : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p), "l"(pol));
-            break;
-        case 3:
-            asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.f32 {%0, %1, %2, %3}, [%4], %5;"
-                : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p), "l"(pol));
-            break;
-        default: v = __ldg(p);
-    }
+    if (keep)
+        asm("ld.global.nc.L2::cache_hint.v4.f32 {%0, %1, %2, %3}, [%4], %5;"
+            : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p), "l"(pol));
+    else
+        v = __ldg(p);
     return v;
 }
-__device__ __forceinline__ float ldx(const float* p, int mode, uint64_t pol) {
+__device__ __forceinline__ float ldx(const float* p, bool keep, uint64_t pol) {
     float v;
-    switch (mode) {
-        case 1: asm("ld.global.nc.L1::no_allocate.f32 %0, [%1];" : "=f"(v) : "l"(p)); break;
-        case 2: asm("ld.global.nc.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(p), "l"(pol)); break;
-        case 3:
-            asm("ld.global.nc.L1::no_allocate.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(p), "l"(pol));
-            break;
-        default: v = __ldg(p);
-    }
+    if (keep)
+        asm("ld.global.nc.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(p), "l"(pol));
+    else
+        v = __ldg(p);
     return v;
 }
 __device__ __forceinline__ uint64_t policy_evict_last() {
@@ -115,7 +102,7 @@ struct BlockArgs {
     int32_t db;             // deg_bound
     int32_t stage;          // shared-memory entries per warp (>= db + 8, multiple of 4)
     int32_t rso_stage;      // shared-memory row offsets per warp (>= max_block_warps)
-    const int32_t* scol;    // plan's degree-sorted colidx (relabelled; heat class in bits 29-30)
+    const int32_t* cols;    // column indices, indexed like vals (rowptr-relative)
     const int32_t* srp;     // sorted rowptr
     const int32_t* rso;     // row_src_off
     const int32_t* perm;    // sorted -> original row
@@ -125,7 +112,7 @@ struct BlockArgs {
     float* ovp;             // oversized partials [ov_chunks][FV]
     int64_t n_zero;         // sorted rows [0, n_zero) have degree 0
     int32_t FV;             // vectors per row (F/4 on the float4 path, F otherwise)
-    int32_t xmode;          // X-load flavour (see ldx)
+    int32_t keep;           // X loads with an L2 evict_last hint
 };
 
 template <int L, int T, bool V4, int U>
@@ -147,7 +134,7 @@ __global__ void __launch_bounds__(kCtaThreads, 4) k_spmm_block(const __grid_cons
     const int32_t FV = a.FV;
     const int64_t gw = (int64_t)blockIdx.x * kWarpsPerCta + warp;
     const int64_t W = (int64_t)gridDim.x * kWarpsPerCta;
-    const int xmode = a.xmode;
+    const bool keep = a.keep;
     const uint64_t pol = policy_evict_last();
 
     // degree-0 rows: Y row = 0 (reading Q16)
@@ -187,7 +174,7 @@ __global__ void __launch_bounds__(kCtaThreads, 4) k_spmm_block(const __grid_cons
                 const int32_t r = e / d;
                 off = s_rso[r] + (e - r * d);
             }
-            s_col[e] = ldcs_i(a.scol + loc + e) & ((1 << 29) - 1);
+            s_col[e] = ldcs_i(a.cols + off);
             s_val[e] = ldcs_f(a.vals + off);
         }
         __syncwarp();
@@ -236,7 +223,7 @@ __global__ void __launch_bounds__(kCtaThreads, 4) k_spmm_block(const __grid_cons
                     for (int t = 0; t < T; ++t) {
                         const int32_t c = cc + li + t * L;
                         if (ok && c < FV)
-                            xv[u][t] = ldx(X + (int64_t)col[u] * FV + c, xmode, pol);
+                            xv[u][t] = ldx(X + (int64_t)col[u] * FV + c, keep, pol);
                         else
                             vzero(xv[u][t]);
                     }
@@ -283,163 +270,6 @@ __global__ void __launch_bounds__(kCtaThreads, 4) k_spmm_block(const __grid_cons
             }
             __syncwarp();
         }
-    }
-}
-
-// ---------------------------------------------------------------- lean fast path
-// Same mapping and results as k_spmm_block for the common shape (float4 path, one vector
-// per lane: F % 4 == 0, F <= 128), written for occupancy: the gather of X rows is latency
-// bound and B200 sustains ~18 TB/s of L2->SM gather only with ~64 resident warps/SM
-// (tools/gather_probe.cu), so the hot loop keeps only the 4 in-flight rows, the accumulator
-// and a countdown to the end of the current row segment in registers; everything per-row
-// happens in the cold flush path.
-struct LeanArgs {
-    const int4* desc;
-    int64_t nblocks;
-    int64_t first_ov;
-    int64_t n_zero;
-    const int32_t* scol;    // plan's degree-sorted colidx (relabelled; heat class in bits 29-30)
-    const int32_t* srp;
-    const int32_t* rso;
-    const int32_t* perm;
-    const float* vals;      // caller vals, offset by rowptr[0]
-    const float4* X;
-    float4* Y;
-    float4* ovp;
-    int32_t db, stage, rso_stage, FV;
-    int32_t min_cls;        // heat class from which X rows are kept in L2 (evict_last); 4: none
-};
-
-// X-row load with the L2 residency hint: hot rows evict_last, the rest default priority.
-__device__ __forceinline__ float4 ldx_heat(const float4* p, bool hot, uint64_t pol) {
-    float4 v;
-    if (hot)
-        asm("ld.global.nc.L2::cache_hint.v4.f32 {%0, %1, %2, %3}, [%4], %5;"
-            : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p), "l"(pol));
-    else
-        v = __ldg(p);
-    return v;
-}
-
-template <int L>
-__global__ void __launch_bounds__(kCtaThreads, 6) k_spmm_lean(const __grid_constant__ LeanArgs a) {
-    constexpr int G = 32 / L;
-    constexpr int32_t kColMask = (1 << 29) - 1;
-    extern __shared__ __align__(16) unsigned char smem[];
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int s = lane / L, li = lane % L;
-    const int per_warp = 2 * a.stage + 2 * a.rso_stage;
-    int32_t* s_col = reinterpret_cast<int32_t*>(smem) + warp * per_warp;
-    float* s_val = reinterpret_cast<float*>(s_col + a.stage);
-    int32_t* s_rso = s_col + 2 * a.stage;
-    int32_t* s_perm = s_rso + a.rso_stage;
-    const uint64_t pol = policy_evict_last();
-    float4* s_part = reinterpret_cast<float4*>(smem + (size_t)kWarpsPerCta * per_warp * 4) + warp * (2 * 32);
-    const int32_t FV = a.FV;
-    const bool lane_on = li < FV;
-    const int64_t gw = (int64_t)blockIdx.x * kWarpsPerCta + warp;
-    const int64_t W = (int64_t)gridDim.x * kWarpsPerCta;
-
-    for (int64_t r = gw * G + s; r < a.n_zero; r += W * G)  // degree-0 rows (Q16)
-        if (lane_on) sty(a.Y + (int64_t)a.perm[r] * FV + li, vzero4());
-
-    const float4* __restrict__ Xl = a.X + li;
-    for (int64_t b = gw; b < a.nblocks; b += W) {
-        const int4 m = __ldg(a.desc + b);
-        const bool ov = m.x > a.db;
-        const int32_t d = m.x, loc = m.y, row0 = m.z;
-        const int32_t total = ov ? m.w : (m.w & 0xffff) * d;
-        const int32_t seg = ov ? total : d;
-
-        // ---- stage: colidx contiguous from the plan's sorted array; vals through row_src_off;
-        // perm of the descriptor's rows (for the stores)
-        __syncwarp();
-        int32_t vbase0 = 0;
-        if (ov) {
-            vbase0 = __ldg(a.rso + row0) + (loc - __ldg(a.srp + row0));
-        } else {
-            for (int32_t r = lane; r < (m.w & 0xffff); r += 32) {
-                s_rso[r] = __ldg(a.rso + row0 + r);
-                s_perm[r] = __ldg(a.perm + row0 + r);
-            }
-            __syncwarp();
-        }
-        for (int32_t e = lane; e < total; e += 32) {
-            s_col[e] = ldcs_i(a.scol + loc + e);
-            int32_t off;
-            if (ov) {
-                off = vbase0 + e;
-            } else {
-                const int32_t r = e / d;
-                off = s_rso[r] + (e - r * d);
-            }
-            s_val[e] = ldcs_f(a.vals + off);
-        }
-        __syncwarp();
-
-        const int32_t Q = (((total + G - 1) / G) + 3) & ~3;
-        const int32_t q0 = min(s * Q, total), q1 = min(q0 + Q, total);
-        float4 acc = vzero4();
-        int32_t left = seg - (q0 % seg);  // entries left in the current row segment
-
-        // cold path: a row segment ends at q_end
-        auto flush = [&](int32_t q_end) {
-            const int32_t rstart = q_end + 1 - seg;
-            if (rstart >= q0) {
-                if (lane_on) {
-                    float4* dst = ov ? a.ovp + (b - a.first_ov) * (int64_t)FV
-                                     : a.Y + (int64_t)s_perm[rstart / seg] * FV;
-                    sty(dst + li, acc);
-                }
-            } else {
-                s_part[s * 2 * L + li] = acc;  // head partial: finished below
-            }
-            acc = vzero4();
-            left = seg;
-        };
-
-        for (int32_t q = q0; q < q1; q += 4) {
-            const int4 c = *reinterpret_cast<const int4*>(s_col + q);
-            const float4 z = vzero4();
-            const int32_t mc = a.min_cls;
-            const float4 x0 = (lane_on) ? ldx_heat(Xl + (int64_t)(c.x & kColMask) * FV, (c.x >> 29) >= mc, pol) : z;
-            const float4 x1 = (lane_on && q + 1 < q1) ? ldx_heat(Xl + (int64_t)(c.y & kColMask) * FV, (c.y >> 29) >= mc, pol) : z;
-            const float4 x2 = (lane_on && q + 2 < q1) ? ldx_heat(Xl + (int64_t)(c.z & kColMask) * FV, (c.z >> 29) >= mc, pol) : z;
-            const float4 x3 = (lane_on && q + 3 < q1) ? ldx_heat(Xl + (int64_t)(c.w & kColMask) * FV, (c.w >> 29) >= mc, pol) : z;
-            const float4 v = *reinterpret_cast<const float4*>(s_val + q);
-            vfma(acc, v.x, x0);
-            if (--left == 0) flush(q);
-            if (q + 1 < q1) {
-                vfma(acc, v.y, x1);
-                if (--left == 0) flush(q + 1);
-            }
-            if (q + 2 < q1) {
-                vfma(acc, v.z, x2);
-                if (--left == 0) flush(q + 2);
-            }
-            if (q + 3 < q1) {
-                vfma(acc, v.w, x3);
-                if (--left == 0) flush(q + 3);
-            }
-        }
-        if (q1 > q0 && left < seg) {  // range ends inside a row: tail (1) or middle (0) partial
-            const int32_t cs = q1 - (seg - left);
-            s_part[(s * 2 + (cs >= q0 ? 1 : 0)) * L + li] = acc;
-        }
-        __syncwarp();
-        const int32_t h = q0 % seg;
-        if (q1 > q0 && h != 0 && q0 - h + seg <= q1) {  // we finish a row begun earlier
-            const int32_t fin_rs = q0 - h;
-            const int s_first = fin_rs / Q;
-            float4 sum = s_part[(s_first * 2 + 1) * L + li];
-            for (int s2 = s_first + 1; s2 <= s; ++s2) vadd(sum, s_part[(s2 * 2) * L + li]);
-            if (lane_on) {
-                float4* dst = ov ? a.ovp + (b - a.first_ov) * (int64_t)FV
-                                 : a.Y + (int64_t)s_perm[fin_rs / seg] * FV;
-                sty(dst + li, sum);
-            }
-        }
-        __syncwarp();
     }
 }
 
@@ -540,7 +370,7 @@ __global__ void __launch_bounds__(kCtaThreads) k_spmm_warp(const WarpArgs a) {
                     for (int i = 0; i < T; ++i) {
                         const int32_t c = cc + li + i * L;
                         if (q + u < len && c < FV)
-                            xv[u][i] = ldx(X + (int64_t)col[u] * FV + c, 0, 0);
+                            xv[u][i] = ldx(X + (int64_t)col[u] * FV + c, false, 0);
                         else
                             vzero(xv[u][i]);
                     }
@@ -598,8 +428,6 @@ void launch_block_u(const BlockArgs& a, cudaStream_t s, size_t smem) {
     static size_t occ_smem = 0;
     if (occ < 0 || occ_smem != smem) {
         AGCN_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-        static const int carve = env_int("AGCN_CARVEOUT", -1);
-        if (carve >= 0) AGCN_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, carve));
         AGCN_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kCtaThreads, smem));
         if (occ < 1) occ = 1;
         occ_smem = smem;
@@ -667,26 +495,6 @@ void launch_warp(const WarpArgs& a, cudaStream_t s) {
         }                                                                            \
     } while (0)
 
-template <int L>
-void launch_lean(const LeanArgs& a, cudaStream_t s, size_t smem) {
-    auto kern = k_spmm_lean<L>;
-    static int occ = -1;
-    static size_t occ_smem = 0;
-    if (occ < 0 || occ_smem != smem) {
-        AGCN_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-        static const int carve = env_int("AGCN_CARVEOUT", -1);
-        if (carve >= 0) AGCN_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, carve));
-        AGCN_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kCtaThreads, smem));
-        if (occ < 1) occ = 1;
-        occ_smem = smem;
-    }
-    const int64_t work = std::max<int64_t>(a.nblocks, (a.n_zero + 31) / 32);
-    const int64_t want = (work + kWarpsPerCta - 1) / kWarpsPerCta;
-    const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)num_sms() * occ));
-    kern<<<(unsigned)grid, kCtaThreads, smem, s>>>(a);
-    post_launch();
-}
-
 template <int L, int T>
 void block_v4(const BlockArgs& a, cudaStream_t s, size_t smem) { launch_block<L, T, true>(a, s, smem); }
 template <int L, int T>
@@ -711,7 +519,7 @@ int num_sms() {
 }
 
 void spmm_launch(agcn_plan_s* p, const float* vals, const float* X, int32_t F, float* Y,
-                 cudaStream_t s) {
+                 cudaStream_t s, const agcn_spmm_opts_t& o) {
     if (p->n == 0) return;
     const bool foreign = s != p->stream;
     if (foreign) {  // plan built on another stream: wait for it; remember this use for destroy
@@ -728,7 +536,7 @@ void spmm_launch(agcn_plan_s* p, const float* vals, const float* X, int32_t F, f
     if (p->partition == AGCN_PARTITION_WARP) {
         AGCN_CUDA(cudaMemsetAsync(Y, 0, sizeof(float) * (size_t)p->n * F, s));
         if (p->ntasks == 0) return;
-        WarpArgs a{p->tasks, p->ntasks, p->rowptr_copy, p->colidx_copy, vals + p->rp_base, X, Y, FV};
+        WarpArgs a{p->tasks, p->ntasks, p->rowptr_copy, p->cols, vals + p->rp_base, X, Y, FV};
         if (v4)
             AGCN_DISPATCH_LT(sh, warp_v4, a, s);
         else
@@ -751,9 +559,7 @@ void spmm_launch(agcn_plan_s* p, const float* vals, const float* X, int32_t F, f
     a.db = p->deg_bound;
     a.stage = ((p->deg_bound + 3) & ~3) + 8;
     a.rso_stage = (p->mbw + 3) & ~3;
-    a.scol = p->sorted_colidx;
-    static const int xmode = env_int("AGCN_XMODE", 0);
-    a.xmode = xmode;
+    a.cols = p->cols;
     a.srp = p->sorted_rowptr;
     a.rso = p->row_src_off;
     a.perm = p->perm;
@@ -765,24 +571,19 @@ void spmm_launch(agcn_plan_s* p, const float* vals, const float* X, int32_t F, f
     a.FV = FV;
     const size_t elt = v4 ? sizeof(float4) : sizeof(float);
     const size_t smem = (size_t)kWarpsPerCta * ((2 * a.stage + a.rso_stage) * 4 + 64 * sh.T * elt);
-    static const int lean_env = env_int("AGCN_LEAN", 1);
-    if (v4 && sh.T == 1 && lean_env) {
-        // rows of heat class >= min_cls are kept in L2: ~100 MB of hot rows (plan.cu kHeatK)
-        static const int heat_env = env_int("AGCN_HEAT", 1);
-        const int min_cls = !p->heat || !heat_env ? 4 : F <= 64 ? 1 : F <= 128 ? 2 : F <= 256 ? 3 : 4;
-        LeanArgs la{a.desc, a.nblocks, a.first_ov, a.n_zero, a.scol, a.srp, a.rso, a.perm, a.vals,
-                    reinterpret_cast<const float4*>(X), reinterpret_cast<float4*>(Y),
-                    reinterpret_cast<float4*>(p->ov_partial), a.db, a.stage, a.rso_stage, FV, min_cls};
-        const size_t lsmem = (size_t)kWarpsPerCta * ((2 * a.stage + 2 * a.rso_stage) * 4 + 64 * 16);
-        switch (sh.L) {
-            case 1: launch_lean<1>(la, s, lsmem); break;
-            case 2: launch_lean<2>(la, s, lsmem); break;
-            case 4: launch_lean<4>(la, s, lsmem); break;
-            case 8: launch_lean<8>(la, s, lsmem); break;
-            case 16: launch_lean<16>(la, s, lsmem); break;
-            default: launch_lean<32>(la, s, lsmem); break;
-        }
-    } else if (v4)
+    // kernel choice (agcn_spmm_opts_t): WIDE when applicable, else GENERAL
+    const bool wide_ok = wide_supported(p, X, Y, F);
+    int kernel = o.kernel;
+    if (kernel == AGCN_KERNEL_AUTO) kernel = wide_ok ? AGCN_KERNEL_WIDE : AGCN_KERNEL_GENERAL;
+    AGCN_CHECK(kernel != AGCN_KERNEL_WIDE || wide_ok, AGCN_ERR_UNSUPPORTED,
+               "WIDE kernel needs F in {8,16,32,64,128,256}, 32-byte aligned X/Y, max_block_warps <= 32");
+    // L2 residency of X: evict_last hints when X fits in L2 (auto), or as requested
+    const double x_bytes = 4.0 * (double)p->x_rows * F;
+    const bool keep = o.l2_hint < 0 ? x_bytes <= kL2KeepBytes : o.l2_hint > 0;
+    a.keep = keep;
+    if (kernel == AGCN_KERNEL_WIDE)
+        launch_wide(p, vals, X, F, Y, keep, s);
+    else if (v4)
         AGCN_DISPATCH_LT(sh, block_v4, a, s, smem);
     else
         AGCN_DISPATCH_LT(sh, block_v1, a, s, smem);

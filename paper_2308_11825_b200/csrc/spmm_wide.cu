@@ -1,0 +1,268 @@
+// spmm_wide.cu -- the occupancy-first SpMM kernel for F in {8, 16, 32, 64, 128, 256}.
+//
+// Same work decomposition and results contract as k_spmm_block (spmm.cu): one 128-bit
+// descriptor {deg, loc, row, info} per warp at a time, a "combined warp"
+// of L = F/8 lanes per X row, G = 32/L of them per warp.  What changes is how the
+// kernel reaches the L2->SM gather roof on B200 (tools/gather_probe.cu: ~18-19 TB/s random
+// row gathers need 64 resident warps per SM, i.e. <= 32 registers and no shared memory):
+//  * every lane moves 32 bytes per X row with one 256-bit load (LDG.E.256), so a warp issues
+//    G rows per load instruction;
+//  * no shared-memory staging: a combined warp loads L (colidx, val) pairs with one
+//    coalesced load per lane and broadcasts them with shuffles;
+//  * rows are whole units of a combined warp: a descriptor's R rows go round-robin to
+//    groups of K combined warps (K = the largest power of two with K*R <= G); the K
+//    members of a group split the row's nonzeros into contiguous parts and add their
+//    partial rows with a fixed xor-shuffle tree.  The paper's level-2 merge
+//    (atomicAdd_block) becomes that deterministic shuffle tree; level 3
+//    (rows with degree > deg_bound) writes per-chunk partial rows summed by k_ov_reduce.
+//  * the row offsets / output rows of the descriptor (<= 32 rows) are fetched once per
+//    descriptor, one per lane, and shuffled to the combined warps.
+//  * colidx / vals are read straight from the caller's CSR through row_src_off (the plan
+//    never copies them), one batch of pairs ahead (prefetch); both are evict-first streams
+//    (ld.global.cs).  When X fits in L2 its rows are loaded with an evict_last hint.
+#include <algorithm>
+#include <cstdlib>
+
+#include "internal.h"
+
+namespace agcn {
+namespace {
+
+constexpr int kWarps = 8;
+constexpr int kThreads = kWarps * 32;
+
+struct f8 {
+    float4 a, b;
+};
+
+__device__ __forceinline__ void ld8(f8& r, const float* p, int hint) {
+    // hint: 0 plain, 1 evict_last (hot), 2 evict_first (cold)
+    if (hint == 1)
+        asm("ld.global.nc.L2::evict_last.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                     : "=f"(r.a.x), "=f"(r.a.y), "=f"(r.a.z), "=f"(r.a.w), "=f"(r.b.x), "=f"(r.b.y),
+                       "=f"(r.b.z), "=f"(r.b.w)
+                     : "l"(p));
+    else if (hint == 2)
+        asm("ld.global.nc.L2::evict_first.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                     : "=f"(r.a.x), "=f"(r.a.y), "=f"(r.a.z), "=f"(r.a.w), "=f"(r.b.x), "=f"(r.b.y),
+                       "=f"(r.b.z), "=f"(r.b.w)
+                     : "l"(p));
+    else
+        asm("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                     : "=f"(r.a.x), "=f"(r.a.y), "=f"(r.a.z), "=f"(r.a.w), "=f"(r.b.x), "=f"(r.b.y),
+                       "=f"(r.b.z), "=f"(r.b.w)
+                     : "l"(p));
+}
+
+__device__ __forceinline__ void fma8(f8& acc, float v, const f8& x) {
+    acc.a.x = fmaf(v, x.a.x, acc.a.x);
+    acc.a.y = fmaf(v, x.a.y, acc.a.y);
+    acc.a.z = fmaf(v, x.a.z, acc.a.z);
+    acc.a.w = fmaf(v, x.a.w, acc.a.w);
+    acc.b.x = fmaf(v, x.b.x, acc.b.x);
+    acc.b.y = fmaf(v, x.b.y, acc.b.y);
+    acc.b.z = fmaf(v, x.b.z, acc.b.z);
+    acc.b.w = fmaf(v, x.b.w, acc.b.w);
+}
+
+__device__ __forceinline__ void st8(float* p, const f8& v) {
+    __stcs(reinterpret_cast<float4*>(p), v.a);
+    __stcs(reinterpret_cast<float4*>(p) + 1, v.b);
+}
+
+__device__ __forceinline__ float shfl_xor_add(float v, int o) {
+    return v + __shfl_xor_sync(0xffffffffu, v, o);
+}
+
+struct WideArgs {
+    const int4* desc;
+    int64_t nblocks;
+    int64_t first_ov;     // descriptor index of the first oversized chunk
+    int64_t n_zero;       // sorted rows [0, n_zero) have degree 0
+    const int32_t* cols;  // column indices, indexed like vals (rowptr-relative)
+    const int32_t* srp;   // sorted rowptr
+    const int32_t* rso;   // row_src_off
+    const int32_t* perm;  // sorted -> original row
+    const float* vals;    // caller vals, offset by rowptr[0]
+    const float* X;
+    float* Y;
+    float* ovp;           // oversized partial rows [ov_chunks][F]
+    int32_t db;           // deg_bound
+};
+
+// L lanes per X row (F = 8 L), U X rows in flight per lane, MINB resident CTAs per SM
+// (register budget), KEEP: X-row loads carry an L2 evict_last hint.
+template <int L, int U, int MINB, bool KEEP>
+__global__ void __launch_bounds__(kThreads, MINB) k_spmm_wide(const __grid_constant__ WideArgs a) {
+    constexpr int G = 32 / L;
+    constexpr int F = 8 * L;
+    static_assert(L % U == 0, "U must divide L");
+    const int lane = threadIdx.x & 31;
+    const int s = lane / L, li = lane % L;
+    const int32_t gw = blockIdx.x * kWarps + (threadIdx.x >> 5);
+    const int32_t W = gridDim.x * kWarps;
+    const float* __restrict__ Xl = a.X + li * 8;
+
+    // degree-0 rows: Y row = 0 (reading Q16)
+    {
+        f8 z;
+        z.a = z.b = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int64_t r = (int64_t)gw * G + s; r < a.n_zero; r += (int64_t)W * G)
+            st8(a.Y + (int64_t)__ldg(a.perm + r) * F + li * 8, z);
+    }
+
+    const int32_t nblocks = (int32_t)a.nblocks;
+    for (int32_t b = gw; b < nblocks; b += W) {
+        const int4 m = __ldg(a.desc + b);
+        const bool ov = m.x > a.db;
+        const int32_t R = ov ? 1 : (m.w & 0xffff);      // rows of the descriptor (<= 32)
+        const int32_t d = ov ? m.w : m.x;               // nonzeros per row (chunk size if ov)
+        // per-row data, one row per lane: where the row's entries start in the caller's
+        // colidx / vals (P:295 step (3) row-pointer update), and its output row
+        int32_t rso_l = 0, dst_l = 0;
+        if (lane < R) {
+            rso_l = __ldg(a.rso + m.z + lane);
+            if (ov)
+                rso_l += m.y - __ldg(a.srp + m.z);      // chunk offset inside the row
+            else
+                dst_l = __ldg(a.perm + m.z + lane);
+        }
+        int K = 1;                                       // combined warps per row
+        while (2 * K * R <= G) K *= 2;
+        const int NG = G / K;                            // row groups per warp
+        const int g = s / K, k = s - g * K;
+        const int32_t part = (d + K - 1) / K;            // nonzeros per group member
+        const int32_t p0 = k * part;
+        const int32_t len_k = max(0, min(d, p0 + part) - p0);
+        for (int32_t r0 = 0; r0 < R; r0 += NG) {
+            const int32_t r = r0 + g;
+            const int32_t mylen = r < R ? len_k : 0;
+            const int32_t e0 = __shfl_sync(0xffffffffu, rso_l, r & 31) + p0;  // first entry
+            f8 acc;
+            acc.a = acc.b = make_float4(0.f, 0.f, 0.f, 0.f);
+            // (colidx, val) pairs, L per batch, one per lane; the next batch is prefetched
+            int32_t c = 0;
+            float v = 0.f;
+            if (li < mylen) {
+                c = __ldcs(a.cols + e0 + li);
+                v = __ldcs(a.vals + e0 + li);
+            }
+            for (int32_t base = 0; base < part; base += L) {     // warp-uniform trip count
+                const int32_t jn = base + L + li;
+                int32_t cn = 0;
+                float vn = 0.f;
+                if (jn < mylen) {
+                    cn = __ldcs(a.cols + e0 + jn);
+                    vn = __ldcs(a.vals + e0 + jn);
+                }
+                const int32_t nb = mylen - base;                 // valid pairs in this batch (may be <= 0)
+                const int32_t nbu = min(L, part - base);         // warp-uniform bound
+#pragma unroll
+                for (int q = 0; q < L; q += U) {
+                    if (q >= nbu) break;
+                    f8 x[U];
+                    float vv[U];
+#pragma unroll
+                    for (int u = 0; u < U; ++u) {
+                        const int32_t cu = __shfl_sync(0xffffffffu, c, s * L + q + u);
+                        vv[u] = __shfl_sync(0xffffffffu, v, s * L + q + u);
+                        if (q + u < nb)
+                            ld8(x[u], Xl + (int64_t)cu * F, KEEP ? 1 : 0);
+                        else
+                            x[u].a = x[u].b = make_float4(0.f, 0.f, 0.f, 0.f);
+                    }
+#pragma unroll
+                    for (int u = 0; u < U; ++u) fma8(acc, vv[u], x[u]);
+                }
+                c = cn;
+                v = vn;
+            }
+            // combine the K partial rows of a group (fixed xor tree: deterministic)
+            for (int o = L; o < K * L; o <<= 1) {
+                acc.a.x = shfl_xor_add(acc.a.x, o);
+                acc.a.y = shfl_xor_add(acc.a.y, o);
+                acc.a.z = shfl_xor_add(acc.a.z, o);
+                acc.a.w = shfl_xor_add(acc.a.w, o);
+                acc.b.x = shfl_xor_add(acc.b.x, o);
+                acc.b.y = shfl_xor_add(acc.b.y, o);
+                acc.b.z = shfl_xor_add(acc.b.z, o);
+                acc.b.w = shfl_xor_add(acc.b.w, o);
+            }
+            const int32_t rd = __shfl_sync(0xffffffffu, dst_l, r & 31);
+            if (k == 0 && r < R) {
+                float* dst = ov ? a.ovp + (int64_t)(b - a.first_ov) * F : a.Y + (int64_t)rd * F;
+                st8(dst + li * 8, acc);
+            }
+        }
+    }
+}
+
+template <int L, int U, int MINB, bool KEEP>
+void launch_t(const WideArgs& a, cudaStream_t s) {
+    auto kern = k_spmm_wide<L, U, MINB, KEEP>;
+    static int occ = -1;
+    if (occ < 0) {
+        AGCN_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kThreads, 0));
+        if (occ < 1) occ = 1;
+    }
+    constexpr int G = 32 / L;
+    const int64_t work = std::max<int64_t>(a.nblocks, (a.n_zero + G - 1) / G);
+    const int64_t want = (work + kWarps - 1) / kWarps;
+    const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)num_sms() * occ));
+    kern<<<(unsigned)grid, kThreads, 0, s>>>(a);
+    post_launch();
+}
+
+int env_int(const char* name, int dflt) {  // experiment switch
+    const char* v = getenv(name);
+    return v ? atoi(v) : dflt;
+}
+
+template <int L, int U, int MINB>
+void launch_k(const WideArgs& a, bool keep, cudaStream_t s) {
+    if (keep)
+        launch_t<L, U, MINB, true>(a, s);
+    else
+        launch_t<L, U, MINB, false>(a, s);
+}
+
+template <int L>
+void launch(const WideArgs& a, bool keep, cudaStream_t s) {
+    // register budget vs rows in flight (AGCN_WIDE_VARIANT, A/B only):
+    //   0: U 4 at 4 CTAs/SM (64 regs)   1: U 8 at 2 CTAs/SM   2: U 8 at 3 CTAs/SM
+    //   3: U 2 at 6 CTAs/SM (40 regs)   4: U 4 at 3 CTAs/SM
+    static const int variant = env_int("AGCN_WIDE_VARIANT", 0);
+    constexpr int U2 = L >= 2 ? 2 : 1, U4 = L >= 4 ? 4 : U2, U8 = L >= 8 ? 8 : U4;
+    switch (variant) {
+        case 1: launch_k<L, U8, 2>(a, keep, s); break;
+        case 2: launch_k<L, U8, 3>(a, keep, s); break;
+        case 3: launch_k<L, U2, 6>(a, keep, s); break;
+        case 4: launch_k<L, U4, 3>(a, keep, s); break;
+        default: launch_k<L, U4, 4>(a, keep, s); break;
+    }
+}
+
+}  // namespace
+
+bool wide_supported(const agcn_plan_s* p, const float* X, const float* Y, int32_t F) {
+    const bool shape = F == 8 || F == 16 || F == 32 || F == 64 || F == 128 || F == 256;
+    const bool al = ((reinterpret_cast<uintptr_t>(X) | reinterpret_cast<uintptr_t>(Y)) & 31u) == 0;
+    return shape && al && p->mbw <= 32;
+}
+
+void launch_wide(agcn_plan_s* p, const float* vals, const float* X, int32_t F, float* Y,
+                 bool l2_keep, cudaStream_t s) {
+    WideArgs a{p->desc, p->nblocks, p->nb_small, p->n_zero, p->cols, p->sorted_rowptr,
+               p->row_src_off, p->perm, vals + p->rp_base, X, Y, p->ov_partial, p->deg_bound};
+    AGCN_CHECK(p->nblocks < (1ll << 31), AGCN_ERR_OVERFLOW, "too many descriptors");
+    switch (F) {
+        case 8: launch<1>(a, l2_keep, s); break;
+        case 16: launch<2>(a, l2_keep, s); break;
+        case 32: launch<4>(a, l2_keep, s); break;
+        case 64: launch<8>(a, l2_keep, s); break;
+        case 128: launch<16>(a, l2_keep, s); break;
+        default: launch<32>(a, l2_keep, s); break;
+    }
+}
+
+}  // namespace agcn

@@ -48,9 +48,9 @@ def check_plan_vs_oracle(rowptr, colidx, mbw=12, mwn=32, n_cols=None):
     return p
 
 
-def check_spmm(p, rowptr, colidx, vals, X, Y=None):
+def check_spmm(p, rowptr, colidx, vals, X, Y=None, kernel="auto"):
     if Y is None:
-        Y = p.spmm(cu(vals), cu(X)).cpu().numpy()
+        Y = p.spmm(cu(vals), cu(X), kernel=kernel).cpu().numpy()
     r = oracle.spmm_check(rowptr, colidx, vals, X, Y)
     assert r["nfail"] == 0, r
     return Y
@@ -135,6 +135,51 @@ def test_spmm_c2_F(F):
     w = gen.make_config("c2", vals_kind="uniform")
     p = make_plan(w.rowptr, w.colidx)
     check_spmm(p, w.rowptr, w.colidx, w.vals, w.X(F))
+
+
+KERNEL_F = [("general", F) for F in (3, 4, 16, 64, 128, 100)] + \
+    [("wide", F) for F in (8, 16, 32, 64, 128, 256)]
+
+
+@pytest.mark.parametrize("kernel,F", KERNEL_F)
+def test_spmm_every_kernel(kernel, F):
+    """Every SpMM kernel variant (agcn_spmm_opts_t.kernel) against the oracle."""
+    w = gen.make_config("c2", vals_kind="uniform")
+    p = make_plan(w.rowptr, w.colidx)
+    check_spmm(p, w.rowptr, w.colidx, w.vals, w.X(F), kernel=kernel)
+    rowptr, colidx = _rows_csr(np.array([0, 1, 2, 3, 5, 31, 33, 64, 97, 130, 200, 383, 384, 385, 768,
+                                         769, 2000, 0, 7]), 500, 11)
+    rng = np.random.default_rng(F)
+    vals = rng.uniform(-1, 1, colidx.size).astype(np.float32)
+    X = rng.uniform(-1, 1, (500, F)).astype(np.float32)
+    for mbw, mwn in [(12, 32), (2, 2), (1, 1), (32, 8), (5, 7)]:
+        p = make_plan(rowptr, colidx, max_block_warps=mbw, max_warp_nzs=mwn, n_cols=500)
+        check_spmm(p, rowptr, colidx, vals, X, kernel=kernel)
+
+
+def test_spmm_kernel_unsupported_is_reported():
+    w = gen.make_config("c1")
+    p = make_plan(w.rowptr, w.colidx)
+    with pytest.raises(A.AgcnError) as e:
+        p.spmm(cu(w.vals), cu(w.X(100)), kernel="wide")
+    assert e.value.status == "AGCN_ERR_UNSUPPORTED"
+    with pytest.raises(A.AgcnError):
+        p.spmm(cu(w.vals), cu(w.X(64)), kernel="wide", l2_hint=2)
+
+
+def test_wide_kernel_nonfinite_x_rows_not_referenced():
+    """Rows of X that A never references may hold inf/nan: they must not leak into Y."""
+    rowptr = np.array([0, 3, 3, 8], dtype=np.int32)
+    colidx = np.array([1, 2, 3, 1, 2, 3, 4, 5], dtype=np.int32)
+    vals = np.ones(8, dtype=np.float32)
+    X = np.ones((7, 64), dtype=np.float32)
+    X[0] = np.inf
+    X[6] = np.nan
+    for kernel in ("auto", "general", "wide"):
+        p = make_plan(rowptr, colidx, n_cols=7)
+        Y = p.spmm(cu(vals), cu(X), kernel=kernel).cpu().numpy()
+        assert np.isfinite(Y).all(), kernel
+        check_spmm(p, rowptr, colidx, vals, X, Y)
 
 
 def test_spmm_c3_both_partitions():

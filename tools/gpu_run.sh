@@ -23,6 +23,10 @@ for st in $STAGES; do
         env ${AB_VAR}=$v timeout 600 python bench.py --config $c --steps 10 --warmup 3 --no-cpu-baseline --no-e2e --no-cusparse > "$OUT/ab_${c}_${AB_VAR}_$v.log" 2>&1
         echo "ab $c $AB_VAR=$v: $(python -c "import json,sys; d=json.loads(open(sys.argv[1]).read().strip().splitlines()[-1]); print(round(d['ms_per_step'],3), 'spmm', round(d['spmm_only']['ms_per_layer'],3), 'plan', round(d['plan_ms'],3))" "$OUT/ab_${c}_${AB_VAR}_$v.log" 2>&1 | tail -1)"
       done; done;;
+    probe)
+      nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 tools/gather_probe.cu -o /tmp/gather_probe -lcuda > "$OUT/probe_build.log" 2>&1
+      for a in "262144 67108864 0" "262144 67108864 1" "466000 67108864 1" "8388608 67108864 1" "8388608 67108864 0"; do
+        timeout 300 /tmp/gather_probe $a >> "$OUT/probe.log" 2>&1; done; tail -60 "$OUT/probe.log";;
     ncu_list)
       timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv \
         --log-file "$OUT/launches_c5.csv" python bench.py --profile --steps 2 --warmup 1 > "$OUT/ncu_list.log" 2>&1; echo "ncu_list rc=$?";;
