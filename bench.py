@@ -321,7 +321,9 @@ def main():
                                                    "n_oversized_blocks", "max_deg")},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                          "frac": achieved / peaks["hbm_gbs"], "traffic": traffic,
-                         "kernel": "agcn_spmm (k_spmm_block + k_ov_reduce)",
+                         "kernel": "agcn_spmm (%s + k_ov_reduce)" % (
+                             "k_spmm_wide" if args.kernel != "general" and F in (8, 16, 32, 64, 128, 256)
+                             else "k_spmm_block"),
                          "bytes_per_launch": b_comp, "peak_source": peaks["source"],
                          "traffic_source": traffic_src},
             "gpu_launches": int(launches),

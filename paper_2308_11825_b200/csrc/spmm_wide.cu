@@ -22,6 +22,7 @@
 //    (ld.global.cs).  When X fits in L2 its rows are loaded with an evict_last hint.
 #include <algorithm>
 #include <cstdlib>
+#include <cstring>
 
 #include "internal.h"
 
@@ -92,7 +93,7 @@ struct WideArgs {
 
 // L lanes per X row (F = 8 L), U X rows in flight per lane, MINB resident CTAs per SM
 // (register budget), KEEP: X-row loads carry an L2 evict_last hint.
-template <int L, int U, int MINB, bool KEEP>
+template <int L, int U, int MINB, bool KEEP, bool PREF>
 __global__ void __launch_bounds__(kThreads, MINB) k_spmm_wide(const __grid_constant__ WideArgs a) {
     constexpr int G = 32 / L;
     constexpr int F = 8 * L;
@@ -101,19 +102,31 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_wide(const __grid_const
     const int s = lane / L, li = lane % L;
     const int32_t gw = blockIdx.x * kWarps + (threadIdx.x >> 5);
     const int32_t W = gridDim.x * kWarps;
-    const float* __restrict__ Xl = a.X + li * 8;
 
-    // degree-0 rows: Y row = 0 (reading Q16)
+    // degree-0 rows: Y row = 0 (reading Q16); 32 rows per warp step, one perm load per lane
     {
         f8 z;
         z.a = z.b = make_float4(0.f, 0.f, 0.f, 0.f);
-        for (int64_t r = (int64_t)gw * G + s; r < a.n_zero; r += (int64_t)W * G)
-            st8(a.Y + (int64_t)__ldg(a.perm + r) * F + li * 8, z);
+        for (int64_t r0 = (int64_t)gw * 32; r0 < a.n_zero; r0 += (int64_t)W * 32) {
+            const int32_t pr = r0 + lane < a.n_zero ? __ldg(a.perm + r0 + lane) : -1;
+#pragma unroll 4
+            for (int i = 0; i < 32; i += G) {
+                const int32_t o = __shfl_sync(0xffffffffu, pr, i + s);
+                if (o >= 0) st8(a.Y + (int64_t)o * F + li * 8, z);
+            }
+        }
     }
 
     const int32_t nblocks = (int32_t)a.nblocks;
+    int4 m_next = PREF && gw < nblocks ? __ldg(a.desc + gw) : make_int4(0, 0, 0, 0);
     for (int32_t b = gw; b < nblocks; b += W) {
-        const int4 m = __ldg(a.desc + b);
+        int4 m;
+        if (PREF) {                                      // descriptor prefetched one step ahead
+            m = m_next;
+            if (b + W < nblocks) m_next = __ldg(a.desc + b + W);
+        } else {
+            m = __ldg(a.desc + b);
+        }
         const bool ov = m.x > a.db;
         const int32_t R = ov ? 1 : (m.w & 0xffff);      // rows of the descriptor (<= 32)
         const int32_t d = ov ? m.w : m.x;               // nonzeros per row (chunk size if ov)
@@ -129,6 +142,67 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_wide(const __grid_const
         }
         int K = 1;                                       // combined warps per row
         while (2 * K * R <= G) K *= 2;
+        f8 acc;
+        acc.a = acc.b = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (K == 1) {
+            // ---- whole rows per combined warp: sub-warp s owns rows s, s+G, s+2G, ... and
+            // streams their entries back to back (so short rows keep U gathers in flight),
+            // flushing the accumulator at every row boundary (all rows have d entries, so the
+            // boundaries are warp-uniform).
+            const int32_t T = ((R + G - 1) / G) * d;              // sub-warp 0's entries (bound)
+            const int32_t Ts = s < R ? ((R - s + G - 1) / G) * d : 0;
+            int32_t c, cn;
+            float v, vn;
+            auto pair = [&](int32_t t, int32_t& cc, float& vv) {  // entry t of this sub-warp
+                const int32_t ri = t / d;
+                const int32_t e = __shfl_sync(0xffffffffu, rso_l, min(s + ri * G, 31)) + (t - ri * d);
+                cc = 0;
+                vv = 0.f;
+                if (t < Ts) {
+                    cc = __ldg(a.cols + e);
+                    vv = __ldg(a.vals + e);
+                }
+            };
+            pair(li, c, v);
+            int32_t left = d, rowi = 0;
+            for (int32_t base = 0; base < T; base += L) {        // warp-uniform trip count
+                pair(base + L + li, cn, vn);                      // next batch (prefetch)
+                const int32_t nb = Ts - base;                     // valid entries in this batch
+                const int32_t nbu = min(L, T - base);             // warp-uniform bound
+#pragma unroll 1
+                for (int q = 0; q < L; q += U) {
+                    if (q >= nbu) break;
+                    f8 x[U];
+#pragma unroll
+                    for (int u = 0; u < U; ++u) {
+                        const int32_t cu = __shfl_sync(0xffffffffu, c, s * L + q + u);
+                        if (q + u < nb)
+                            ld8(x[u], a.X + ((int64_t)cu * F + li * 8), KEEP ? 1 : 0);
+                        else
+                            x[u].a = x[u].b = make_float4(0.f, 0.f, 0.f, 0.f);
+                    }
+#pragma unroll
+                    for (int u = 0; u < U; ++u) {
+                        fma8(acc, __shfl_sync(0xffffffffu, v, s * L + q + u), x[u]);
+                        if (q + u < nbu && --left == 0) {         // row boundary: store, restart
+                            const int32_t r = s + rowi * G;
+                            const int32_t o = __shfl_sync(0xffffffffu, dst_l, min(r, 31));
+                            if (r < R) {
+                                float* dst = ov ? a.ovp + (int64_t)(b - a.first_ov) * F : a.Y + (int64_t)o * F;
+                                st8(dst + li * 8, acc);
+                            }
+                            acc.a = acc.b = make_float4(0.f, 0.f, 0.f, 0.f);
+                            left = d;
+                            ++rowi;
+                        }
+                    }
+                }
+                c = cn;
+                v = vn;
+            }
+            continue;
+        }
+        // ---- rows split over K combined warps (R <= G/2): contiguous parts, xor-tree merge
         const int NG = G / K;                            // row groups per warp
         const int g = s / K, k = s - g * K;
         const int32_t part = (d + K - 1) / K;            // nonzeros per group member
@@ -138,41 +212,38 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_wide(const __grid_const
             const int32_t r = r0 + g;
             const int32_t mylen = r < R ? len_k : 0;
             const int32_t e0 = __shfl_sync(0xffffffffu, rso_l, r & 31) + p0;  // first entry
-            f8 acc;
             acc.a = acc.b = make_float4(0.f, 0.f, 0.f, 0.f);
             // (colidx, val) pairs, L per batch, one per lane; the next batch is prefetched
             int32_t c = 0;
             float v = 0.f;
             if (li < mylen) {
-                c = __ldcs(a.cols + e0 + li);
-                v = __ldcs(a.vals + e0 + li);
+                c = __ldg(a.cols + e0 + li);
+                v = __ldg(a.vals + e0 + li);
             }
             for (int32_t base = 0; base < part; base += L) {     // warp-uniform trip count
                 const int32_t jn = base + L + li;
                 int32_t cn = 0;
                 float vn = 0.f;
                 if (jn < mylen) {
-                    cn = __ldcs(a.cols + e0 + jn);
-                    vn = __ldcs(a.vals + e0 + jn);
+                    cn = __ldg(a.cols + e0 + jn);
+                    vn = __ldg(a.vals + e0 + jn);
                 }
                 const int32_t nb = mylen - base;                 // valid pairs in this batch (may be <= 0)
                 const int32_t nbu = min(L, part - base);         // warp-uniform bound
-#pragma unroll
+#pragma unroll 1
                 for (int q = 0; q < L; q += U) {
                     if (q >= nbu) break;
                     f8 x[U];
-                    float vv[U];
 #pragma unroll
                     for (int u = 0; u < U; ++u) {
                         const int32_t cu = __shfl_sync(0xffffffffu, c, s * L + q + u);
-                        vv[u] = __shfl_sync(0xffffffffu, v, s * L + q + u);
                         if (q + u < nb)
-                            ld8(x[u], Xl + (int64_t)cu * F, KEEP ? 1 : 0);
+                            ld8(x[u], a.X + ((int64_t)cu * F + li * 8), KEEP ? 1 : 0);
                         else
                             x[u].a = x[u].b = make_float4(0.f, 0.f, 0.f, 0.f);
                     }
 #pragma unroll
-                    for (int u = 0; u < U; ++u) fma8(acc, vv[u], x[u]);
+                    for (int u = 0; u < U; ++u) fma8(acc, __shfl_sync(0xffffffffu, v, s * L + q + u), x[u]);
                 }
                 c = cn;
                 v = vn;
@@ -197,9 +268,9 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_wide(const __grid_const
     }
 }
 
-template <int L, int U, int MINB, bool KEEP>
+template <int L, int U, int MINB, bool KEEP, bool PREF>
 void launch_t(const WideArgs& a, cudaStream_t s) {
-    auto kern = k_spmm_wide<L, U, MINB, KEEP>;
+    auto kern = k_spmm_wide<L, U, MINB, KEEP, PREF>;
     static int occ = -1;
     if (occ < 0) {
         AGCN_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kThreads, 0));
@@ -218,27 +289,26 @@ int env_int(const char* name, int dflt) {  // experiment switch
     return v ? atoi(v) : dflt;
 }
 
-template <int L, int U, int MINB>
+template <int L, int U, int MINB, bool PREF>
 void launch_k(const WideArgs& a, bool keep, cudaStream_t s) {
     if (keep)
-        launch_t<L, U, MINB, true>(a, s);
+        launch_t<L, U, MINB, true, PREF>(a, s);
     else
-        launch_t<L, U, MINB, false>(a, s);
+        launch_t<L, U, MINB, false, PREF>(a, s);
 }
 
 template <int L>
 void launch(const WideArgs& a, bool keep, cudaStream_t s) {
-    // register budget vs rows in flight (AGCN_WIDE_VARIANT, A/B only):
-    //   0: U 4 at 4 CTAs/SM (64 regs)   1: U 8 at 2 CTAs/SM   2: U 8 at 3 CTAs/SM
-    //   3: U 2 at 6 CTAs/SM (40 regs)   4: U 4 at 3 CTAs/SM
+    // register budget vs rows in flight (AGCN_WIDE_VARIANT, A/B only; profiles/r01*_wide*):
+    //   0: U 4 at 3 CTAs/SM (80 regs, no spills; the default)   1: same + descriptor prefetch
+    //   2: U 8 at 2 CTAs/SM + descriptor prefetch               3: U 4 at 4 CTAs/SM (64 regs)
     static const int variant = env_int("AGCN_WIDE_VARIANT", 0);
-    constexpr int U2 = L >= 2 ? 2 : 1, U4 = L >= 4 ? 4 : U2, U8 = L >= 8 ? 8 : U4;
+    constexpr int U4 = L >= 4 ? 4 : L, U8 = L >= 8 ? 8 : U4;
     switch (variant) {
-        case 1: launch_k<L, U8, 2>(a, keep, s); break;
-        case 2: launch_k<L, U8, 3>(a, keep, s); break;
-        case 3: launch_k<L, U2, 6>(a, keep, s); break;
-        case 4: launch_k<L, U4, 3>(a, keep, s); break;
-        default: launch_k<L, U4, 4>(a, keep, s); break;
+        case 1: launch_k<L, U4, 3, true>(a, keep, s); break;
+        case 2: launch_k<L, U8, 2, true>(a, keep, s); break;
+        case 3: launch_k<L, U4, 4, false>(a, keep, s); break;
+        default: launch_k<L, U4, 3, false>(a, keep, s); break;
     }
 }
 

@@ -27,6 +27,10 @@ for st in $STAGES; do
       nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 tools/gather_probe.cu -o /tmp/gather_probe -lcuda > "$OUT/probe_build.log" 2>&1
       for a in "262144 67108864 0" "262144 67108864 1" "466000 67108864 1" "8388608 67108864 1" "8388608 67108864 0"; do
         timeout 300 /tmp/gather_probe $a >> "$OUT/probe.log" 2>&1; done; tail -60 "$OUT/probe.log";;
+    l2probe)
+      nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 tools/l2_probe.cu -o /tmp/l2_probe > "$OUT/l2probe_build.log" 2>&1
+      for a in "8388608 67108864 390000 1.0" "8388608 67108864 390000 0.8" "466000 67108864 466000 0.5" "466000 67108864 300000 0.5"; do
+        timeout 300 /tmp/l2_probe $a >> "$OUT/l2probe.log" 2>&1; done; cat "$OUT/l2probe.log";;
     ncu_list)
       timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv \
         --log-file "$OUT/launches_c5.csv" python bench.py --profile --steps 2 --warmup 1 > "$OUT/ncu_list.log" 2>&1; echo "ncu_list rc=$?";;
