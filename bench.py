@@ -42,6 +42,8 @@ def parse():
     ap.add_argument("--partition", choices=["block", "warp"], default="block")
     ap.add_argument("--kernel", choices=["auto", "general", "wide"], default="auto")
     ap.add_argument("--l2-hint", type=int, default=None, help="None: auto; 0: never; 1: always")
+    ap.add_argument("--col-block-mb", type=int, default=None,
+                    help="None: auto; 0: off (paper chunks); MiB of X per column block")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="CPU-oracle sample budget")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -239,7 +241,8 @@ def main():
         def spmm(Xin, out_rows):
             s0, s1 = ev(), ev()
             s0.record(stream)
-            plan.spmm(va_d, Xin, out=out_rows, kernel=args.kernel, l2_hint=args.l2_hint)
+            plan.spmm(va_d, Xin, out=out_rows, kernel=args.kernel, l2_hint=args.l2_hint,
+                      col_block_mb=args.col_block_mb)
             s1.record(stream)
             if record:
                 rec["spmm"].append((s0, s1))

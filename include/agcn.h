@@ -137,10 +137,18 @@ typedef enum {
 } agcn_kernel_t;
 
 typedef struct {
-    int32_t kernel;   /* agcn_kernel_t; default AGCN_KERNEL_AUTO */
-    int32_t l2_hint;  /* X-row L2 residency: -1 (default) evict_last hints when X fits in L2
-                         (<= 128 MiB), 0 never, 1 always */
-    int32_t reserved[6];
+    int32_t kernel;       /* agcn_kernel_t; default AGCN_KERNEL_AUTO */
+    int32_t l2_hint;      /* X-row L2 residency: -1 (default) evict_last hints when X fits in L2
+                             (<= 128 MiB), 0 never, 1 always */
+    int32_t col_block_mb; /* WIDE kernel, rows of degree > deg_bound: execute them as pieces cut
+                             at column blocks of this many MiB of X, block by block, so the X
+                             slice being gathered stays in L2 (results unchanged: fixed-order
+                             partial sums; applies to rows of degree >= 2048 when X is larger
+                             than one block).  -1 (default) and 0: off (the paper's deg_bound
+                             chunks; measured faster on B200); > 0: MiB per block.
+                             Builds a plan-owned schedule on first use per F (stream-ordered,
+                             no host synchronisation). */
+    int32_t reserved[5];
 } agcn_spmm_opts_t;
 
 /* Fill *opts with the defaults above. */

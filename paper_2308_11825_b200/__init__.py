@@ -149,11 +149,14 @@ class Plan:
                                          out.ctypes.data or None, out.nbytes))
         return out
 
-    def spmm(self, vals, X, out=None, stream=None, kernel: str = "auto", l2_hint: int | None = None):
+    def spmm(self, vals, X, out=None, stream=None, kernel: str = "auto", l2_hint: int | None = None,
+             col_block_mb: int | None = None):
         """Y = A.X (asynchronous on `stream`, default the current torch stream).
 
         kernel: "auto" | "general" | "wide" (agcn_kernel_t); l2_hint: None (auto: evict_last
-        hints on X rows when X fits in L2), 0 (never) or 1 (always).
+        hints on X rows when X fits in L2), 0 (never) or 1 (always).  col_block_mb: None (auto),
+        0 (off: the paper's deg_bound chunks for oversized rows) or the X slice per column block
+        in MiB (agcn_spmm_opts_t.col_block_mb).
         """
         torch = _torch()
         F = X.shape[1] if X.dim() == 2 else 1
@@ -167,7 +170,7 @@ class Plan:
         x = _dev_ptr(X, "float32", "X") if X.numel() else 0
         y = _dev_ptr(out, "float32", "out") if out.numel() else 0
         _check(_lib.lib().agcn_spmm_ex(self.handle, v or None, x or None, int(F), y or None,
-                                       _stream_handle(stream), _spmm_opts(kernel, l2_hint)))
+                                       _stream_handle(stream), _spmm_opts(kernel, l2_hint, col_block_mb)))
         return out
 
     def close(self):
@@ -188,11 +191,12 @@ class Plan:
         self.close()
 
 
-def _spmm_opts(kernel: str = "auto", l2_hint: int | None = None):
+def _spmm_opts(kernel: str = "auto", l2_hint: int | None = None, col_block_mb: int | None = None):
     o = _lib.SpmmOpts()
     _lib.lib().agcn_default_spmm_opts(ctypes.byref(o))
     o.kernel = _lib.KERNELS[kernel]
     o.l2_hint = -1 if l2_hint is None else int(l2_hint)
+    o.col_block_mb = -1 if col_block_mb is None else int(col_block_mb)
     return ctypes.byref(o)
 
 
@@ -210,12 +214,12 @@ def agcn_spmm(plan: Plan, vals, X, F: int, Y, stream=None) -> None:
 
 
 def agcn_spmm_ex(plan: Plan, vals, X, F: int, Y, stream=None, kernel: str = "auto",
-                 l2_hint: int | None = None) -> None:
+                 l2_hint: int | None = None, col_block_mb: int | None = None) -> None:
     v = _dev_ptr(vals, "float32", "vals") if vals.numel() else 0
     x = _dev_ptr(X, "float32", "X") if X.numel() else 0
     y = _dev_ptr(Y, "float32", "Y") if Y.numel() else 0
     _check(_lib.lib().agcn_spmm_ex(plan.handle, v or None, x or None, int(F), y or None,
-                                   _stream_handle(stream), _spmm_opts(kernel, l2_hint)))
+                                   _stream_handle(stream), _spmm_opts(kernel, l2_hint, col_block_mb)))
 
 
 def shard_bounds(rowptr, nranks: int, stream=None) -> np.ndarray:

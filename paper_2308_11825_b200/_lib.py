@@ -26,7 +26,8 @@ KERNELS = {"auto": 0, "general": 1, "wide": 3}
 
 
 class SpmmOpts(ctypes.Structure):
-    _fields_ = [("kernel", c_i32), ("l2_hint", c_i32), ("reserved", c_i32 * 6)]
+    _fields_ = [("kernel", c_i32), ("l2_hint", c_i32), ("col_block_mb", c_i32),
+                ("reserved", c_i32 * 5)]
 
 
 class Stats(ctypes.Structure):
@@ -49,7 +50,7 @@ def lib():
     global _lib
     if _lib is not None:
         return _lib
-    path = _build.build()
+    path = os.environ.get("AGCN_LIBRARY") or _build.build()  # AGCN_LIBRARY: A/B of builds
     L = ctypes.CDLL(path, mode=os.RTLD_LOCAL)
     L.agcn_default_opts.argtypes = [ctypes.POINTER(Opts)]
     L.agcn_default_opts.restype = None

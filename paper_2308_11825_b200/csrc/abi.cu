@@ -113,6 +113,7 @@ void agcn_default_spmm_opts(agcn_spmm_opts_t* o) {
     std::memset(o, 0, sizeof(*o));
     o->kernel = AGCN_KERNEL_AUTO;
     o->l2_hint = -1;
+    o->col_block_mb = -1;
 }
 
 agcn_status_t agcn_spmm_ex(agcn_plan_t plan, const float* vals, const float* X, int32_t F, float* Y,
@@ -125,6 +126,7 @@ agcn_status_t agcn_spmm_ex(agcn_plan_t plan, const float* vals, const float* X, 
         AGCN_CHECK(o.kernel == AGCN_KERNEL_AUTO || o.kernel == AGCN_KERNEL_GENERAL ||
                        o.kernel == AGCN_KERNEL_WIDE, AGCN_ERR_INVALID_ARG, "unknown kernel");
         AGCN_CHECK(o.l2_hint >= -1 && o.l2_hint <= 1, AGCN_ERR_INVALID_ARG, "l2_hint must be -1, 0 or 1");
+        AGCN_CHECK(o.col_block_mb >= -1, AGCN_ERR_INVALID_ARG, "col_block_mb must be >= -1");
         if (plan->n == 0) return;
         AGCN_CHECK(Y != nullptr, AGCN_ERR_INVALID_ARG, "Y is NULL");
         AGCN_CHECK(plan->nnz == 0 || (vals != nullptr && X != nullptr), AGCN_ERR_INVALID_ARG,
@@ -175,7 +177,10 @@ agcn_status_t agcn_plan_stats(agcn_plan_t plan, agcn_plan_stats_t* out) {
         out->max_block_warps = plan->mbw;
         out->max_warp_nzs = plan->mwn;
         out->partition = plan->partition;
-        out->device_bytes = plan->device_bytes + plan->ov_partial_floats * sizeof(float);
+        out->device_bytes = plan->device_bytes + plan->ov_partial_floats * sizeof(float) +
+                            plan->sched.partial_floats * sizeof(float) +
+                            (size_t)plan->sched.cap * sizeof(int4) +
+                            (plan->sched.slot_base ? sizeof(int32_t) * (size_t)(plan->n_ov + 1) : 0);
     });
 }
 

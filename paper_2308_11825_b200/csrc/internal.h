@@ -95,6 +95,21 @@ struct PlanFlags {          // device-written, read back once (validation + size
     int32_t rowptr_last;
     int32_t pad[3];
     int64_t ov_chunks;      // sum over oversized rows of ceil(deg / deg_bound)
+    int64_t ov_chunks_heavy;  // the part of ov_chunks from rows of degree >= kColBlockMinDeg
+};
+
+// Column-blocked execution schedule of the oversized rows (sched.cu), per block width.
+constexpr int32_t kColBlockMinDeg = 2048;  // rows of at least this degree are cut at blocks
+constexpr int32_t kMaxPieces = 16;         // pieces per deg_bound chunk at most
+struct ColSched {
+    int shift = -1;              // column block = column >> shift (-1: not built)
+    int32_t nb = 0;              // column blocks
+    int32_t F = 0;               // F the partial buffer is sized for
+    int64_t cap = 0;             // capacity in pieces (upper bound of the piece count)
+    int4* seg = nullptr;         // [cap] pieces {-1 - slot, first entry, 0, length}, block-major
+    int32_t* slot_base = nullptr;  // [n_ov + 1] first slot of oversized row k; [n_ov] = #pieces
+    float* partial = nullptr;    // [cap][F] partial rows
+    size_t partial_floats = 0, partial_need = 0;
 };
 
 }  // namespace agcn
@@ -108,6 +123,7 @@ struct agcn_plan_s {
 
     // AGCN_PARTITION_BLOCK
     int64_t nblocks = 0, nb_small = 0, n_zero = 0, n_ov = 0, ov_start = 0, ov_chunks = 0;
+    int64_t ov_chunks_heavy = 0;       // chunks of rows of degree >= kColBlockMinDeg
     int64_t max_deg = 0;
     int32_t* perm = nullptr;           // [n]   sorted position -> original row
     int32_t* sorted_rowptr = nullptr;  // [n+1] row pointer of the degree-sorted CSR (P:295 (3))
@@ -128,6 +144,7 @@ struct agcn_plan_s {
     // SpMM scratch (oversized-row partial sums, chunk-major [ov_chunks][F])
     float* ov_partial = nullptr;
     size_t ov_partial_floats = 0;
+    agcn::ColSched sched;              // column-blocked schedule of the oversized rows (WIDE)
 
     size_t device_bytes = 0;
     cudaStream_t stream = nullptr;  // stream the plan was built on
@@ -141,6 +158,10 @@ void spmm_launch(agcn_plan_s* p, const float* vals, const float* X, int32_t F, f
 // spmm_wide.cu: 256-bit-per-lane kernel for F in {8,...,256}
 bool wide_supported(const agcn_plan_s* p, const float* X, const float* Y, int32_t F);
 void launch_wide(agcn_plan_s* p, const float* vals, const float* X, int32_t F, float* Y,
-                 bool l2_keep, cudaStream_t s);
+                 bool l2_keep, bool blocked, cudaStream_t s);
+// sched.cu
+int col_sched_shift(const agcn_plan_s* p, int32_t F, double target_bytes);
+void build_col_sched(agcn_plan_s* p, int shift, int32_t F, cudaStream_t s);
+void free_col_sched(ColSched& cs, cudaStream_t s);
 int num_sms();
 }  // namespace agcn

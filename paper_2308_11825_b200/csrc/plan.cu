@@ -43,7 +43,7 @@ __global__ void __launch_bounds__(kThreads) k_deg_hist(const int32_t* __restrict
     __syncthreads();
     const int64_t lo = (int64_t)blockIdx.x * kTile, hi = min(n, lo + kTile);
     int32_t maxd = 0, bad = 0;
-    long long ovc = 0;
+    long long ovc = 0, ovh = 0;
     for (int64_t i = lo + threadIdx.x; i < hi; i += kThreads) {
         int32_t d = rowptr[i + 1] - rowptr[i];
         if (d < 0) bad = 1;
@@ -51,17 +51,20 @@ __global__ void __launch_bounds__(kThreads) k_deg_hist(const int32_t* __restrict
         atomicAdd(&hist[key], 1);
         maxd = max(maxd, d);
         if (d > db) ovc += (d + db - 1) / db;
+        if (d > db && d >= kColBlockMinDeg) ovh += (d + db - 1) / db;
     }
 #pragma unroll
     for (int o = 16; o; o >>= 1) {
         maxd = max(maxd, __shfl_xor_sync(0xffffffffu, maxd, o));
         bad |= __shfl_xor_sync(0xffffffffu, bad, o);
         ovc += __shfl_xor_sync(0xffffffffu, ovc, o);
+        ovh += __shfl_xor_sync(0xffffffffu, ovh, o);
     }
     if ((threadIdx.x & 31) == 0) {
         if (maxd) atomicMax(&flags->max_deg, maxd);
         if (bad) flags->bad_rowptr = 1;
         if (ovc) atomicAdd((unsigned long long*)&flags->ov_chunks, (unsigned long long)ovc);
+        if (ovh) atomicAdd((unsigned long long*)&flags->ov_chunks_heavy, (unsigned long long)ovh);
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         flags->rowptr_first = rowptr[0];
@@ -442,6 +445,7 @@ void build_block_plan(agcn_plan_s* p, const int32_t* rowptr, const int32_t* coli
     p->n_ov = h_cnt[db + 1];
     p->ov_start = n - p->n_ov;
     p->ov_chunks = hf.ov_chunks;
+    p->ov_chunks_heavy = hf.ov_chunks_heavy;
     p->max_deg = hf.max_deg;
     p->nb_small = blk;
     p->nblocks = blk + hf.ov_chunks;
@@ -573,6 +577,7 @@ void free_plan_arrays(agcn_plan_s* p) {
     if (p->last_use) cudaStreamWaitEvent(p->stream, p->last_use, 0);
     for (void* q : ptrs)
         if (q) cudaFreeAsync(q, p->stream);
+    free_col_sched(p->sched, p->stream);
     if (p->ready) cudaEventDestroy(p->ready);
     if (p->last_use) cudaEventDestroy(p->last_use);
 }

@@ -543,8 +543,24 @@ void spmm_launch(agcn_plan_s* p, const float* vals, const float* X, int32_t F, f
             AGCN_DISPATCH_LT(sh, warp_v1, a, s);
         return;
     }
-    // oversized-row partial buffer (grows, stream-ordered)
-    const size_t need = (size_t)p->ov_chunks * (size_t)F;
+    // kernel choice (agcn_spmm_opts_t): WIDE when applicable, else GENERAL
+    const bool wide_ok = wide_supported(p, X, Y, F);
+    int kernel = o.kernel;
+    if (kernel == AGCN_KERNEL_AUTO) kernel = wide_ok ? AGCN_KERNEL_WIDE : AGCN_KERNEL_GENERAL;
+    AGCN_CHECK(kernel != AGCN_KERNEL_WIDE || wide_ok, AGCN_ERR_UNSUPPORTED,
+               "WIDE kernel needs F in {8,16,32,64,128,256}, 32-byte aligned X/Y, max_block_warps <= 32");
+    // column-blocked oversized rows (WIDE kernel, sched.cu): X slice per block ~ col_block_mb
+    bool blocked = false;
+    if (kernel == AGCN_KERNEL_WIDE && o.col_block_mb > 0) {
+        const double target = o.col_block_mb * 1048576.0;
+        const int shift = col_sched_shift(p, F, target);
+        if (shift >= 0) {
+            if (p->sched.shift != shift || p->sched.F < F || !p->sched.seg) build_col_sched(p, shift, F, s);
+            blocked = true;
+        }
+    }
+    // oversized-row partial buffer of the paper's chunks (grows, stream-ordered)
+    const size_t need = blocked ? 0 : (size_t)p->ov_chunks * (size_t)F;
     if (need > p->ov_partial_floats) {
         if (p->ov_partial) AGCN_CUDA(cudaFreeAsync(p->ov_partial, s));
         p->ov_partial = nullptr;
@@ -571,30 +587,24 @@ void spmm_launch(agcn_plan_s* p, const float* vals, const float* X, int32_t F, f
     a.FV = FV;
     const size_t elt = v4 ? sizeof(float4) : sizeof(float);
     const size_t smem = (size_t)kWarpsPerCta * ((2 * a.stage + a.rso_stage) * 4 + 64 * sh.T * elt);
-    // kernel choice (agcn_spmm_opts_t): WIDE when applicable, else GENERAL
-    const bool wide_ok = wide_supported(p, X, Y, F);
-    int kernel = o.kernel;
-    if (kernel == AGCN_KERNEL_AUTO) kernel = wide_ok ? AGCN_KERNEL_WIDE : AGCN_KERNEL_GENERAL;
-    AGCN_CHECK(kernel != AGCN_KERNEL_WIDE || wide_ok, AGCN_ERR_UNSUPPORTED,
-               "WIDE kernel needs F in {8,16,32,64,128,256}, 32-byte aligned X/Y, max_block_warps <= 32");
     // L2 residency of X: evict_last hints when X fits in L2 (auto), or as requested
     const double x_bytes = 4.0 * (double)p->x_rows * F;
     const bool keep = o.l2_hint < 0 ? x_bytes <= kL2KeepBytes : o.l2_hint > 0;
     a.keep = keep;
     if (kernel == AGCN_KERNEL_WIDE)
-        launch_wide(p, vals, X, F, Y, keep, s);
+        launch_wide(p, vals, X, F, Y, keep, blocked, s);
     else if (v4)
         AGCN_DISPATCH_LT(sh, block_v4, a, s, smem);
     else
         AGCN_DISPATCH_LT(sh, block_v1, a, s, smem);
-    if (p->n_ov > 0) {
+    if (p->n_ov > 0) {  // level 3: oversized rows = fixed-order sums of their partial rows
         const unsigned grid = (unsigned)p->n_ov;
+        const float* part = blocked ? p->sched.partial : p->ov_partial;
+        const int32_t* slots = blocked ? p->sched.slot_base : p->ov_chunk_start;
         if (v4)
-            k_ov_reduce<true><<<grid, kReduceThreads, 0, s>>>(p->ov_partial, p->ov_chunk_start, p->perm,
-                                                              p->ov_start, Y, FV);
+            k_ov_reduce<true><<<grid, kReduceThreads, 0, s>>>(part, slots, p->perm, p->ov_start, Y, FV);
         else
-            k_ov_reduce<false><<<grid, kReduceThreads, 0, s>>>(p->ov_partial, p->ov_chunk_start,
-                                                               p->perm, p->ov_start, Y, FV);
+            k_ov_reduce<false><<<grid, kReduceThreads, 0, s>>>(part, slots, p->perm, p->ov_start, Y, FV);
         post_launch();
     }
 }

@@ -77,7 +77,7 @@ __device__ __forceinline__ float shfl_xor_add(float v, int o) {
 
 struct WideArgs {
     const int4* desc;
-    int64_t nblocks;
+    int64_t n_desc;       // descriptors executed from desc (nblocks, or nb_small with pieces)
     int64_t first_ov;     // descriptor index of the first oversized chunk
     int64_t n_zero;       // sorted rows [0, n_zero) have degree 0
     const int32_t* cols;  // column indices, indexed like vals (rowptr-relative)
@@ -89,11 +89,15 @@ struct WideArgs {
     float* Y;
     float* ovp;           // oversized partial rows [ov_chunks][F]
     int32_t db;           // deg_bound
+    const int4* pieces;   // column-blocked pieces of the oversized rows (sched.cu), or NULL
+    const int32_t* n_pieces;  // device: number of pieces
+    float* piece_partial; // [pieces][F] partial rows (slot-indexed)
+    int64_t piece_cap;    // upper bound of the piece count (grid sizing)
 };
 
 // L lanes per X row (F = 8 L), U X rows in flight per lane, MINB resident CTAs per SM
 // (register budget), KEEP: X-row loads carry an L2 evict_last hint.
-template <int L, int U, int MINB, bool KEEP, bool PREF>
+template <int L, int U, int MINB, bool KEEP, bool PIECES>
 __global__ void __launch_bounds__(kThreads, MINB) k_spmm_wide(const __grid_constant__ WideArgs a) {
     constexpr int G = 32 / L;
     constexpr int F = 8 * L;
@@ -117,28 +121,30 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_wide(const __grid_const
         }
     }
 
-    const int32_t nblocks = (int32_t)a.nblocks;
-    int4 m_next = PREF && gw < nblocks ? __ldg(a.desc + gw) : make_int4(0, 0, 0, 0);
-    for (int32_t b = gw; b < nblocks; b += W) {
-        int4 m;
-        if (PREF) {                                      // descriptor prefetched one step ahead
-            m = m_next;
-            if (b + W < nblocks) m_next = __ldg(a.desc + b + W);
-        } else {
-            m = __ldg(a.desc + b);
-        }
-        const bool ov = m.x > a.db;
+    // execution list: the plan's descriptors [0, n_desc), then (when the column-blocked
+    // schedule replaces the oversized chunks) its pieces, block-major
+    const int32_t n_desc = (int32_t)a.n_desc;
+    const int32_t n_exec = n_desc + (PIECES ? __ldg(a.n_pieces) : 0);
+    for (int32_t b = gw; b < n_exec; b += W) {
+        const bool piece = PIECES && b >= n_desc;
+        const int4 m = piece ? __ldg(a.pieces + (b - n_desc)) : __ldg(a.desc + b);
+        const bool ov = piece || m.x > a.db;
         const int32_t R = ov ? 1 : (m.w & 0xffff);      // rows of the descriptor (<= 32)
-        const int32_t d = ov ? m.w : m.x;               // nonzeros per row (chunk size if ov)
+        const int32_t d = ov ? m.w : m.x;               // nonzeros per row (chunk / piece size if ov)
+        const int32_t slot = PIECES ? -1 - m.x : 0;     // a piece's partial row
         // per-row data, one row per lane: where the row's entries start in the caller's
         // colidx / vals (P:295 step (3) row-pointer update), and its output row
         int32_t rso_l = 0, dst_l = 0;
         if (lane < R) {
-            rso_l = __ldg(a.rso + m.z + lane);
-            if (ov)
-                rso_l += m.y - __ldg(a.srp + m.z);      // chunk offset inside the row
-            else
-                dst_l = __ldg(a.perm + m.z + lane);
+            if (piece) {
+                rso_l = m.y;
+            } else {
+                rso_l = __ldg(a.rso + m.z + lane);
+                if (ov)
+                    rso_l += m.y - __ldg(a.srp + m.z);  // chunk offset inside the row
+                else
+                    dst_l = __ldg(a.perm + m.z + lane);
+            }
         }
         int K = 1;                                       // combined warps per row
         while (2 * K * R <= G) K *= 2;
@@ -188,7 +194,9 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_wide(const __grid_const
                             const int32_t r = s + rowi * G;
                             const int32_t o = __shfl_sync(0xffffffffu, dst_l, min(r, 31));
                             if (r < R) {
-                                float* dst = ov ? a.ovp + (int64_t)(b - a.first_ov) * F : a.Y + (int64_t)o * F;
+                                float* dst = !ov ? a.Y + (int64_t)o * F
+                                 : piece ? a.piece_partial + (int64_t)slot * F
+                                         : a.ovp + (int64_t)(b - a.first_ov) * F;
                                 st8(dst + li * 8, acc);
                             }
                             acc.a = acc.b = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -261,23 +269,25 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_wide(const __grid_const
             }
             const int32_t rd = __shfl_sync(0xffffffffu, dst_l, r & 31);
             if (k == 0 && r < R) {
-                float* dst = ov ? a.ovp + (int64_t)(b - a.first_ov) * F : a.Y + (int64_t)rd * F;
+                float* dst = !ov ? a.Y + (int64_t)rd * F
+                                 : piece ? a.piece_partial + (int64_t)slot * F
+                                         : a.ovp + (int64_t)(b - a.first_ov) * F;
                 st8(dst + li * 8, acc);
             }
         }
     }
 }
 
-template <int L, int U, int MINB, bool KEEP, bool PREF>
+template <int L, int U, int MINB, bool KEEP, bool PIECES>
 void launch_t(const WideArgs& a, cudaStream_t s) {
-    auto kern = k_spmm_wide<L, U, MINB, KEEP, PREF>;
+    auto kern = k_spmm_wide<L, U, MINB, KEEP, PIECES>;
     static int occ = -1;
     if (occ < 0) {
         AGCN_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kThreads, 0));
         if (occ < 1) occ = 1;
     }
     constexpr int G = 32 / L;
-    const int64_t work = std::max<int64_t>(a.nblocks, (a.n_zero + G - 1) / G);
+    const int64_t work = std::max<int64_t>(a.n_desc + (a.pieces ? a.piece_cap : 0), (a.n_zero + G - 1) / G);
     const int64_t want = (work + kWarps - 1) / kWarps;
     const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)num_sms() * occ));
     kern<<<(unsigned)grid, kThreads, 0, s>>>(a);
@@ -289,27 +299,24 @@ int env_int(const char* name, int dflt) {  // experiment switch
     return v ? atoi(v) : dflt;
 }
 
-template <int L, int U, int MINB, bool PREF>
+template <int L, int U, int MINB>
 void launch_k(const WideArgs& a, bool keep, cudaStream_t s) {
-    if (keep)
-        launch_t<L, U, MINB, true, PREF>(a, s);
+    if (a.pieces)
+        keep ? launch_t<L, U, MINB, true, true>(a, s) : launch_t<L, U, MINB, false, true>(a, s);
     else
-        launch_t<L, U, MINB, false, PREF>(a, s);
+        keep ? launch_t<L, U, MINB, true, false>(a, s) : launch_t<L, U, MINB, false, false>(a, s);
 }
 
 template <int L>
 void launch(const WideArgs& a, bool keep, cudaStream_t s) {
-    // register budget vs rows in flight (AGCN_WIDE_VARIANT, A/B only; profiles/r01*_wide*):
-    //   0: U 4 at 3 CTAs/SM (80 regs, no spills; the default)   1: same + descriptor prefetch
-    //   2: U 8 at 2 CTAs/SM + descriptor prefetch               3: U 4 at 4 CTAs/SM (64 regs)
+    // register budget vs rows in flight (AGCN_WIDE_VARIANT, A/B only; profiles/r01k_wide_ab.md):
+    //   0: U 4 at 3 CTAs/SM (80 regs, no spills; the default)   3: U 4 at 4 CTAs/SM (64 regs)
     static const int variant = env_int("AGCN_WIDE_VARIANT", 0);
-    constexpr int U4 = L >= 4 ? 4 : L, U8 = L >= 8 ? 8 : U4;
-    switch (variant) {
-        case 1: launch_k<L, U4, 3, true>(a, keep, s); break;
-        case 2: launch_k<L, U8, 2, true>(a, keep, s); break;
-        case 3: launch_k<L, U4, 4, false>(a, keep, s); break;
-        default: launch_k<L, U4, 3, false>(a, keep, s); break;
-    }
+    constexpr int U4 = L >= 4 ? 4 : L;
+    if (variant == 3)
+        launch_k<L, U4, 4>(a, keep, s);
+    else
+        launch_k<L, U4, 3>(a, keep, s);
 }
 
 }  // namespace
@@ -321,10 +328,13 @@ bool wide_supported(const agcn_plan_s* p, const float* X, const float* Y, int32_
 }
 
 void launch_wide(agcn_plan_s* p, const float* vals, const float* X, int32_t F, float* Y,
-                 bool l2_keep, cudaStream_t s) {
-    WideArgs a{p->desc, p->nblocks, p->nb_small, p->n_zero, p->cols, p->sorted_rowptr,
-               p->row_src_off, p->perm, vals + p->rp_base, X, Y, p->ov_partial, p->deg_bound};
-    AGCN_CHECK(p->nblocks < (1ll << 31), AGCN_ERR_OVERFLOW, "too many descriptors");
+                 bool l2_keep, bool blocked, cudaStream_t s) {
+    const ColSched& cs = p->sched;
+    WideArgs a{p->desc, blocked ? p->nb_small : p->nblocks, p->nb_small, p->n_zero, p->cols,
+               p->sorted_rowptr, p->row_src_off, p->perm, vals + p->rp_base, X, Y, p->ov_partial,
+               p->deg_bound, blocked ? cs.seg : nullptr, blocked ? cs.slot_base + p->n_ov : nullptr,
+               blocked ? cs.partial : nullptr, blocked ? cs.cap : 0};
+    AGCN_CHECK(a.n_desc + a.piece_cap < (1ll << 31), AGCN_ERR_OVERFLOW, "too many descriptors");
     switch (F) {
         case 8: launch<1>(a, l2_keep, s); break;
         case 16: launch<2>(a, l2_keep, s); break;

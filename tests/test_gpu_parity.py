@@ -157,6 +157,36 @@ def test_spmm_every_kernel(kernel, F):
         check_spmm(p, rowptr, colidx, vals, X, kernel=kernel)
 
 
+@pytest.mark.parametrize("F", [8, 64, 128, 256])
+def test_column_blocked_oversized_rows(F):
+    """Oversized rows executed as column-blocked pieces (agcn_spmm_opts_t.col_block_mb) give
+    the oracle's result; unsorted rows (plain chunks) and sorted rows mixed; deterministic."""
+    rng = np.random.default_rng(F)
+    n_cols = 100000
+    degs = np.array([0, 3, 385, 900, 5000, 17, 384, 2000, 769, 12000, 1, 0, 400, 2100, 30000])
+    rowptr, colidx = _rows_csr(degs, n_cols, 3)
+    colidx = colidx.copy()
+    for r in range(degs.size):  # canonical CSR: sorted columns per row (duplicates kept)
+        colidx[rowptr[r]:rowptr[r + 1]].sort()
+    for r in (2, 7):  # two light rows with unsorted columns
+        a, b = rowptr[r], rowptr[r + 1]
+        colidx[a:b] = rng.permutation(colidx[a:b])
+    a = rowptr[9] + 1000  # a heavy row unsorted in a window straddling two chunks
+    colidx[a:a + 500] = rng.permutation(colidx[a:a + 500])
+    a = rowptr[14] + 384 * 7  # a chunk of a heavy row starting below the previous entry
+    colidx[a:a + 384] = np.sort(rng.integers(0, 50, 384))
+    vals = rng.uniform(-1, 1, colidx.size).astype(np.float32)
+    X = rng.uniform(-1, 1, (n_cols, F)).astype(np.float32)
+    p = make_plan(rowptr, colidx, n_cols=n_cols)
+    Ys = []
+    for mb in (1, 2, 0):  # 1 MiB and 2 MiB blocks, then off
+        Y = p.spmm(cu(vals), cu(X), kernel="wide", col_block_mb=mb).cpu().numpy()
+        check_spmm(p, rowptr, colidx, vals, X, Y)
+        Ys.append(Y)
+    Y2 = p.spmm(cu(vals), cu(X), kernel="wide", col_block_mb=1).cpu().numpy()
+    assert np.array_equal(Ys[0], Y2)          # bitwise reproducible
+
+
 def test_spmm_kernel_unsupported_is_reported():
     w = gen.make_config("c1")
     p = make_plan(w.rowptr, w.colidx)
