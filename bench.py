@@ -40,7 +40,7 @@ def parse():
     ap.add_argument("--F", type=int, default=None)
     ap.add_argument("--layers", type=int, default=None)
     ap.add_argument("--partition", choices=["block", "warp"], default="block")
-    ap.add_argument("--kernel", choices=["auto", "general", "wide"], default="auto")
+    ap.add_argument("--kernel", choices=["auto", "general", "wide", "pipe"], default="auto")
     ap.add_argument("--l2-hint", type=int, default=None, help="None: auto; 0: never; 1: always")
     ap.add_argument("--col-block-mb", type=int, default=None,
                     help="None: auto; 0: off (paper chunks); MiB of X per column block")

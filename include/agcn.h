@@ -132,8 +132,10 @@ typedef enum {
     AGCN_KERNEL_AUTO = 0,    /* WIDE when applicable, else GENERAL */
     AGCN_KERNEL_GENERAL = 1, /* any F: float4 (F % 4 == 0, 16-B aligned X/Y) or scalar lanes;
                                 shared-memory staging of each descriptor's colidx / vals */
-    AGCN_KERNEL_WIDE = 3     /* F in {8,16,32,64,128,256}, 32-B aligned X/Y, max_block_warps
+    AGCN_KERNEL_WIDE = 3,    /* F in {8,16,32,64,128,256}, 32-B aligned X/Y, max_block_warps
                                 <= 32: one 256-bit row slice per lane, shuffle-broadcast CSR */
+    AGCN_KERNEL_PIPE = 4     /* F in {32,64,128,256}, 32-B aligned X/Y, max_block_warps <= 32:
+                                as WIDE, X rows gathered through a cp.async shared-memory ring */
 } agcn_kernel_t;
 
 typedef struct {

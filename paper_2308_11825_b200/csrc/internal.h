@@ -159,6 +159,9 @@ void spmm_launch(agcn_plan_s* p, const float* vals, const float* X, int32_t F, f
 bool wide_supported(const agcn_plan_s* p, const float* X, const float* Y, int32_t F);
 void launch_wide(agcn_plan_s* p, const float* vals, const float* X, int32_t F, float* Y,
                  bool l2_keep, bool blocked, cudaStream_t s);
+// spmm_pipe.cu: cp.async shared-memory gather pipeline, F in {32,64,128,256}
+bool pipe_supported(const agcn_plan_s* p, const float* X, const float* Y, int32_t F);
+void launch_pipe(agcn_plan_s* p, const float* vals, const float* X, int32_t F, float* Y, cudaStream_t s);
 // sched.cu
 int col_sched_shift(const agcn_plan_s* p, int32_t F, double target_bytes);
 void build_col_sched(agcn_plan_s* p, int shift, int32_t F, cudaStream_t s);

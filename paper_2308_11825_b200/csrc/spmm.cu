@@ -549,6 +549,8 @@ void spmm_launch(agcn_plan_s* p, const float* vals, const float* X, int32_t F, f
     if (kernel == AGCN_KERNEL_AUTO) kernel = wide_ok ? AGCN_KERNEL_WIDE : AGCN_KERNEL_GENERAL;
     AGCN_CHECK(kernel != AGCN_KERNEL_WIDE || wide_ok, AGCN_ERR_UNSUPPORTED,
                "WIDE kernel needs F in {8,16,32,64,128,256}, 32-byte aligned X/Y, max_block_warps <= 32");
+    AGCN_CHECK(kernel != AGCN_KERNEL_PIPE || pipe_supported(p, X, Y, F), AGCN_ERR_UNSUPPORTED,
+               "PIPE kernel needs F in {32,64,128,256}, 32-byte aligned X/Y, max_block_warps <= 32");
     // column-blocked oversized rows (WIDE kernel, sched.cu): X slice per block ~ col_block_mb
     bool blocked = false;
     if (kernel == AGCN_KERNEL_WIDE && o.col_block_mb > 0) {
@@ -591,7 +593,9 @@ void spmm_launch(agcn_plan_s* p, const float* vals, const float* X, int32_t F, f
     const double x_bytes = 4.0 * (double)p->x_rows * F;
     const bool keep = o.l2_hint < 0 ? x_bytes <= kL2KeepBytes : o.l2_hint > 0;
     a.keep = keep;
-    if (kernel == AGCN_KERNEL_WIDE)
+    if (kernel == AGCN_KERNEL_PIPE)
+        launch_pipe(p, vals, X, F, Y, s);
+    else if (kernel == AGCN_KERNEL_WIDE)
         launch_wide(p, vals, X, F, Y, keep, blocked, s);
     else if (v4)
         AGCN_DISPATCH_LT(sh, block_v4, a, s, smem);
