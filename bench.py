@@ -40,7 +40,7 @@ def parse():
     ap.add_argument("--F", type=int, default=None)
     ap.add_argument("--layers", type=int, default=None)
     ap.add_argument("--partition", choices=["block", "warp"], default="block")
-    ap.add_argument("--kernel", choices=["auto", "general", "wide", "pipe"], default="auto")
+    ap.add_argument("--kernel", choices=["auto", "general", "looped", "wide", "pipe"], default="auto")
     ap.add_argument("--l2-hint", type=int, default=None, help="None: auto; 0: never; 1: always")
     ap.add_argument("--col-block-mb", type=int, default=None,
                     help="None: auto; 0: off (paper chunks); MiB of X per column block")
@@ -49,6 +49,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cusparse", action="store_true")
+    ap.add_argument("--no-graph", action="store_true", help="skip the CUDA-graph kernel-only timing")
     ap.add_argument("--profile", action="store_true",
                     help="short run for ncu: no clocks/e2e/cpu/cusparse legs")
     return ap.parse_args()
@@ -325,13 +326,51 @@ def main():
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                          "frac": achieved / peaks["hbm_gbs"], "traffic": traffic,
                          "kernel": "agcn_spmm (%s + k_ov_reduce)" % (
-                             "k_spmm_wide" if args.kernel != "general" and F in (8, 16, 32, 64, 128, 256)
+                             "k_spmm_pipe" if args.kernel == "pipe" else
+                             "k_spmm_wide" if args.kernel in ("auto", "wide") and F in (8, 16, 32, 64, 128, 256)
                              else "k_spmm_block"),
                          "bytes_per_launch": b_comp, "peak_source": peaks["source"],
                          "traffic_source": traffic_src},
             "gpu_launches": int(launches),
             "clocks": clk,
         }
+
+    # ---- kernel-only SpMM time (the paper's protocol): 20 agcn_spmm calls captured in
+    # one CUDA graph and replayed, so host launch overhead is excluded (warm L2 when the
+    # inputs fit in it)
+    if rank == 0 and P == 1 and not args.profile and not args.no_graph:
+        try:
+            S = torch.cuda.Stream()
+            with torch.cuda.stream(S):
+                plan_g = A.Plan(rp_local, ci_d, stream=S, **plan_kw)
+                Yg = torch.empty((n, F), dtype=torch.float32, device=dev)
+                run = lambda: plan_g.spmm(va_d, X0, out=Yg, stream=S, kernel=args.kernel,  # noqa: E731
+                                          l2_hint=args.l2_hint, col_block_mb=args.col_block_mb)
+                for _ in range(3):
+                    run()
+            torch.cuda.synchronize()
+            reps = 20
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=S):
+                for _ in range(reps):
+                    run()
+            g.replay()
+            torch.cuda.synchronize()
+            a, b = ev(), ev()
+            with torch.cuda.stream(S):  # replay() launches on the current stream
+                a.record(S)
+                for _ in range(3):
+                    g.replay()
+                b.record(S)
+            torch.cuda.synchronize()
+            gms = a.elapsed_time(b) / (3 * reps)
+            line["spmm_graph"] = {"ms_per_layer": gms, "gflops": flops_layer / (gms * 1e-3) / 1e9,
+                                  "b_comp_gbs": b_comp / (gms * 1e-3) / 1e9,
+                                  "how": f"{reps} agcn_spmm in one CUDA graph, replayed 3x"}
+            del g
+            plan_g.close()
+        except Exception as e:  # pragma: no cover
+            line["spmm_graph"] = {"error": str(e)[:200]}
 
     # ---- cuSPARSE on the same box (1 GPU, whole graph, one layer)
     if rank == 0 and P == 1 and not args.no_cusparse and not args.profile:
@@ -351,6 +390,33 @@ def main():
             line["cusparse"] = {"ms_per_layer": cms, "gflops": flops_layer / (cms * 1e-3) / 1e9,
                                 "via": "torch.sparse.mm (cusparseSpMM, CSR)",
                                 "speedup_agcn_spmm": cms / spmm_max}
+            if not args.no_graph:  # kernel-only, like spmm_graph
+                try:
+                    S2 = torch.cuda.Stream()
+                    with torch.cuda.stream(S2):
+                        for _ in range(3):
+                            torch.sparse.mm(Acsr, Xd)
+                    torch.cuda.synchronize()
+                    g2 = torch.cuda.CUDAGraph()
+                    with torch.cuda.graph(g2, stream=S2):
+                        for _ in range(10):
+                            torch.sparse.mm(Acsr, Xd)
+                    g2.replay()
+                    torch.cuda.synchronize()
+                    a, b = ev(), ev()
+                    with torch.cuda.stream(S2):
+                        a.record(S2)
+                        for _ in range(3):
+                            g2.replay()
+                        b.record(S2)
+                    torch.cuda.synchronize()
+                    cg = a.elapsed_time(b) / 30
+                    line["cusparse"]["graph_ms_per_layer"] = cg
+                    if "ms_per_layer" in line.get("spmm_graph", {}):
+                        line["cusparse"]["graph_speedup_agcn_spmm"] = cg / line["spmm_graph"]["ms_per_layer"]
+                    del g2
+                except Exception as e:  # pragma: no cover
+                    line["cusparse"]["graph_error"] = str(e)[:160]
         except Exception as e:  # pragma: no cover
             line["cusparse"] = {"error": str(e)[:200]}
 

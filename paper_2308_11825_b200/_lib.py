@@ -22,7 +22,7 @@ class Opts(ctypes.Structure):
                 ("col_slot_rows", c_i64)]
 
 
-KERNELS = {"auto": 0, "general": 1, "wide": 3, "pipe": 4}
+KERNELS = {"auto": 0, "general": 1, "looped": 2, "wide": 3, "pipe": 4}
 
 
 class SpmmOpts(ctypes.Structure):

@@ -123,9 +123,8 @@ agcn_status_t agcn_spmm_ex(agcn_plan_t plan, const float* vals, const float* X, 
         AGCN_CHECK(F > 0, AGCN_ERR_INVALID_ARG, "F must be > 0");
         agcn_spmm_opts_t o;
         if (opts) o = *opts; else agcn_default_spmm_opts(&o);
-        AGCN_CHECK(o.kernel == AGCN_KERNEL_AUTO || o.kernel == AGCN_KERNEL_GENERAL ||
-                       o.kernel == AGCN_KERNEL_WIDE || o.kernel == AGCN_KERNEL_PIPE,
-                   AGCN_ERR_INVALID_ARG, "unknown kernel");
+        AGCN_CHECK(o.kernel >= AGCN_KERNEL_AUTO && o.kernel <= AGCN_KERNEL_PIPE, AGCN_ERR_INVALID_ARG,
+                   "unknown kernel");
         AGCN_CHECK(o.l2_hint >= -1 && o.l2_hint <= 1, AGCN_ERR_INVALID_ARG, "l2_hint must be -1, 0 or 1");
         AGCN_CHECK(o.col_block_mb >= -1, AGCN_ERR_INVALID_ARG, "col_block_mb must be >= -1");
         if (plan->n == 0) return;

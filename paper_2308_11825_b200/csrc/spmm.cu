@@ -530,9 +530,12 @@ void spmm_launch(agcn_plan_s* p, const float* vals, const float* X, int32_t F, f
         agcn_plan_s* p; cudaStream_t s; bool on;
         ~Rec() { if (on) cudaEventRecord(p->last_use, s); }
     } rec{p, s, foreign};
-    const bool v4 = (F % 4 == 0) && aligned16(X) && aligned16(Y);
+    // LOOPED (ablation 2, Fig. 4(a) / Table II): no combined warp -- one warp of 32 scalar lanes
+    // walks the columns of a row in strides of 32
+    const bool looped = o.kernel == AGCN_KERNEL_LOOPED;
+    const bool v4 = !looped && (F % 4 == 0) && aligned16(X) && aligned16(Y);
     const int32_t FV = v4 ? F / 4 : F;
-    const Shape sh = pick_shape(FV);
+    const Shape sh = looped ? Shape{32, 1} : pick_shape(FV);
     if (p->partition == AGCN_PARTITION_WARP) {
         AGCN_CUDA(cudaMemsetAsync(Y, 0, sizeof(float) * (size_t)p->n * F, s));
         if (p->ntasks == 0) return;
@@ -547,6 +550,7 @@ void spmm_launch(agcn_plan_s* p, const float* vals, const float* X, int32_t F, f
     const bool wide_ok = wide_supported(p, X, Y, F);
     int kernel = o.kernel;
     if (kernel == AGCN_KERNEL_AUTO) kernel = wide_ok ? AGCN_KERNEL_WIDE : AGCN_KERNEL_GENERAL;
+    if (kernel == AGCN_KERNEL_LOOPED) kernel = AGCN_KERNEL_GENERAL;  // with the {32 lanes, scalar} shape
     AGCN_CHECK(kernel != AGCN_KERNEL_WIDE || wide_ok, AGCN_ERR_UNSUPPORTED,
                "WIDE kernel needs F in {8,16,32,64,128,256}, 32-byte aligned X/Y, max_block_warps <= 32");
     AGCN_CHECK(kernel != AGCN_KERNEL_PIPE || pipe_supported(p, X, Y, F), AGCN_ERR_UNSUPPORTED,

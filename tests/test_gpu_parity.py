@@ -138,6 +138,7 @@ def test_spmm_c2_F(F):
 
 
 KERNEL_F = [("general", F) for F in (3, 4, 16, 64, 128, 100)] + \
+    [("looped", F) for F in (1, 16, 33, 64, 100, 128)] + \
     [("wide", F) for F in (8, 16, 32, 64, 128, 256)] + \
     [("pipe", F) for F in (32, 64, 128, 256)]
 
@@ -206,7 +207,7 @@ def test_wide_kernel_nonfinite_x_rows_not_referenced():
     X = np.ones((7, 64), dtype=np.float32)
     X[0] = np.inf
     X[6] = np.nan
-    for kernel in ("auto", "general", "wide", "pipe"):
+    for kernel in ("auto", "general", "looped", "wide", "pipe"):
         p = make_plan(rowptr, colidx, n_cols=7)
         Y = p.spmm(cu(vals), cu(X), kernel=kernel).cpu().numpy()
         assert np.isfinite(Y).all(), kernel
