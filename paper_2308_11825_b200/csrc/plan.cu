@@ -13,6 +13,7 @@
 // and, for the ablation arm, the warp-level partition of Fig. 3(b)    P:417.
 #include <algorithm>
 #include <cstring>
+#include <mutex>
 #include <vector>
 
 #include "internal.h"
@@ -387,6 +388,46 @@ void set_spmm_cols(agcn_plan_s* p, const int32_t* colidx, cudaStream_t s) {
     p->cols = p->cols_copy;
 }
 
+// A second stream per device for plan work that can overlap the main sequence (validation).
+cudaStream_t aux_stream(int dev) {
+    static std::mutex mu;
+    static cudaStream_t streams[64] = {};
+    std::lock_guard<std::mutex> lock(mu);
+    if (dev < 0 || dev >= 64) return nullptr;
+    if (!streams[dev]) AGCN_CUDA(cudaStreamCreateWithFlags(&streams[dev], cudaStreamNonBlocking));
+    return streams[dev];
+}
+
+// Fork / join of one overlap region.  If the region is left early (an error), the main
+// stream still waits for the side work before anything declared earlier (scratch freed on
+// the main stream) is released.
+struct Overlap {
+    cudaStream_t main, side;
+    cudaEvent_t fork = nullptr, join = nullptr;
+    bool joined = false;
+    Overlap(cudaStream_t m, cudaStream_t sd) : main(m), side(sd) {
+        if (!side) return;
+        AGCN_CUDA(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
+        AGCN_CUDA(cudaEventCreateWithFlags(&join, cudaEventDisableTiming));
+        AGCN_CUDA(cudaEventRecord(fork, main));
+        AGCN_CUDA(cudaStreamWaitEvent(side, fork, 0));
+    }
+    void finish() {  // after the side work is enqueued: main waits for it
+        if (!side || joined) return;
+        AGCN_CUDA(cudaEventRecord(join, side));
+        AGCN_CUDA(cudaStreamWaitEvent(main, join, 0));
+        joined = true;
+    }
+    ~Overlap() {
+        if (side && !joined) {
+            cudaEventRecord(join, side);
+            cudaStreamWaitEvent(main, join, 0);
+        }
+        if (fork) cudaEventDestroy(fork);
+        if (join) cudaEventDestroy(join);
+    }
+};
+
 // ---------------------------------------------------------------- block-partition plan
 void build_block_plan(agcn_plan_s* p, const int32_t* rowptr, const int32_t* colidx,
                       const agcn_opts_t& o, cudaStream_t s) {
@@ -401,12 +442,15 @@ void build_block_plan(agcn_plan_s* p, const int32_t* rowptr, const int32_t* coli
     AGCN_CUDA(cudaMemsetAsync(d_flags, 0, sizeof(PlanFlags), s));
     AGCN_CUDA(cudaMemsetAsync(bin_cnt, 0, sizeof(int32_t) * nbins, s));
 
+    // colidx validation on a second stream, overlapping the histogram and scan below
+    Overlap ov(s, o.validate && nnz > 0 ? aux_stream(p->device) : nullptr);
+    if (o.validate) validate_cols(rowptr, colidx, nnz, p->n_cols, d_flags, ov.side ? ov.side : s);
     // (1)+(2a) per-tile bucket histograms, bucket totals, max degree, rowptr validation
     k_deg_hist<<<(unsigned)ntiles, kThreads, nbins * sizeof(int32_t), s>>>(rowptr, n, db, nbins, ntiles,
                                                                          table, bin_cnt, d_flags);
     post_launch();
-    if (o.validate) validate_cols(rowptr, colidx, nnz, p->n_cols, d_flags, s);
     exclusive_scan_i32(table, table, (int64_t)nbins * ntiles, s);
+    ov.finish();
 
     std::vector<int32_t> h_cnt(nbins);
     PlanFlags hf{};

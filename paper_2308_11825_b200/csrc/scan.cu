@@ -89,11 +89,44 @@ __global__ void __launch_bounds__(kScanThreads) k_tile_scan(const int32_t* __res
     if (blockIdx.x == 0 && threadIdx.x == 0) out[n] = sums[ntiles];
 }
 
+// One CTA for short arrays (one launch instead of three): tiles in order with a carry.
+// In place is fine: every tile is read before it is written, by the same threads.
+__global__ void __launch_bounds__(kScanThreads) k_scan_small(const int32_t* __restrict__ in,
+                                                            int32_t* __restrict__ out, int64_t n) {
+    int32_t carry = 0;
+    for (int64_t t0 = 0; t0 < n; t0 += kScanTile) {
+        const int64_t base = t0 + (int64_t)threadIdx.x * kScanItems;
+        int32_t v[kScanItems];
+        int32_t sum = 0;
+#pragma unroll
+        for (int i = 0; i < kScanItems; ++i) {
+            v[i] = base + i < n ? in[base + i] : 0;
+            sum += v[i];
+        }
+        int32_t tot;
+        int32_t ex = block_excl_scan(sum, &tot) + carry;
+#pragma unroll
+        for (int i = 0; i < kScanItems; ++i) {
+            if (base + i < n) out[base + i] = ex;
+            ex += v[i];
+        }
+        carry += tot;
+    }
+    if (threadIdx.x == 0) out[n] = carry;
+}
+
+constexpr int64_t kSmallScan = 16 * kScanTile;  // up to 64K elements: single CTA
+
 }  // namespace
 
 void exclusive_scan_i32(const int32_t* in, int32_t* out, int64_t n, cudaStream_t s) {
     if (n <= 0) {
         AGCN_CUDA(cudaMemsetAsync(out, 0, sizeof(int32_t), s));
+        return;
+    }
+    if (n <= kSmallScan) {
+        k_scan_small<<<1, kScanThreads, 0, s>>>(in, out, n);
+        post_launch();
         return;
     }
     const int64_t ntiles = (n + kScanTile - 1) / kScanTile;
