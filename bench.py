@@ -50,6 +50,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cusparse", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="skip the CUDA-graph kernel-only timing")
+    ap.add_argument("--dist-backend", choices=["nccl", "gloo"], default="nccl",
+                    help="gloo: test mode, every rank on cuda:0, all-gather staged through the host")
     ap.add_argument("--profile", action="store_true",
                     help="short run for ncu: no clocks/e2e/cpu/cusparse legs")
     return ap.parse_args()
@@ -187,15 +189,20 @@ def main():
 
     import agcn_inputs as gen
     import paper_2308_11825_b200 as A
-    from paper_2308_11825_b200.dist import ShardLayout, propagate
+    from paper_2308_11825_b200.dist import ShardLayout, make_all_gather, propagate
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.dist_backend == "gloo":  # test mode: all ranks share cuda:0 (no NCCL, no NVLink)
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group("gloo")
     P = world
     A.library_path()
 
@@ -224,10 +231,12 @@ def main():
     ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
     rec = {"plan": [], "spmm": [], "ag": []}
 
+    gather = make_all_gather(args.dist_backend) if P > 1 else None
+
     def all_gather(full, slot):
         e0, e1 = ev(), ev()
         e0.record(stream)
-        dist.all_gather_into_tensor(full, slot)
+        gather(full, slot)
         e1.record(stream)
         rec["ag"].append((e0, e1))
 
@@ -457,7 +466,7 @@ def main():
                 pe = A.Plan(rp_e, ci_e, **plan_kw)
                 bufs_e = [torch.empty_like(Xe) for _ in range(min(layers, 2))]
                 oute = propagate(lay, lambda Xin, o: pe.spmm(va_e, Xin, out=o), Xe, bufs_e, layers,
-                                 lambda full, slot: dist.all_gather_into_tensor(full, slot))
+                                 gather)
                 Y_h.copy_(lay.own_rows(oute))
                 torch.cuda.synchronize()
                 dt = torch.tensor([time.perf_counter() - t0], device=dev)

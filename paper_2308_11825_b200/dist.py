@@ -94,3 +94,25 @@ def propagate(layout: ShardLayout, spmm, X0, bufs, layers: int, all_gather=None)
             all_gather(nxt, layout.slot(nxt))
         cur = nxt
     return cur
+
+
+def make_all_gather(backend: str):
+    """In-place all-gather of the S-row slots of a padded [P*S, F] buffer.
+
+    nccl: one ``all_gather_into_tensor`` on the device buffer (NVLink / NVSwitch).
+    gloo: the same collective staged through host memory -- only for testing the multi-rank
+    path with several ranks on one GPU (gloo has no device all-gather).
+    """
+    import torch.distributed as dist
+
+    if backend == "nccl":
+        return lambda full, slot: dist.all_gather_into_tensor(full, slot)
+
+    def gloo_all_gather(full, slot):
+        h_full = full.cpu()
+        n = slot.shape[0]
+        rank = dist.get_rank()
+        dist.all_gather_into_tensor(h_full, h_full[rank * n:(rank + 1) * n].clone())
+        full.copy_(h_full)
+
+    return gloo_all_gather
