@@ -50,6 +50,10 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cusparse", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="skip the CUDA-graph kernel-only timing")
+    ap.add_argument("--aggregation", choices=["sum", "mean"], default="sum",
+                    help="sum: GCN (the metric's workload); mean: GraphSAGE-mean (P:126)")
+    ap.add_argument("--gin-eps", type=float, default=None, help="GIN self term (1 + eps) x_i (square A)")
+    ap.add_argument("--bias-relu", action="store_true", help="fused bias + ReLU epilogue")
     ap.add_argument("--dist-backend", choices=["nccl", "gloo"], default="nccl",
                     help="gloo: test mode, every rank on cuda:0, all-gather staged through the host")
     ap.add_argument("--profile", action="store_true",
@@ -227,6 +231,18 @@ def main():
     if P > 1:
         plan_kw.update(col_bounds=bounds, col_slot_rows=S)
 
+    bias_d = torch.linspace(-0.5, 0.5, F, device=dev) if args.bias_relu else None
+
+    def epi_kw(Xin):  # aggregation variant / epilogue of agcn_spmm; default: plain GCN sum
+        kw = {"aggregation": args.aggregation}
+        if args.gin_eps is not None:
+            if P > 1:
+                raise SystemExit("--gin-eps: single GPU only (the self rows are the rank's own rows)")
+            kw.update(self_x=Xin, self_scale=1.0 + args.gin_eps)
+        if args.bias_relu:
+            kw.update(bias=bias_d, relu=True)
+        return kw
+
     stream = torch.cuda.current_stream()
     ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
     rec = {"plan": [], "spmm": [], "ag": []}
@@ -252,7 +268,7 @@ def main():
             s0, s1 = ev(), ev()
             s0.record(stream)
             plan.spmm(va_d, Xin, out=out_rows, kernel=args.kernel, l2_hint=args.l2_hint,
-                      col_block_mb=args.col_block_mb)
+                      col_block_mb=args.col_block_mb, **epi_kw(Xin))
             s1.record(stream)
             if record:
                 rec["spmm"].append((s0, s1))
@@ -322,7 +338,8 @@ def main():
             "scaling": "strong" if P > 1 else "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic",
             "config": {"workload": w.meta["desc"], "name": w.name, "n": n, "nnz": nnz, "F": F,
-                       "layers": layers, "partition": args.partition, "kernel": args.kernel, "parallelism": f"row-shard{P}",
+                       "layers": layers, "partition": args.partition, "kernel": args.kernel,
+                       "aggregation": args.aggregation, "gin_eps": args.gin_eps, "bias_relu": args.bias_relu, "parallelism": f"row-shard{P}",
                        "max_block_warps": 12, "max_warp_nzs": 32,
                        "l2": "inputs larger than L2 (CSR + X > 126 MB)" if
                              (8 * nnz + 4 * n * F) > 126e6 else "inputs fit in L2 (warm)",
@@ -354,7 +371,8 @@ def main():
                 plan_g = A.Plan(rp_local, ci_d, stream=S, **plan_kw)
                 Yg = torch.empty((n, F), dtype=torch.float32, device=dev)
                 run = lambda: plan_g.spmm(va_d, X0, out=Yg, stream=S, kernel=args.kernel,  # noqa: E731
-                                          l2_hint=args.l2_hint, col_block_mb=args.col_block_mb)
+                                          l2_hint=args.l2_hint, col_block_mb=args.col_block_mb,
+                                          **epi_kw(X0))
                 for _ in range(3):
                     run()
             torch.cuda.synchronize()

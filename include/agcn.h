@@ -141,6 +141,11 @@ typedef enum {
                                 as WIDE, X rows gathered through a cp.async shared-memory ring */
 } agcn_kernel_t;
 
+typedef enum {
+    AGCN_AGG_SUM = 0,  /* y_i = sum_j a_ij x_j (GCN aggregation) */
+    AGCN_AGG_MEAN = 1  /* y_i = sum_j a_ij x_j / deg_i, 0 for deg_i = 0 (GraphSAGE-mean) */
+} agcn_aggregation_t;
+
 typedef struct {
     int32_t kernel;       /* agcn_kernel_t; default AGCN_KERNEL_AUTO */
     int32_t l2_hint;      /* X-row L2 residency: -1 (default) evict_last hints when X fits in L2
@@ -153,7 +158,17 @@ typedef struct {
                              chunks; measured faster on B200); > 0: MiB per block.
                              Builds a plan-owned schedule on first use per F (stream-ordered,
                              no host synchronisation). */
-    int32_t reserved[5];
+    /* Epilogue, applied to every output row i (fused into the WIDE kernel's stores and the
+       oversized-row reduction; a separate pass over Y for the other kernels):
+         y_i = agg(i) + self_scale * self[i] + bias;  y_i = max(y_i, 0) if relu
+       agg(i) per `aggregation`.  GIN: self = X, self_scale = 1 + eps. */
+    int32_t aggregation;  /* agcn_aggregation_t; default AGCN_AGG_SUM */
+    float self_scale;     /* 0 (default): no self term */
+    int32_t relu;         /* 0 (default) / 1 */
+    const float* self;    /* DEVICE [n x F] row-major, row i pairs with output row i; 16-byte
+                             aligned; required iff self_scale != 0 */
+    const float* bias;    /* DEVICE [F], 16-byte aligned, or NULL */
+    int64_t reserved[4];
 } agcn_spmm_opts_t;
 
 /* Fill *opts with the defaults above. */

@@ -117,6 +117,45 @@ def spmm_check(rowptr, colidx, vals, X, Y, rows=None, rel=REL_TOL, abs_tol=ABS_T
     return {"max_ratio": mr.value, "worst": (int(worst[0]), int(worst[1])), "nfail": int(nf)}
 
 
+def spmm_epilogue(rowptr, colidx, vals, X, aggregation="sum", self_x=None, self_scale=0.0,
+                  bias=None, relu=False):
+    """The aggregation variants of P:126 on top of the fp64 definition (reading Q34):
+    y_i = (sum_j a_ij x_j) * (1 / deg_i if aggregation == "mean", 0 for deg_i = 0)
+          + self_scale * self_x[i] + bias;  y = max(y, 0) if relu.
+    GCN: sum; GraphSAGE-mean: mean; GIN: sum with self_x = X, self_scale = 1 + eps.
+    Returns (y_ref, tol_scale): fp64 result and the magnitude the tolerance is relative to,
+    (scale_i * sum_j |a_ij x_jk| + |self_scale * self_x[i,k]| + |bias_k|)."""
+    y, sabs = spmm(rowptr, colidx, vals, X)
+    deg = np.diff(np.asarray(rowptr, dtype=np.int64)).astype(np.float64)
+    if aggregation == "mean":
+        sc = np.where(deg > 0, 1.0 / np.maximum(deg, 1.0), 0.0)[:, None]
+        y = y * sc
+        sabs = sabs * sc
+    elif aggregation != "sum":
+        raise ValueError(aggregation)
+    if self_scale != 0.0:
+        t = float(np.float32(self_scale)) * np.asarray(self_x, dtype=np.float64)
+        y = y + t
+        sabs = sabs + np.abs(t)
+    if bias is not None:
+        b = np.asarray(bias, dtype=np.float64)[None, :]
+        y = y + b
+        sabs = sabs + np.abs(b)
+    if relu:
+        y = np.maximum(y, 0.0)
+    return y, sabs
+
+
+def check_epilogue(Y, y_ref, tol_scale, rel=REL_TOL, abs_tol=ABS_TOL):
+    """|Y - y_ref| <= rel * tol_scale + abs_tol per element (NaN fails); ReLU is 1-Lipschitz, so
+    the bound of the pre-activation carries over.  Returns dict(max_ratio, nfail)."""
+    Y = np.asarray(Y, dtype=np.float64)
+    err = np.abs(Y - y_ref)
+    ratio = err / (rel * tol_scale + abs_tol)
+    ratio[~np.isfinite(Y)] = np.inf
+    return {"max_ratio": float(ratio.max()) if ratio.size else 0.0, "nfail": int((~(ratio <= 1.0)).sum())}
+
+
 # ---------------------------------------------------------------- preprocessing (P:295)
 def degree_sort(rowptr):
     """Stable ascending counting sort of rows by degree -> perm (sorted_to_orig)."""

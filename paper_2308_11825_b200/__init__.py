@@ -150,13 +150,17 @@ class Plan:
         return out
 
     def spmm(self, vals, X, out=None, stream=None, kernel: str = "auto", l2_hint: int | None = None,
-             col_block_mb: int | None = None):
+             col_block_mb: int | None = None, aggregation: str = "sum", self_x=None,
+             self_scale: float = 0.0, bias=None, relu: bool = False):
         """Y = A.X (asynchronous on `stream`, default the current torch stream).
 
         kernel: "auto" | "general" | "wide" (agcn_kernel_t); l2_hint: None (auto: evict_last
         hints on X rows when X fits in L2), 0 (never) or 1 (always).  col_block_mb: None (auto),
         0 (off: the paper's deg_bound chunks for oversized rows) or the X slice per column block
         in MiB (agcn_spmm_opts_t.col_block_mb).
+        Epilogue (agcn_spmm_opts_t): y_i = agg_i + self_scale * self_x[i] + bias, then ReLU if
+        relu; aggregation "sum" (GCN) or "mean" (GraphSAGE-mean, / deg_i); GIN: self_x = X,
+        self_scale = 1 + eps.
         """
         torch = _torch()
         F = X.shape[1] if X.dim() == 2 else 1
@@ -169,8 +173,10 @@ class Plan:
         v = _dev_ptr(vals, "float32", "vals") if vals.numel() else 0
         x = _dev_ptr(X, "float32", "X") if X.numel() else 0
         y = _dev_ptr(out, "float32", "out") if out.numel() else 0
+        opts = _spmm_opts(kernel, l2_hint, col_block_mb, aggregation, self_x, self_scale, bias, relu,
+                          shape=(self.n, F))
         _check(_lib.lib().agcn_spmm_ex(self.handle, v or None, x or None, int(F), y or None,
-                                       _stream_handle(stream), _spmm_opts(kernel, l2_hint, col_block_mb)))
+                                       _stream_handle(stream), opts))
         return out
 
     def close(self):
@@ -191,12 +197,25 @@ class Plan:
         self.close()
 
 
-def _spmm_opts(kernel: str = "auto", l2_hint: int | None = None, col_block_mb: int | None = None):
+def _spmm_opts(kernel: str = "auto", l2_hint: int | None = None, col_block_mb: int | None = None,
+               aggregation: str = "sum", self_x=None, self_scale: float = 0.0, bias=None,
+               relu: bool = False, shape=None):
     o = _lib.SpmmOpts()
     _lib.lib().agcn_default_spmm_opts(ctypes.byref(o))
     o.kernel = _lib.KERNELS[kernel]
     o.l2_hint = -1 if l2_hint is None else int(l2_hint)
     o.col_block_mb = -1 if col_block_mb is None else int(col_block_mb)
+    o.aggregation = {"sum": 0, "mean": 1}[aggregation]
+    o.relu = int(bool(relu))
+    o.self_scale = float(self_scale)
+    if self_x is not None:
+        if shape is not None and tuple(self_x.shape) != tuple(shape):
+            raise ValueError(f"self_x must be {tuple(shape)}, got {tuple(self_x.shape)}")
+        o.self = _dev_ptr(self_x, "float32", "self_x")
+    if bias is not None:
+        if shape is not None and tuple(bias.shape) != (shape[1],):
+            raise ValueError(f"bias must be [{shape[1]}]")
+        o.bias = _dev_ptr(bias, "float32", "bias")
     return ctypes.byref(o)
 
 

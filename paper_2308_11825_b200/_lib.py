@@ -27,7 +27,8 @@ KERNELS = {"auto": 0, "general": 1, "looped": 2, "wide": 3, "pipe": 4}
 
 class SpmmOpts(ctypes.Structure):
     _fields_ = [("kernel", c_i32), ("l2_hint", c_i32), ("col_block_mb", c_i32),
-                ("reserved", c_i32 * 5)]
+                ("aggregation", c_i32), ("self_scale", ctypes.c_float), ("relu", c_i32),
+                ("self", c_vp), ("bias", c_vp), ("reserved", c_i64 * 4)]
 
 
 class Stats(ctypes.Structure):

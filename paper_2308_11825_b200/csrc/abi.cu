@@ -127,6 +127,12 @@ agcn_status_t agcn_spmm_ex(agcn_plan_t plan, const float* vals, const float* X, 
                    "unknown kernel");
         AGCN_CHECK(o.l2_hint >= -1 && o.l2_hint <= 1, AGCN_ERR_INVALID_ARG, "l2_hint must be -1, 0 or 1");
         AGCN_CHECK(o.col_block_mb >= -1, AGCN_ERR_INVALID_ARG, "col_block_mb must be >= -1");
+        AGCN_CHECK(o.aggregation == AGCN_AGG_SUM || o.aggregation == AGCN_AGG_MEAN, AGCN_ERR_INVALID_ARG,
+                   "unknown aggregation");
+        AGCN_CHECK(o.self_scale == 0.f || o.self != nullptr, AGCN_ERR_INVALID_ARG,
+                   "self_scale != 0 needs the self matrix");
+        AGCN_CHECK(((reinterpret_cast<uintptr_t>(o.self) | reinterpret_cast<uintptr_t>(o.bias)) & 15u) == 0,
+                   AGCN_ERR_INVALID_ARG, "self and bias must be 16-byte aligned");
         if (plan->n == 0) return;
         AGCN_CHECK(Y != nullptr, AGCN_ERR_INVALID_ARG, "Y is NULL");
         AGCN_CHECK(plan->nnz == 0 || (vals != nullptr && X != nullptr), AGCN_ERR_INVALID_ARG,

@@ -86,6 +86,45 @@ private:
 // In-place (out == in) is allowed only if in has n+1 entries.  int32 values.
 void exclusive_scan_i32(const int32_t* in, int32_t* out, int64_t n, cudaStream_t s);
 
+// ------------------------------------------------------------------ SpMM epilogue
+// y_i = agg(i) * (mean ? 1/deg_i : 1) + self_scale * self[i] + bias; relu (agcn_spmm_opts_t)
+struct Epi {
+    const float* self;
+    const float* bias;
+    float self_scale;
+    int32_t mean, relu;
+    int32_t F;
+    __host__ __device__ bool active() const { return mean || self || bias || relu; }
+};
+
+__device__ __forceinline__ float4 epi4(float4 y, int32_t deg, int64_t orow, int32_t c, const Epi& e) {
+    if (e.mean) {
+        const float sc = deg > 0 ? 1.f / (float)deg : 0.f;
+        y.x *= sc; y.y *= sc; y.z *= sc; y.w *= sc;
+    }
+    if (e.self) {
+        const float4 v = __ldg(reinterpret_cast<const float4*>(e.self + orow * e.F + c));
+        y.x = fmaf(e.self_scale, v.x, y.x); y.y = fmaf(e.self_scale, v.y, y.y);
+        y.z = fmaf(e.self_scale, v.z, y.z); y.w = fmaf(e.self_scale, v.w, y.w);
+    }
+    if (e.bias) {
+        const float4 v = __ldg(reinterpret_cast<const float4*>(e.bias + c));
+        y.x += v.x; y.y += v.y; y.z += v.z; y.w += v.w;
+    }
+    if (e.relu) {
+        y.x = fmaxf(y.x, 0.f); y.y = fmaxf(y.y, 0.f); y.z = fmaxf(y.z, 0.f); y.w = fmaxf(y.w, 0.f);
+    }
+    return y;
+}
+
+__device__ __forceinline__ float epi1(float y, int32_t deg, int64_t orow, int32_t c, const Epi& e) {
+    if (e.mean) y *= deg > 0 ? 1.f / (float)deg : 0.f;
+    if (e.self) y = fmaf(e.self_scale, __ldg(e.self + orow * e.F + c), y);
+    if (e.bias) y += __ldg(e.bias + c);
+    if (e.relu) y = fmaxf(y, 0.f);
+    return y;
+}
+
 // ------------------------------------------------------------------ plan object
 struct PlanFlags {          // device-written, read back once (validation + sizes)
     int32_t bad_rowptr;     // rowptr decreases somewhere
@@ -158,7 +197,7 @@ void spmm_launch(agcn_plan_s* p, const float* vals, const float* X, int32_t F, f
 // spmm_wide.cu: 256-bit-per-lane kernel for F in {8,...,256}
 bool wide_supported(const agcn_plan_s* p, const float* X, const float* Y, int32_t F);
 void launch_wide(agcn_plan_s* p, const float* vals, const float* X, int32_t F, float* Y,
-                 bool l2_keep, bool blocked, cudaStream_t s);
+                 bool l2_keep, bool blocked, const Epi& epi, cudaStream_t s);
 // spmm_pipe.cu: cp.async shared-memory gather pipeline, F in {32,64,128,256}
 bool pipe_supported(const agcn_plan_s* p, const float* X, const float* Y, int32_t F);
 void launch_pipe(agcn_plan_s* p, const float* vals, const float* X, int32_t F, float* Y, cudaStream_t s);

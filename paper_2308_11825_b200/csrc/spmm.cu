@@ -273,6 +273,29 @@ __global__ void __launch_bounds__(kCtaThreads, 4) k_spmm_block(const __grid_cons
     }
 }
 
+__device__ __forceinline__ float4 epi_v(float4 y, int32_t deg, int64_t orow, int32_t c, const Epi& e) {
+    return epi4(y, deg, orow, 4 * c, e);  // c counts float4 vectors
+}
+__device__ __forceinline__ float epi_v(float y, int32_t deg, int64_t orow, int32_t c, const Epi& e) {
+    return epi1(y, deg, orow, c, e);
+}
+
+// Output epilogue as its own pass (kernels without the fused one), in place on Y, for rows
+// [k0, k1): sorted rows (perm != NULL, degree from the sorted rowptr) or original rows
+// (perm == NULL, degree from rp).  One thread per element.
+__global__ void k_epilogue(float* __restrict__ Y, int64_t k0, int64_t k1, int32_t F,
+                           const int32_t* __restrict__ perm, const int32_t* __restrict__ rp, const Epi epi) {
+    const int64_t total = (k1 - k0) * (int64_t)F;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t k = k0 + i / F;
+        const int32_t c = (int32_t)(i % F);
+        const int64_t orow = perm ? perm[k] : k;
+        float* y = Y + orow * F + c;
+        *y = epi1(*y, rp[k + 1] - rp[k], orow, c, epi);
+    }
+}
+
 // Level-3 merge: oversized row k gets the sum of its chunk partials.  One CTA per row:
 // thread (g, c) sums chunks c0+g, c0+g+NG, ... of vector column c in order, then thread
 // (0, c) adds the NG group sums in group order -> fixed summation order (deterministic).
@@ -280,7 +303,8 @@ constexpr int kReduceThreads = 128;
 template <bool V4>
 __global__ void __launch_bounds__(kReduceThreads) k_ov_reduce(
     const float* __restrict__ ovp_f, const int32_t* __restrict__ chunk_start,
-    const int32_t* __restrict__ perm, int64_t ov_start, float* __restrict__ Y_f, int32_t FV) {
+    const int32_t* __restrict__ perm, int64_t ov_start, float* __restrict__ Y_f, int32_t FV,
+    const int32_t* __restrict__ srp, const Epi epi) {
     using VT = typename VecT<V4>::T;
     __shared__ VT part[kReduceThreads];
     const VT* ovp = reinterpret_cast<const VT*>(ovp_f);
@@ -312,6 +336,7 @@ __global__ void __launch_bounds__(kReduceThreads) k_ov_reduce(
         if (g == 0 && c < FV) {
             VT sum = part[cl];
             for (int gg = 1; gg < NG; ++gg) vadd(sum, part[gg * FVc + cl]);
+            if (epi.active()) sum = epi_v(sum, srp[ov_start + k + 1] - srp[ov_start + k], orow, c, epi);
             sty(Y + orow * FV + c, sum);
         }
         __syncthreads();
@@ -416,6 +441,15 @@ Shape pick_shape(int32_t FV) {
                 break;
             }
     return best;
+}
+
+void launch_epilogue(float* Y, int64_t k0, int64_t k1, int32_t F, const int32_t* perm, const int32_t* rp,
+                     const Epi& epi, cudaStream_t s) {
+    if (k1 <= k0) return;
+    const int64_t total = (k1 - k0) * (int64_t)F;
+    const unsigned grid = (unsigned)std::min<int64_t>((total + 255) / 256, 148 * 16);
+    k_epilogue<<<grid, 256, 0, s>>>(Y, k0, k1, F, perm, rp, epi);
+    post_launch();
 }
 
 int g_num_sms = 0;
@@ -532,18 +566,22 @@ void spmm_launch(agcn_plan_s* p, const float* vals, const float* X, int32_t F, f
     } rec{p, s, foreign};
     // LOOPED (ablation 2, Fig. 4(a) / Table II): no combined warp -- one warp of 32 scalar lanes
     // walks the columns of a row in strides of 32
+    const Epi epi{o.self_scale != 0.f ? o.self : nullptr, o.bias, o.self_scale,
+                  o.aggregation == AGCN_AGG_MEAN, o.relu != 0, F};
     const bool looped = o.kernel == AGCN_KERNEL_LOOPED;
     const bool v4 = !looped && (F % 4 == 0) && aligned16(X) && aligned16(Y);
     const int32_t FV = v4 ? F / 4 : F;
     const Shape sh = looped ? Shape{32, 1} : pick_shape(FV);
     if (p->partition == AGCN_PARTITION_WARP) {
         AGCN_CUDA(cudaMemsetAsync(Y, 0, sizeof(float) * (size_t)p->n * F, s));
-        if (p->ntasks == 0) return;
-        WarpArgs a{p->tasks, p->ntasks, p->rowptr_copy, p->cols, vals + p->rp_base, X, Y, FV};
-        if (v4)
-            AGCN_DISPATCH_LT(sh, warp_v4, a, s);
-        else
-            AGCN_DISPATCH_LT(sh, warp_v1, a, s);
+        if (p->ntasks > 0) {
+            WarpArgs a{p->tasks, p->ntasks, p->rowptr_copy, p->cols, vals + p->rp_base, X, Y, FV};
+            if (v4)
+                AGCN_DISPATCH_LT(sh, warp_v4, a, s);
+            else
+                AGCN_DISPATCH_LT(sh, warp_v1, a, s);
+        }
+        if (epi.active()) launch_epilogue(Y, 0, p->n, F, nullptr, p->rowptr_copy, epi, s);
         return;
     }
     // kernel choice (agcn_spmm_opts_t): WIDE when applicable, else GENERAL
@@ -600,19 +638,23 @@ void spmm_launch(agcn_plan_s* p, const float* vals, const float* X, int32_t F, f
     if (kernel == AGCN_KERNEL_PIPE)
         launch_pipe(p, vals, X, F, Y, s);
     else if (kernel == AGCN_KERNEL_WIDE)
-        launch_wide(p, vals, X, F, Y, keep, blocked, s);
+        launch_wide(p, vals, X, F, Y, keep, blocked, epi, s);  // epilogue fused
     else if (v4)
         AGCN_DISPATCH_LT(sh, block_v4, a, s, smem);
     else
         AGCN_DISPATCH_LT(sh, block_v1, a, s, smem);
+    if (kernel != AGCN_KERNEL_WIDE && epi.active())  // rows of degree <= deg_bound
+        launch_epilogue(Y, 0, p->ov_start, F, p->perm, p->sorted_rowptr, epi, s);
     if (p->n_ov > 0) {  // level 3: oversized rows = fixed-order sums of their partial rows
         const unsigned grid = (unsigned)p->n_ov;
         const float* part = blocked ? p->sched.partial : p->ov_partial;
         const int32_t* slots = blocked ? p->sched.slot_base : p->ov_chunk_start;
         if (v4)
-            k_ov_reduce<true><<<grid, kReduceThreads, 0, s>>>(part, slots, p->perm, p->ov_start, Y, FV);
+            k_ov_reduce<true><<<grid, kReduceThreads, 0, s>>>(part, slots, p->perm, p->ov_start, Y, FV,
+                                                              p->sorted_rowptr, epi);
         else
-            k_ov_reduce<false><<<grid, kReduceThreads, 0, s>>>(part, slots, p->perm, p->ov_start, Y, FV);
+            k_ov_reduce<false><<<grid, kReduceThreads, 0, s>>>(part, slots, p->perm, p->ov_start, Y, FV,
+                                                               p->sorted_rowptr, epi);
         post_launch();
     }
 }

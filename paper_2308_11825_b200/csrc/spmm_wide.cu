@@ -93,11 +93,23 @@ struct WideArgs {
     const int32_t* n_pieces;  // device: number of pieces
     float* piece_partial; // [pieces][F] partial rows (slot-indexed)
     int64_t piece_cap;    // upper bound of the piece count (grid sizing)
+    Epi epi;              // output epilogue (EPI)
 };
+
+// a finished output row slice of 8 floats at column c of original row orow (degree deg)
+template <bool EPI>
+__device__ __forceinline__ void store_row(float* Y, int64_t orow, int32_t c, int32_t F, int32_t deg, f8 v,
+                                          const Epi& e) {
+    if (EPI) {
+        v.a = epi4(v.a, deg, orow, c, e);
+        v.b = epi4(v.b, deg, orow, c + 4, e);
+    }
+    st8(Y + orow * F + c, v);
+}
 
 // L lanes per X row (F = 8 L), U X rows in flight per lane, MINB resident CTAs per SM
 // (register budget), KEEP: X-row loads carry an L2 evict_last hint.
-template <int L, int U, int MINB, bool KEEP, bool PIECES>
+template <int L, int U, int MINB, bool KEEP, bool PIECES, bool EPI>
 __global__ void __launch_bounds__(kThreads, MINB) k_spmm_wide(const __grid_constant__ WideArgs a) {
     constexpr int G = 32 / L;
     constexpr int F = 8 * L;
@@ -116,7 +128,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_wide(const __grid_const
 #pragma unroll 4
             for (int i = 0; i < 32; i += G) {
                 const int32_t o = __shfl_sync(0xffffffffu, pr, i + s);
-                if (o >= 0) st8(a.Y + (int64_t)o * F + li * 8, z);
+                if (o >= 0) store_row<EPI>(a.Y, o, li * 8, F, 0, z, a.epi);
             }
         }
     }
@@ -194,10 +206,11 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_wide(const __grid_const
                             const int32_t r = s + rowi * G;
                             const int32_t o = __shfl_sync(0xffffffffu, dst_l, min(r, 31));
                             if (r < R) {
-                                float* dst = !ov ? a.Y + (int64_t)o * F
-                                 : piece ? a.piece_partial + (int64_t)slot * F
-                                         : a.ovp + (int64_t)(b - a.first_ov) * F;
-                                st8(dst + li * 8, acc);
+                                if (!ov)
+                                    store_row<EPI>(a.Y, o, li * 8, F, d, acc, a.epi);
+                                else
+                                    st8((piece ? a.piece_partial + (int64_t)slot * F
+                                               : a.ovp + (int64_t)(b - a.first_ov) * F) + li * 8, acc);
                             }
                             acc.a = acc.b = make_float4(0.f, 0.f, 0.f, 0.f);
                             left = d;
@@ -269,18 +282,19 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_wide(const __grid_const
             }
             const int32_t rd = __shfl_sync(0xffffffffu, dst_l, r & 31);
             if (k == 0 && r < R) {
-                float* dst = !ov ? a.Y + (int64_t)rd * F
-                                 : piece ? a.piece_partial + (int64_t)slot * F
-                                         : a.ovp + (int64_t)(b - a.first_ov) * F;
-                st8(dst + li * 8, acc);
+                if (!ov)
+                    store_row<EPI>(a.Y, rd, li * 8, F, d, acc, a.epi);
+                else
+                    st8((piece ? a.piece_partial + (int64_t)slot * F
+                               : a.ovp + (int64_t)(b - a.first_ov) * F) + li * 8, acc);
             }
         }
     }
 }
 
-template <int L, int U, int MINB, bool KEEP, bool PIECES>
+template <int L, int U, int MINB, bool KEEP, bool PIECES, bool EPI>
 void launch_t(const WideArgs& a, cudaStream_t s) {
-    auto kern = k_spmm_wide<L, U, MINB, KEEP, PIECES>;
+    auto kern = k_spmm_wide<L, U, MINB, KEEP, PIECES, EPI>;
     static int occ = -1;
     if (occ < 0) {
         AGCN_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kThreads, 0));
@@ -299,12 +313,20 @@ int env_int(const char* name, int dflt) {  // experiment switch
     return v ? atoi(v) : dflt;
 }
 
+template <int L, int U, int MINB, bool EPI>
+void launch_e(const WideArgs& a, bool keep, cudaStream_t s) {
+    if (a.pieces)
+        keep ? launch_t<L, U, MINB, true, true, EPI>(a, s) : launch_t<L, U, MINB, false, true, EPI>(a, s);
+    else
+        keep ? launch_t<L, U, MINB, true, false, EPI>(a, s) : launch_t<L, U, MINB, false, false, EPI>(a, s);
+}
+
 template <int L, int U, int MINB>
 void launch_k(const WideArgs& a, bool keep, cudaStream_t s) {
-    if (a.pieces)
-        keep ? launch_t<L, U, MINB, true, true>(a, s) : launch_t<L, U, MINB, false, true>(a, s);
+    if (a.epi.active())
+        launch_e<L, U, MINB, true>(a, keep, s);
     else
-        keep ? launch_t<L, U, MINB, true, false>(a, s) : launch_t<L, U, MINB, false, false>(a, s);
+        launch_e<L, U, MINB, false>(a, keep, s);
 }
 
 template <int L>
@@ -328,12 +350,12 @@ bool wide_supported(const agcn_plan_s* p, const float* X, const float* Y, int32_
 }
 
 void launch_wide(agcn_plan_s* p, const float* vals, const float* X, int32_t F, float* Y,
-                 bool l2_keep, bool blocked, cudaStream_t s) {
+                 bool l2_keep, bool blocked, const Epi& epi, cudaStream_t s) {
     const ColSched& cs = p->sched;
     WideArgs a{p->desc, blocked ? p->nb_small : p->nblocks, p->nb_small, p->n_zero, p->cols,
                p->sorted_rowptr, p->row_src_off, p->perm, vals + p->rp_base, X, Y, p->ov_partial,
                p->deg_bound, blocked ? cs.seg : nullptr, blocked ? cs.slot_base + p->n_ov : nullptr,
-               blocked ? cs.partial : nullptr, blocked ? cs.cap : 0};
+               blocked ? cs.partial : nullptr, blocked ? cs.cap : 0, epi};
     AGCN_CHECK(a.n_desc + a.piece_cap < (1ll << 31), AGCN_ERR_OVERFLOW, "too many descriptors");
     switch (F) {
         case 8: launch<1>(a, l2_keep, s); break;

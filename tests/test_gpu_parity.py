@@ -369,3 +369,53 @@ def test_launch_counter_moves():
     c0 = A.launch_count()
     p.spmm(cu(w.vals), cu(w.X()))
     assert A.launch_count() > c0
+
+
+# ---------------------------------------------------------------- aggregation variants / epilogue
+EPI_CASES = [
+    dict(aggregation="mean"),
+    dict(self_scale=1.5, self_x=True),                       # GIN, eps = 0.5
+    dict(bias=True, relu=True),
+    dict(aggregation="mean", self_scale=-0.75, self_x=True, bias=True, relu=True),
+]
+
+
+@pytest.mark.parametrize("kernel,F", [("auto", 64), ("wide", 128), ("general", 100), ("general", 64),
+                                      ("looped", 16), ("pipe", 64)])
+@pytest.mark.parametrize("case", range(len(EPI_CASES)))
+def test_spmm_epilogue(kernel, F, case):
+    """GCN / GraphSAGE-mean / GIN aggregation with bias and ReLU vs the oracle, through
+    the fused epilogue (WIDE, oversized-row reduction) and the separate pass (other kernels)."""
+    ep = dict(EPI_CASES[case])
+    rowptr, colidx = _rows_csr(np.array([0, 1, 2, 3, 5, 31, 33, 64, 97, 130, 200, 383, 384, 385,
+                                         768, 769, 2000, 0, 7]), 19, 11)
+    n = rowptr.size - 1
+    rng = np.random.default_rng(case * 10 + F)
+    vals = rng.uniform(-1, 1, colidx.size).astype(np.float32)
+    X = rng.uniform(-1, 1, (n, F)).astype(np.float32)
+    bias = rng.uniform(-1, 1, F).astype(np.float32)
+    p = make_plan(rowptr, colidx)
+    kw = {"aggregation": ep.get("aggregation", "sum"), "self_scale": ep.get("self_scale", 0.0),
+          "relu": ep.get("relu", False)}
+    if ep.get("self_x"):
+        kw["self_x"] = cu(X)
+    if ep.get("bias"):
+        kw["bias"] = cu(bias)
+    Y = p.spmm(cu(vals), cu(X), kernel=kernel, **kw).cpu().numpy()
+    y, t = oracle.spmm_epilogue(rowptr, colidx, vals, X, aggregation=kw["aggregation"],
+                                self_x=X if ep.get("self_x") else None,
+                                self_scale=kw["self_scale"], bias=bias if ep.get("bias") else None,
+                                relu=kw["relu"])
+    r = oracle.check_epilogue(Y, y, t)
+    assert r["nfail"] == 0, r
+
+
+def test_spmm_epilogue_warp_partition_and_sharded_rows():
+    w = gen.make_config("c2", vals_kind="uniform")
+    X = w.X(64)
+    b = np.linspace(-1, 1, 64).astype(np.float32)
+    y, t = oracle.spmm_epilogue(w.rowptr, w.colidx, w.vals, X, aggregation="mean", bias=b, relu=True)
+    for part in ("warp", "block"):
+        p = make_plan(w.rowptr, w.colidx, partition=part)
+        Y = p.spmm(cu(w.vals), cu(X), aggregation="mean", bias=cu(b), relu=True).cpu().numpy()
+        assert oracle.check_epilogue(Y, y, t)["nfail"] == 0, part

@@ -345,3 +345,37 @@ def test_combined_warp_values():
         lanes = np.arange(rd)
         active = lanes < F                                    # lanes >= F truncated
         assert active.sum() == F and rd % 32 == 0 and rd - F < 32
+
+
+# ---------------------------------------------------------------- aggregation variants
+def test_epilogue_mean_is_neighbour_mean():
+    """GraphSAGE-mean with unit values = the arithmetic mean of the neighbours' rows (dense)."""
+    rng = np.random.default_rng(7)
+    n, nc, F = 40, 30, 5
+    rowptr, colidx = gen.random_csr(n, nc, 7, max_deg=9, dup=False)
+    vals = np.ones(colidx.size, np.float32)
+    X = rng.uniform(-1, 1, (nc, F)).astype(np.float32)
+    y, _ = oracle.spmm_epilogue(rowptr, colidx, vals, X, aggregation="mean")
+    for i in range(n):
+        nb = colidx[rowptr[i]:rowptr[i + 1]]
+        want = X[nb].astype(np.float64).mean(0) if nb.size else np.zeros(F)
+        assert np.allclose(y[i], want, rtol=1e-12, atol=1e-12)
+
+
+def test_epilogue_gin_self_term_bias_relu():
+    """GIN on an edgeless graph reduces to (1 + eps) * x; bias broadcasts; ReLU clips."""
+    rng = np.random.default_rng(8)
+    n, F = 12, 6
+    rowptr = np.zeros(n + 1, np.int32)
+    colidx = np.zeros(0, np.int32)
+    X = rng.uniform(-1, 1, (n, F)).astype(np.float32)
+    b = rng.uniform(-1, 1, F).astype(np.float32)
+    y, t = oracle.spmm_epilogue(rowptr, colidx, np.zeros(0, np.float32), X, self_x=X,
+                                self_scale=1.25, bias=b)
+    assert np.allclose(y, 1.25 * X.astype(np.float64) + b, rtol=0, atol=1e-12)
+    assert np.allclose(t, np.abs(1.25 * X.astype(np.float64)) + np.abs(b), rtol=0, atol=1e-12)
+    yr, _ = oracle.spmm_epilogue(rowptr, colidx, np.zeros(0, np.float32), X, self_x=X,
+                                 self_scale=1.25, bias=b, relu=True)
+    assert np.array_equal(yr, np.maximum(y, 0.0))
+    r = oracle.check_epilogue((y + 1e-3).astype(np.float32), y, t)   # planted error fails
+    assert r["nfail"] > 0
