@@ -214,6 +214,27 @@ agcn_status_t agcn_propagate_host(const int32_t* rowptr_host, const int32_t* col
                                   const float* X_host, int32_t F, int32_t layers, float* Y_host,
                                   const agcn_opts_t* opts);
 
+/*
+ * CSR of A^T on the device, for the backward pass of a GCN layer (dX = A^T . dY).  A stable
+ * counting sort of the nonzeros by column (the degree sort's machinery): row j of A^T
+ * lists the rows i with a_ij != 0 in increasing i.
+ *   rowptr: DEVICE int32[n+1] (rowptr[0] may be nonzero: colidx is indexed by rowptr values);
+ *   colidx: DEVICE int32, 0 <= colidx < n_cols (not validated here: build a plan first).
+ *   rowptr_t: DEVICE int32[n_cols+1] out (starts at 0); colidx_t: DEVICE int32[nnz] out;
+ *   src: DEVICE int32[nnz] out -- entry k of A^T is entry src[k] of A (rowptr-relative),
+ *        so vals_t = vals[src] (agcn_gather_vals).
+ * Outputs are caller-owned and must not overlap the inputs.  Asynchronous on `stream`
+ * (stream-ordered scratch, no host synchronisation).
+ */
+agcn_status_t agcn_transpose(const int32_t* rowptr, const int32_t* colidx, int64_t n, int64_t n_cols,
+                             int64_t nnz, int32_t* rowptr_t, int32_t* colidx_t, int32_t* src,
+                             agcn_stream_t stream);
+
+/* out[k] = vals[src[k]] for k < nnz (DEVICE arrays; vals indexed rowptr-relative, like src).
+   Asynchronous on `stream`. */
+agcn_status_t agcn_gather_vals(const float* vals, const int32_t* src, int64_t nnz, float* out,
+                               agcn_stream_t stream);
+
 agcn_status_t agcn_last_status(void);
 const char* agcn_last_error(void);
 

@@ -156,6 +156,22 @@ def check_epilogue(Y, y_ref, tol_scale, rel=REL_TOL, abs_tol=ABS_TOL):
     return {"max_ratio": float(ratio.max()) if ratio.size else 0.0, "nfail": int((~(ratio <= 1.0)).sum())}
 
 
+def transpose(rowptr, colidx, n_cols: int):
+    """CSR of A^T (backward pass, dX = A^T dY): (rowptr_t, colidx_t, src) with
+    row j of A^T = the rows i holding column j in increasing i (a stable sort of the entries
+    by column: np.argsort(kind="stable") is the library step); entry k of A^T is entry
+    src[k] of A (rowptr-relative)."""
+    rowptr = np.asarray(rowptr, dtype=np.int64)
+    base = int(rowptr[0])
+    nnz = int(rowptr[-1] - base)
+    cols = np.asarray(colidx, dtype=np.int64)[base:base + nnz]
+    src = np.argsort(cols, kind="stable").astype(np.int32)
+    rows = np.repeat(np.arange(rowptr.size - 1, dtype=np.int32), np.diff(rowptr))
+    rowptr_t = np.zeros(n_cols + 1, dtype=np.int32)
+    rowptr_t[1:] = np.cumsum(np.bincount(cols, minlength=n_cols))
+    return rowptr_t, rows[src], src
+
+
 # ---------------------------------------------------------------- preprocessing (P:295)
 def degree_sort(rowptr):
     """Stable ascending counting sort of rows by degree -> perm (sorted_to_orig)."""

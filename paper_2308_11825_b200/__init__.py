@@ -17,7 +17,7 @@ import numpy as np
 from . import _lib
 from ._lib import FIELDS, STATUS
 
-__all__ = ["Plan", "AgcnError", "agcn_plan", "agcn_spmm", "agcn_spmm_ex", "shard_bounds", "propagate_host",
+__all__ = ["Plan", "AgcnError", "agcn_plan", "agcn_spmm", "agcn_spmm_ex", "transpose", "gather_vals", "shard_bounds", "propagate_host",
            "launch_count", "version", "library_path"]
 
 
@@ -239,6 +239,39 @@ def agcn_spmm_ex(plan: Plan, vals, X, F: int, Y, stream=None, kernel: str = "aut
     y = _dev_ptr(Y, "float32", "Y") if Y.numel() else 0
     _check(_lib.lib().agcn_spmm_ex(plan.handle, v or None, x or None, int(F), y or None,
                                    _stream_handle(stream), _spmm_opts(kernel, l2_hint, col_block_mb)))
+
+
+def transpose(rowptr, colidx, n_cols: int, stream=None):
+    """agcn_transpose: (rowptr_t, colidx_t, src) of A^T on the device (dX = A^T . dY).
+
+    Row j of A^T lists the rows i with a_ij != 0 in increasing i; entry k of A^T is entry
+    src[k] of A, so vals_t = gather_vals(vals, src).
+    """
+    torch = _torch()
+    n = rowptr.numel() - 1
+    nnz = int(rowptr[-1].item() - rowptr[0].item()) if n >= 0 else 0
+    dev = rowptr.device
+    rowptr_t = torch.empty(n_cols + 1, dtype=torch.int32, device=dev)
+    colidx_t = torch.empty(nnz, dtype=torch.int32, device=dev)
+    src = torch.empty(nnz, dtype=torch.int32, device=dev)
+    _check(_lib.lib().agcn_transpose(_dev_ptr(rowptr, "int32", "rowptr"),
+                                     _dev_ptr(colidx, "int32", "colidx") if colidx.numel() else None,
+                                     n, int(n_cols), nnz, rowptr_t.data_ptr(),
+                                     colidx_t.data_ptr() if nnz else None, src.data_ptr() if nnz else None,
+                                     _stream_handle(stream)))
+    return rowptr_t, colidx_t, src
+
+
+def gather_vals(vals, src, out=None, stream=None):
+    """agcn_gather_vals: out[k] = vals[src[k]] (values of A^T from those of A)."""
+    torch = _torch()
+    if out is None:
+        out = torch.empty(src.numel(), dtype=torch.float32, device=src.device)
+    if src.numel():
+        _check(_lib.lib().agcn_gather_vals(_dev_ptr(vals, "float32", "vals"), _dev_ptr(src, "int32", "src"),
+                                           src.numel(), _dev_ptr(out, "float32", "out"),
+                                           _stream_handle(stream)))
+    return out
 
 
 def shard_bounds(rowptr, nranks: int, stream=None) -> np.ndarray:

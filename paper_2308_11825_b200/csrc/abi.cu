@@ -285,6 +285,17 @@ agcn_status_t agcn_propagate_host(const int32_t* rowptr_h, const int32_t* colidx
     });
 }
 
+agcn_status_t agcn_transpose(const int32_t* rowptr, const int32_t* colidx, int64_t n, int64_t n_cols,
+                             int64_t nnz, int32_t* rowptr_t, int32_t* colidx_t, int32_t* src,
+                             agcn_stream_t stream) {
+    return guarded([&] { transpose_csr(rowptr, colidx, n, n_cols, nnz, rowptr_t, colidx_t, src, (cudaStream_t)stream); });
+}
+
+agcn_status_t agcn_gather_vals(const float* vals, const int32_t* src, int64_t nnz, float* out,
+                               agcn_stream_t stream) {
+    return guarded([&] { gather_vals(vals, src, nnz, out, (cudaStream_t)stream); });
+}
+
 agcn_status_t agcn_last_status(void) { return agcn::last_status(); }
 const char* agcn_last_error(void) { return agcn::last_message(); }
 uint64_t agcn_launch_count(void) { return agcn::g_launches.load(); }

@@ -201,6 +201,13 @@ void launch_wide(agcn_plan_s* p, const float* vals, const float* X, int32_t F, f
 // spmm_pipe.cu: cp.async shared-memory gather pipeline, F in {32,64,128,256}
 bool pipe_supported(const agcn_plan_s* p, const float* X, const float* Y, int32_t F);
 void launch_pipe(agcn_plan_s* p, const float* vals, const float* X, int32_t F, float* Y, cudaStream_t s);
+// plan.cu: stable LSD radix sort of (key, val) pairs (8-bit digits); result in ka/va
+void radix_sort_pairs(int32_t*& ka, int32_t*& va, int32_t*& kb, int32_t*& vb, int64_t m, int64_t max_key,
+                      cudaStream_t s);
+// transpose.cu
+void transpose_csr(const int32_t* rowptr, const int32_t* colidx, int64_t n, int64_t n_cols, int64_t nnz,
+                   int32_t* rowptr_t, int32_t* colidx_t, int32_t* src, cudaStream_t s);
+void gather_vals(const float* vals, const int32_t* src, int64_t nnz, float* out, cudaStream_t s);
 // sched.cu
 int col_sched_shift(const agcn_plan_s* p, int32_t F, double target_bytes);
 void build_col_sched(agcn_plan_s* p, int shift, int32_t F, cudaStream_t s);

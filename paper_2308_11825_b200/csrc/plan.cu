@@ -428,6 +428,35 @@ struct Overlap {
     }
 };
 
+}  // namespace
+
+// Stable LSD radix sort of (key, val) int32 pairs by key (0 <= key <= max_key), 8-bit digits,
+// through the stable bucket scatter above.  ka/va in, kb/vb scratch; on return ka/va point at
+// the sorted pairs (either buffer pair).
+void radix_sort_pairs(int32_t*& ka, int32_t*& va, int32_t*& kb, int32_t*& vb, int64_t m, int64_t max_key,
+                      cudaStream_t s) {
+    if (m <= 1) return;
+    int passes = 0;
+    for (int64_t v = max_key; v > 0; v >>= 8) ++passes;
+    const int64_t mt = (m + kTile - 1) / kTile;
+    AGCN_CHECK(256 * mt < (1ll << 31), AGCN_ERR_OVERFLOW, "radix sort too large");
+    Scratch tmp(s);
+    int32_t* rt = tmp.alloc<int32_t>(256 * mt + 1);
+    for (int pass = 0; pass < passes; ++pass) {
+        RadixSrc src{ka, va, kb, vb, 8 * pass};
+        k_bucket_hist<RadixSrc><<<(unsigned)mt, kThreads, 256 * sizeof(int32_t), s>>>(src, m, 256, mt, rt);
+        post_launch();
+        exclusive_scan_i32(rt, rt, 256 * mt, s);
+        k_bucket_scatter<RadixSrc><<<(unsigned)mt, kThreads, kWarps * 256 * sizeof(int32_t), s>>>(
+            src, m, 256, mt, rt);
+        post_launch();
+        std::swap(ka, kb);
+        std::swap(va, vb);
+    }
+}
+
+namespace {
+
 // ---------------------------------------------------------------- block-partition plan
 void build_block_plan(agcn_plan_s* p, const int32_t* rowptr, const int32_t* colidx,
                       const agcn_opts_t& o, cudaStream_t s) {
@@ -517,27 +546,13 @@ void build_block_plan(agcn_plan_s* p, const int32_t* rowptr, const int32_t* coli
     // radix sort of that bucket by degree (8-bit digits) completes the ascending stable order.
     const int64_t m = p->n_ov;
     if (m > 1) {
-        int passes = 0;
-        for (int64_t v = p->max_deg; v > 0; v >>= 8) ++passes;
-        const int64_t mt = (m + kTile - 1) / kTile;
         int32_t* ka = tmp.alloc<int32_t>(m);
         int32_t* va = tmp.alloc<int32_t>(m);
         int32_t* kb = tmp.alloc<int32_t>(m);
         int32_t* vb = tmp.alloc<int32_t>(m);
-        int32_t* rt = tmp.alloc<int32_t>(256 * mt + 1);
         k_ov_init<<<blocks_for(m, 256), 256, 0, s>>>(p->perm + p->ov_start, rowptr, m, ka, va);
         post_launch();
-        for (int pass = 0; pass < passes; ++pass) {
-            RadixSrc src{ka, va, kb, vb, 8 * pass};
-            k_bucket_hist<RadixSrc><<<(unsigned)mt, kThreads, 256 * sizeof(int32_t), s>>>(src, m, 256, mt, rt);
-            post_launch();
-            exclusive_scan_i32(rt, rt, 256 * mt, s);
-            k_bucket_scatter<RadixSrc><<<(unsigned)mt, kThreads, kWarps * 256 * sizeof(int32_t), s>>>(
-                src, m, 256, mt, rt);
-            post_launch();
-            std::swap(ka, kb);
-            std::swap(va, vb);
-        }
+        radix_sort_pairs(ka, va, kb, vb, m, p->max_deg, s);
         AGCN_CUDA(cudaMemcpyAsync(p->perm + p->ov_start, va, sizeof(int32_t) * m,
                                   cudaMemcpyDeviceToDevice, s));
     }

@@ -419,3 +419,34 @@ def test_spmm_epilogue_warp_partition_and_sharded_rows():
         p = make_plan(w.rowptr, w.colidx, partition=part)
         Y = p.spmm(cu(w.vals), cu(X), aggregation="mean", bias=cu(b), relu=True).cpu().numpy()
         assert oracle.check_epilogue(Y, y, t)["nfail"] == 0, part
+
+
+# ---------------------------------------------------------------- transpose / backward (8(f4))
+@pytest.mark.parametrize("name", ["c1", "c3"])
+def test_transpose_bit_exact_and_backward(name):
+    w = gen.make_config(name, vals_kind="uniform")
+    rp, ci = cu(w.rowptr), cu(w.colidx)
+    rt, ct, src = A.transpose(rp, ci, w.n)
+    ort, oct_, osrc = oracle.transpose(w.rowptr, w.colidx, w.n)
+    assert np.array_equal(rt.cpu().numpy(), ort)
+    assert np.array_equal(ct.cpu().numpy(), oct_)
+    assert np.array_equal(src.cpu().numpy(), osrc)
+    vt = A.gather_vals(cu(w.vals), src)
+    assert np.array_equal(vt.cpu().numpy(), w.vals[osrc])
+    dY = w.X(64)                                           # backward: dX = A^T dY
+    pt = A.Plan(rt, ct, n_cols=w.n)
+    dX = pt.spmm(vt, cu(dY)).cpu().numpy()
+    check_spmm(pt, ort, oct_, w.vals[osrc], dY, dX)
+
+
+def test_transpose_rectangular_shard_and_empty():
+    rowptr, colidx = _rows_csr(np.array([0, 3, 0, 7, 1, 0]), 9, 4)
+    base = 5                                               # a row shard: rowptr[0] != 0
+    rp = np.concatenate([[0], rowptr + base]).astype(np.int32)[1:]
+    ci = np.concatenate([np.zeros(base, np.int32), colidx]).astype(np.int32)
+    rt, ct, src = A.transpose(cu(rp), cu(ci), 9)
+    ort, oct_, osrc = oracle.transpose(rp, ci, 9)
+    assert np.array_equal(rt.cpu().numpy(), ort) and np.array_equal(ct.cpu().numpy(), oct_)
+    assert np.array_equal(src.cpu().numpy(), osrc)
+    rt, ct, src = A.transpose(cu(np.zeros(4, np.int32)), cu(np.zeros(0, np.int32)), 3)
+    assert np.array_equal(rt.cpu().numpy(), np.zeros(4, np.int32)) and ct.numel() == 0

@@ -379,3 +379,23 @@ def test_epilogue_gin_self_term_bias_relu():
     assert np.array_equal(yr, np.maximum(y, 0.0))
     r = oracle.check_epilogue((y + 1e-3).astype(np.float32), y, t)   # planted error fails
     assert r["nfail"] > 0
+
+
+# ---------------------------------------------------------------- transpose (backward, 8(f4))
+@pytest.mark.parametrize("seed", range(6))
+def test_transpose_dense_and_involution(seed):
+    rng = np.random.default_rng(seed)
+    n, nc = int(rng.integers(1, 60)), int(rng.integers(1, 60))
+    rowptr, colidx = gen.random_csr(n, nc, seed, max_deg=20, dup=bool(seed % 2))
+    vals = rng.uniform(-1, 1, colidx.size)
+    rt, ct, src = oracle.transpose(rowptr, colidx, nc)
+    D = np.zeros((n, nc))
+    np.add.at(D, (np.repeat(np.arange(n), np.diff(rowptr)), colidx), vals)
+    Dt = np.zeros((nc, n))
+    np.add.at(Dt, (np.repeat(np.arange(nc), np.diff(rt)), ct), vals[src])
+    assert np.array_equal(Dt, D.T)                         # dense brute force
+    for j in range(nc):                                    # rows of A^T ascending (stable)
+        assert np.all(np.diff(ct[rt[j]:rt[j + 1]]) >= 0)
+    r2, c2, s2 = oracle.transpose(rt, ct, n)               # (A^T)^T = A, entry for entry
+    assert np.array_equal(r2, rowptr.astype(np.int32)) and np.array_equal(c2, colidx)
+    assert np.array_equal(src[s2], np.arange(colidx.size))
