@@ -41,6 +41,8 @@ def parse():
     ap.add_argument("--layers", type=int, default=None)
     ap.add_argument("--partition", choices=["block", "warp"], default="block")
     ap.add_argument("--kernel", choices=["auto", "general", "looped", "wide", "pipe"], default="auto")
+    ap.add_argument("--mbw", type=int, default=12, help="Alg. 1 max_block_warps (P:318; paper: 12)")
+    ap.add_argument("--mwn", type=int, default=32, help="Alg. 1 max_warp_nzs (P:318; SPEC default 32)")
     ap.add_argument("--l2-hint", type=int, default=None, help="None: auto; 0: never; 1: always")
     ap.add_argument("--col-block-mb", type=int, default=None,
                     help="None: auto; 0: off (paper chunks); MiB of X per column block")
@@ -227,7 +229,7 @@ def main():
     X0 = torch.zeros((lay.padded_rows, F), dtype=torch.float32, device=dev)
     lay.pad(torch.from_numpy(X_host).to(dev), X0)
     bufs = [torch.empty_like(X0) for _ in range(min(layers, 2))]
-    plan_kw = dict(n_cols=n, max_block_warps=12, max_warp_nzs=32, partition=args.partition)
+    plan_kw = dict(n_cols=n, max_block_warps=args.mbw, max_warp_nzs=args.mwn, partition=args.partition)
     if P > 1:
         plan_kw.update(col_bounds=bounds, col_slot_rows=S)
 
@@ -340,7 +342,7 @@ def main():
             "config": {"workload": w.meta["desc"], "name": w.name, "n": n, "nnz": nnz, "F": F,
                        "layers": layers, "partition": args.partition, "kernel": args.kernel,
                        "aggregation": args.aggregation, "gin_eps": args.gin_eps, "bias_relu": args.bias_relu, "parallelism": f"row-shard{P}",
-                       "max_block_warps": 12, "max_warp_nzs": 32,
+                       "max_block_warps": args.mbw, "max_warp_nzs": args.mwn,
                        "l2": "inputs larger than L2 (CSR + X > 126 MB)" if
                              (8 * nnz + 4 * n * F) > 126e6 else "inputs fit in L2 (warm)",
                        "step": "agcn_plan + layers x agcn_spmm (+ all-gather if N>1)"},
