@@ -156,6 +156,37 @@ def check_epilogue(Y, y_ref, tol_scale, rel=REL_TOL, abs_tol=ABS_TOL):
     return {"max_ratio": float(ratio.max()) if ratio.size else 0.0, "nfail": int((~(ratio <= 1.0)).sum())}
 
 
+def gcn_layer(rowptr, colidx, vals, X, W, bias=None, relu=True):
+    """One GCN layer in fp64 (X' = sigma(A' Y), Y = X W; sigma = ReLU, plus a bias):
+    Y = X W (numpy matmul, the library step), then y_i = sum_p a_p Y[col_p] (the SpMM
+    definition written out with np.add.reduceat), + bias, ReLU.  Returns (y_ref, tol_scale)
+    with tol_scale = sum_p |a_p| sum_k |x_{col_p,k}| |w_kc| (+ |bias|): the magnitude the
+    fp32 tolerance (1e-5 relative) applies to for either evaluation order."""
+    rowptr = np.asarray(rowptr, dtype=np.int64)
+    base = int(rowptr[0])
+    nnz = int(rowptr[-1] - base)
+    cols = np.asarray(colidx, dtype=np.int64)[base:base + nnz]
+    a = np.asarray(vals, dtype=np.float64)[base:base + nnz]
+    X64, W64 = np.asarray(X, dtype=np.float64), np.asarray(W, dtype=np.float64)
+    T = X64 @ W64
+    Tabs = np.abs(X64) @ np.abs(W64)
+    n, Fo = rowptr.size - 1, W64.shape[1]
+    y = np.zeros((n, Fo))
+    t = np.zeros((n, Fo))
+    nz = np.flatnonzero(np.diff(rowptr) > 0)
+    if nnz:
+        starts = (rowptr[:-1] - base)[nz]
+        y[nz] = np.add.reduceat(a[:, None] * T[cols], starts, axis=0)
+        t[nz] = np.add.reduceat(np.abs(a)[:, None] * Tabs[cols], starts, axis=0)
+    if bias is not None:
+        b = np.asarray(bias, dtype=np.float64)[None, :]
+        y = y + b
+        t = t + np.abs(b)
+    if relu:
+        y = np.maximum(y, 0.0)
+    return y, t
+
+
 def transpose(rowptr, colidx, n_cols: int):
     """CSR of A^T (backward pass, dX = A^T dY): (rowptr_t, colidx_t, src) with
     row j of A^T = the rows i holding column j in increasing i (a stable sort of the entries

@@ -459,3 +459,19 @@ def test_transpose_rectangular_shard_and_empty():
     assert np.array_equal(src.cpu().numpy(), osrc)
     rt, ct, src = A.transpose(cu(np.zeros(4, np.int32)), cu(np.zeros(0, np.int32)), 3)
     assert np.array_equal(rt.cpu().numpy(), np.zeros(4, np.int32)) and ct.numel() == 0
+
+
+# ---------------------------------------------------------------- GCN layer (8(f3))
+@pytest.mark.parametrize("fin,fout", [(64, 16), (16, 64), (128, 128), (32, 8)])
+def test_gcn_layer(fin, fout):
+    from paper_2308_11825_b200.layer import GCNLayer
+    w = gen.make_config("c2", vals_kind="uniform")
+    rng = np.random.default_rng(fin + fout)
+    X = w.X(fin)
+    W = rng.uniform(-0.5, 0.5, (fin, fout)).astype(np.float32)
+    b = rng.uniform(-0.5, 0.5, fout).astype(np.float32)
+    layer = GCNLayer(make_plan(w.rowptr, w.colidx), cu(w.vals), cu(W), cu(b), relu=True)
+    Y = layer(cu(X)).cpu().numpy()
+    y, t = oracle.gcn_layer(w.rowptr, w.colidx, w.vals, X, W, b, relu=True)
+    r = oracle.check_epilogue(Y, y, t)
+    assert r["nfail"] == 0, (layer.order, r)

@@ -399,3 +399,20 @@ def test_transpose_dense_and_involution(seed):
     r2, c2, s2 = oracle.transpose(rt, ct, n)               # (A^T)^T = A, entry for entry
     assert np.array_equal(r2, rowptr.astype(np.int32)) and np.array_equal(c2, colidx)
     assert np.array_equal(src[s2], np.arange(colidx.size))
+
+
+# ---------------------------------------------------------------- GCN layer (8(f3))
+def test_gcn_layer_reduces_to_spmm_and_dense():
+    rng = np.random.default_rng(9)
+    n, F = 30, 6
+    rowptr, colidx = gen.random_csr(n, n, 9, max_deg=8, dup=True)
+    vals = rng.uniform(-1, 1, colidx.size).astype(np.float32)
+    X = rng.uniform(-1, 1, (n, F)).astype(np.float32)
+    y, _ = oracle.gcn_layer(rowptr, colidx, vals, X, np.eye(F), relu=False)   # W = I: the SpMM
+    y0, _ = oracle.spmm(rowptr, colidx, vals, X)
+    assert np.allclose(y, y0, rtol=1e-13, atol=1e-13)
+    W = rng.uniform(-1, 1, (F, 4))
+    b = rng.uniform(-1, 1, 4)
+    eye = np.arange(n + 1, dtype=np.int32)                                  # A = I: dense layer
+    y1, _ = oracle.gcn_layer(eye, np.arange(n, dtype=np.int32), np.ones(n, np.float32), X, W, b)
+    assert np.allclose(y1, np.maximum(X.astype(np.float64) @ W + b, 0), rtol=1e-13, atol=1e-13)
