@@ -235,6 +235,19 @@ agcn_status_t agcn_transpose(const int32_t* rowptr, const int32_t* colidx, int64
 agcn_status_t agcn_gather_vals(const float* vals, const int32_t* src, int64_t nnz, float* out,
                                agcn_stream_t stream);
 
+/*
+ * Dense Y = X . W (+ bias, ReLU) on the tcgen05 tensor cores, kind::tf32 -- the X.W of a GCN
+ * layer.  TF32 precision: operands rounded to a 10-bit mantissa,
+ * fp32 accumulation: |y - y_ref| <= ~2^-9 sum_k |x_k w_k|.
+ *   X:  DEVICE fp32 [M x K] row-major;  Wt: DEVICE fp32 [N x K] row-major (W transposed);
+ *   Y:  DEVICE fp32 [M x N] row-major;  bias: DEVICE fp32 [N] or NULL;  relu: 0 / 1.
+ * K in [4, 256] with K % 4 == 0; N in {16, 32, 64, 128, 256}; 16-byte aligned pointers;
+ * (K rounded up to 32) x (128 + N) x 4 bytes must fit in shared memory -> else
+ * AGCN_ERR_UNSUPPORTED.  Asynchronous on `stream`.
+ */
+agcn_status_t agcn_gemm_xw(const float* X, int64_t M, int32_t K, const float* Wt, int32_t N, float* Y,
+                           const float* bias, int32_t relu, agcn_stream_t stream);
+
 agcn_status_t agcn_last_status(void);
 const char* agcn_last_error(void);
 

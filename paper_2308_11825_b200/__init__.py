@@ -17,7 +17,7 @@ import numpy as np
 from . import _lib
 from ._lib import FIELDS, STATUS
 
-__all__ = ["Plan", "AgcnError", "agcn_plan", "agcn_spmm", "agcn_spmm_ex", "transpose", "gather_vals", "shard_bounds", "propagate_host",
+__all__ = ["Plan", "AgcnError", "agcn_plan", "agcn_spmm", "agcn_spmm_ex", "transpose", "gather_vals", "gemm_xw", "shard_bounds", "propagate_host",
            "launch_count", "version", "library_path"]
 
 
@@ -271,6 +271,24 @@ def gather_vals(vals, src, out=None, stream=None):
         _check(_lib.lib().agcn_gather_vals(_dev_ptr(vals, "float32", "vals"), _dev_ptr(src, "int32", "src"),
                                            src.numel(), _dev_ptr(out, "float32", "out"),
                                            _stream_handle(stream)))
+    return out
+
+
+def gemm_xw(X, Wt, bias=None, relu: bool = False, out=None, stream=None):
+    """agcn_gemm_xw: Y = X . W (+ bias, ReLU) on the tcgen05 tensor cores (TF32).
+
+    X: [M, K] float32 CUDA; Wt: W transposed, [N, K] float32 CUDA (contiguous)."""
+    torch = _torch()
+    M, K = X.shape
+    N = Wt.shape[0]
+    if Wt.shape[1] != K:
+        raise ValueError("Wt must be [N, K]")
+    if out is None:
+        out = torch.empty((M, N), dtype=torch.float32, device=X.device)
+    b = _dev_ptr(bias, "float32", "bias") if bias is not None else None
+    _check(_lib.lib().agcn_gemm_xw(_dev_ptr(X, "float32", "X"), int(M), int(K), _dev_ptr(Wt, "float32", "Wt"),
+                                   int(N), _dev_ptr(out, "float32", "out"), b, int(bool(relu)),
+                                   _stream_handle(stream)))
     return out
 
 

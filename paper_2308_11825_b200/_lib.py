@@ -80,6 +80,8 @@ def lib():
     L.agcn_transpose.restype = c_i32
     L.agcn_gather_vals.argtypes = [c_vp, c_vp, c_i64, c_vp, c_vp]
     L.agcn_gather_vals.restype = c_i32
+    L.agcn_gemm_xw.argtypes = [c_vp, c_i64, c_i32, c_vp, c_i32, c_vp, c_vp, c_i32, c_vp]
+    L.agcn_gemm_xw.restype = c_i32
     L.agcn_last_status.argtypes = []
     L.agcn_last_status.restype = c_i32
     L.agcn_last_error.argtypes = []
@@ -95,4 +97,4 @@ def lib():
 EXPORTS = ["agcn_default_opts", "agcn_plan", "agcn_plan_ex", "agcn_spmm", "agcn_default_spmm_opts",
            "agcn_spmm_ex", "agcn_plan_destroy",
            "agcn_plan_stats", "agcn_plan_copy", "agcn_shard_bounds", "agcn_propagate_host",
-           "agcn_transpose", "agcn_gather_vals", "agcn_last_status", "agcn_last_error", "agcn_launch_count", "agcn_version"]
+           "agcn_transpose", "agcn_gather_vals", "agcn_gemm_xw", "agcn_last_status", "agcn_last_error", "agcn_launch_count", "agcn_version"]

@@ -296,6 +296,11 @@ agcn_status_t agcn_gather_vals(const float* vals, const int32_t* src, int64_t nn
     return guarded([&] { gather_vals(vals, src, nnz, out, (cudaStream_t)stream); });
 }
 
+agcn_status_t agcn_gemm_xw(const float* X, int64_t M, int32_t K, const float* Wt, int32_t N, float* Y,
+                           const float* bias, int32_t relu, agcn_stream_t stream) {
+    return guarded([&] { gemm_xw_tf32(X, M, K, Wt, N, Y, bias, relu, (cudaStream_t)stream); });
+}
+
 agcn_status_t agcn_last_status(void) { return agcn::last_status(); }
 const char* agcn_last_error(void) { return agcn::last_message(); }
 uint64_t agcn_launch_count(void) { return agcn::g_launches.load(); }

@@ -1,0 +1,284 @@
+// gemm_tc.cu -- Y = X . W on the 5th-generation tensor cores (tcgen05, kind::tf32), for the
+// dense half of a GCN layer (X' = sigma(A' (X W))).
+//
+// The product is skinny -- M = rows of X (up to millions), K = F_in <= 256, N = F_out <= 256 --
+// so it is HBM-bound (K*N*2/(4(K+N)) flop per byte), and one CTA per 128-row tile is the whole
+// design: TMA (cp.async.bulk.tensor, SWIZZLE_128B) brings the 128 x K tile of X and, once per
+// CTA, all of W^T (N x K, K-major) into shared memory; one elected thread issues the
+// tcgen05.mma chain (M = 128, N, K in steps of 8) into a TMEM accumulator of N columns;
+// tcgen05.commit signals an mbarrier; four warps read their 32 TMEM lanes (tcgen05.ld
+// 32x32b) and write the rows, with an optional bias / ReLU.  Several CTAs per SM overlap one
+// tile's loads with another's MMA and stores.
+//
+// Precision: kind::tf32 reads the fp32 operands with a 10-bit mantissa (products exact in the
+// fp32 accumulator): |y - y_ref| <= 2^-9 sum_k |x_k w_k| + fp32 accumulation.  agcn_gemm_xw
+// documents it; GCNLayer(precision="tf32") opts into it (default: fp32 cuBLAS).
+#include <cuda.h>
+
+#include <algorithm>
+#include <mutex>
+
+#include "internal.h"
+
+namespace agcn {
+namespace {
+
+constexpr int kGemmThreads = 128;  // 4 warps: one per 32 TMEM lanes (rows) of the 128-row tile
+constexpr int kBM = 128;           // rows per tile (UMMA M)
+constexpr int kBK = 32;            // fp32 per 128-byte swizzle row (one TMA box / k stage)
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+        "@!P1 bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(phase)
+        : "memory");
+}
+
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+            smem_u32(dst)),
+        "l"(map), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+        : "memory");
+}
+
+// UMMA shared-memory descriptor, K-major, SWIZZLE_128B: rows of 128 B, 8-row atoms of 1 KB
+// stacked along M/N (stride byte offset 1 KB), version 1 (sm_100).
+__device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr) {
+    uint64_t d = 0;
+    d |= (uint64_t)((saddr >> 4) & 0x3FFF);         // start address [0,14)
+    d |= (uint64_t)1 << 16;                          // leading byte offset (unused for SW128 K-major)
+    d |= (uint64_t)(1024 >> 4) << 32;                // stride byte offset [32,46)
+    d |= (uint64_t)1 << 46;                          // version [46,48) = 1
+    d |= (uint64_t)2 << 61;                          // layout type [61,64): SWIZZLE_128B
+    return d;
+}
+
+// Instruction descriptor: D = F32, A = B = TF32, both K-major, N, M = 128.
+template <int N>
+__device__ __forceinline__ uint32_t idesc_tf32() {
+    return (1u << 4)                 // c_format F32
+           | (2u << 7)               // a_format TF32
+           | (2u << 10)              // b_format TF32
+           | ((uint32_t)(N >> 3) << 17)
+           | ((uint32_t)(kBM >> 4) << 24);
+}
+
+__device__ __forceinline__ void umma_tf32(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "setp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n"
+        "}\n" ::"r"(tmem_d),
+        "l"(da), "l"(db), "r"(idesc), "r"(acc));
+}
+
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
+    uint32_t r[16];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// N output columns (16..256, multiple of 16), KT = ceil(K / 32) k stages (runtime, <= kt_max).
+template <int N>
+__global__ void __launch_bounds__(kGemmThreads) k_gemm_tf32(const __grid_constant__ CUtensorMap tmX,
+                                                           const __grid_constant__ CUtensorMap tmW,
+                                                           float* __restrict__ Y, int64_t M, int32_t KT,
+                                                           const float* __restrict__ bias, int32_t relu) {
+    constexpr uint32_t kTmemCols = N <= 32 ? 32 : N <= 64 ? 64 : N <= 128 ? 128 : 256;
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    // 1 KB alignment for SWIZZLE_128B
+    unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    float* sA = reinterpret_cast<float*>(smem);                                   // [KT][128][32]
+    float* sB = reinterpret_cast<float*>(smem + (size_t)KT * kBM * kBK * 4);       // [KT][N][32]
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + (size_t)KT * (kBM + N) * kBK * 4);
+    uint64_t* barA = bars;      // X tile landed
+    uint64_t* barB = bars + 1;  // W landed (once)
+    uint64_t* barM = bars + 2;  // MMA chain done
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+    if (threadIdx.x == 0) {
+        mbar_init(barA, 1);
+        mbar_init(barB, 1);
+        mbar_init(barM, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&tmX) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&tmW) : "memory");
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "n"(kTmemCols));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tmem = *tmem_slot;
+
+    if (threadIdx.x == 0) {  // W^T, all k stages, once per CTA
+        mbar_expect_tx(barB, (uint32_t)(KT * N * kBK * 4));
+        for (int k = 0; k < KT; ++k) tma_load_2d(sB + (size_t)k * N * kBK, &tmW, barB, k * kBK, 0);
+    }
+    const int64_t ntiles = (M + kBM - 1) / kBM;
+    uint32_t phase = 0;
+    bool w_ready = false;
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, phase ^= 1) {
+        if (threadIdx.x == 0) {
+            mbar_expect_tx(barA, (uint32_t)(KT * kBM * kBK * 4));
+            for (int k = 0; k < KT; ++k)
+                tma_load_2d(sA + (size_t)k * kBM * kBK, &tmX, barA, k * kBK, (int)(t * kBM));
+            if (!w_ready) {
+                mbar_wait(barB, 0);
+                w_ready = true;
+            }
+            mbar_wait(barA, phase);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            const uint32_t idesc = idesc_tf32<N>();
+            for (int k = 0; k < KT; ++k) {
+                const uint32_t a0 = smem_u32(sA + (size_t)k * kBM * kBK);
+                const uint32_t b0 = smem_u32(sB + (size_t)k * N * kBK);
+#pragma unroll
+                for (int kk = 0; kk < kBK / 8; ++kk)  // UMMA K = 8 tf32 = 32 bytes
+                    umma_tf32(tmem, umma_desc_sw128(a0 + kk * 32), umma_desc_sw128(b0 + kk * 32), idesc,
+                              (k | kk) != 0);
+            }
+            asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                             smem_u32(barM))
+                         : "memory");
+        }
+        __syncwarp();
+        mbar_wait(barM, phase);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        // epilogue: warp w owns TMEM lanes (tile rows) [32 w, 32 w + 32)
+        const int64_t row = t * kBM + warp * 32 + lane;
+#pragma unroll 1
+        for (int c0 = 0; c0 < N; c0 += 16) {
+            float v[16];
+            tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c0, v);
+            if (row < M) {
+                float* dst = Y + row * N + c0;
+#pragma unroll
+                for (int i = 0; i < 16; i += 4) {
+                    float4 o = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+                    if (bias) {
+                        o.x += __ldg(bias + c0 + i);
+                        o.y += __ldg(bias + c0 + i + 1);
+                        o.z += __ldg(bias + c0 + i + 2);
+                        o.w += __ldg(bias + c0 + i + 3);
+                    }
+                    if (relu) {
+                        o.x = fmaxf(o.x, 0.f); o.y = fmaxf(o.y, 0.f); o.z = fmaxf(o.z, 0.f); o.w = fmaxf(o.w, 0.f);
+                    }
+                    __stcs(reinterpret_cast<float4*>(dst + i), o);
+                }
+            }
+        }
+        // TMEM and the X tile are reused by the next tile: everyone done reading first
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        __syncthreads();
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    }
+    if (threadIdx.x == 0 && !w_ready) mbar_wait(barB, 0);  // never leave a TMA in flight
+    __syncthreads();
+    if (warp == 0)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kTmemCols));
+}
+
+// ---------------------------------------------------------------- host: tensor maps
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+    static EncodeTiledFn fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        cudaDriverEntryPointQueryResult q;
+        void* p = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeTiledFn>(p);
+    });
+    AGCN_CHECK(fn != nullptr, AGCN_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+    return fn;
+}
+
+// 2D fp32 row-major [rows x cols] (ld = cols), box {32 cols, box_rows}, SWIZZLE_128B, OOB -> 0
+CUtensorMap make_map(const float* base, int64_t rows, int64_t cols, uint32_t box_rows) {
+    CUtensorMap m;
+    cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+    cuuint64_t strides[1] = {(cuuint64_t)cols * 4};
+    cuuint32_t box[2] = {(cuuint32_t)kBK, box_rows};
+    cuuint32_t es[2] = {1, 1};
+    CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box, es,
+                             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    AGCN_CHECK(r == CUDA_SUCCESS, AGCN_ERR_INVALID_ARG, "tensor map encode failed (alignment / sizes)");
+    return m;
+}
+
+template <int N>
+void launch_gemm(const CUtensorMap& mx, const CUtensorMap& mw, float* Y, int64_t M, int32_t KT, const float* bias,
+                 int32_t relu, cudaStream_t s) {
+    const size_t smem = 1024 + (size_t)KT * (kBM + N) * kBK * 4 + 64;
+    AGCN_CHECK(smem <= 227 * 1024, AGCN_ERR_UNSUPPORTED, "F_in x F_out too large for the tcgen05 GEMM");
+    auto kern = k_gemm_tf32<N>;
+    AGCN_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int occ = 0;
+    AGCN_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kGemmThreads, smem));
+    constexpr int cols = N <= 32 ? 32 : N <= 64 ? 64 : N <= 128 ? 128 : 256;
+    occ = std::max(1, std::min(occ, 512 / cols));  // resident CTAs share the SM's 512 TMEM columns
+    const int64_t ntiles = (M + kBM - 1) / kBM;
+    const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(ntiles, (int64_t)num_sms() * occ));
+    kern<<<(unsigned)grid, kGemmThreads, smem, s>>>(mx, mw, Y, M, KT, bias, relu);
+    post_launch();
+}
+
+}  // namespace
+
+void gemm_xw_tf32(const float* X, int64_t M, int32_t K, const float* Wt, int32_t N, float* Y, const float* bias,
+                  int32_t relu, cudaStream_t s) {
+    AGCN_CHECK(M >= 0 && K >= 1 && K <= 256 && (K % 4) == 0, AGCN_ERR_UNSUPPORTED, "K must be in [4, 256], K % 4 == 0");
+    AGCN_CHECK(N == 16 || N == 32 || N == 64 || N == 128 || N == 256, AGCN_ERR_UNSUPPORTED,
+               "N must be 16, 32, 64, 128 or 256");
+    AGCN_CHECK(X && Wt && Y, AGCN_ERR_INVALID_ARG, "NULL pointer");
+    AGCN_CHECK(((reinterpret_cast<uintptr_t>(X) | reinterpret_cast<uintptr_t>(Wt) | reinterpret_cast<uintptr_t>(Y)) & 15u) == 0,
+               AGCN_ERR_INVALID_ARG, "X, W^T and Y must be 16-byte aligned");
+    if (M == 0) return;
+    const int32_t KT = (K + kBK - 1) / kBK;
+    const CUtensorMap mx = make_map(X, M, K, kBM);
+    const CUtensorMap mw = make_map(Wt, N, K, (uint32_t)N);
+    switch (N) {
+        case 16: launch_gemm<16>(mx, mw, Y, M, KT, bias, relu, s); break;
+        case 32: launch_gemm<32>(mx, mw, Y, M, KT, bias, relu, s); break;
+        case 64: launch_gemm<64>(mx, mw, Y, M, KT, bias, relu, s); break;
+        case 128: launch_gemm<128>(mx, mw, Y, M, KT, bias, relu, s); break;
+        default: launch_gemm<256>(mx, mw, Y, M, KT, bias, relu, s); break;
+    }
+}
+
+}  // namespace agcn

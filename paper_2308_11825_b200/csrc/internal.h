@@ -204,6 +204,9 @@ void launch_pipe(agcn_plan_s* p, const float* vals, const float* X, int32_t F, f
 // plan.cu: stable LSD radix sort of (key, val) pairs (8-bit digits); result in ka/va
 void radix_sort_pairs(int32_t*& ka, int32_t*& va, int32_t*& kb, int32_t*& vb, int64_t m, int64_t max_key,
                       cudaStream_t s);
+// gemm_tc.cu: Y = X W on tcgen05 (kind::tf32); Wt = W^T [N x K] row-major
+void gemm_xw_tf32(const float* X, int64_t M, int32_t K, const float* Wt, int32_t N, float* Y, const float* bias,
+                  int32_t relu, cudaStream_t s);
 // transpose.cu
 void transpose_csr(const int32_t* rowptr, const int32_t* colidx, int64_t n, int64_t n_cols, int64_t nnz,
                    int32_t* rowptr_t, int32_t* colidx_t, int32_t* src, cudaStream_t s);

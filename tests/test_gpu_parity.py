@@ -462,16 +462,40 @@ def test_transpose_rectangular_shard_and_empty():
 
 
 # ---------------------------------------------------------------- GCN layer (8(f3))
-@pytest.mark.parametrize("fin,fout", [(64, 16), (16, 64), (128, 128), (32, 8)])
-def test_gcn_layer(fin, fout):
+@pytest.mark.parametrize("fin,fout,prec", [(64, 16, "fp32"), (16, 64, "fp32"), (128, 128, "fp32"),
+                                           (32, 8, "fp32"), (64, 16, "tf32"), (16, 64, "tf32"),
+                                           (128, 128, "tf32")])
+def test_gcn_layer(fin, fout, prec):
+    """fp32: the north-star tolerance (1e-5 relative); tf32 (tcgen05 X.W): 2^-9 relative."""
     from paper_2308_11825_b200.layer import GCNLayer
     w = gen.make_config("c2", vals_kind="uniform")
     rng = np.random.default_rng(fin + fout)
     X = w.X(fin)
     W = rng.uniform(-0.5, 0.5, (fin, fout)).astype(np.float32)
     b = rng.uniform(-0.5, 0.5, fout).astype(np.float32)
-    layer = GCNLayer(make_plan(w.rowptr, w.colidx), cu(w.vals), cu(W), cu(b), relu=True)
+    layer = GCNLayer(make_plan(w.rowptr, w.colidx), cu(w.vals), cu(W), cu(b), relu=True, precision=prec)
     Y = layer(cu(X)).cpu().numpy()
     y, t = oracle.gcn_layer(w.rowptr, w.colidx, w.vals, X, W, b, relu=True)
-    r = oracle.check_epilogue(Y, y, t)
+    r = oracle.check_epilogue(Y, y, t, rel=1e-5 if prec == "fp32" else 2.0 ** -9)
     assert r["nfail"] == 0, (layer.order, r)
+
+
+# ---------------------------------------------------------------- tcgen05 GEMM (8(f3))
+@pytest.mark.parametrize("M,K,N", [(1, 4, 16), (127, 32, 16), (300, 64, 64), (1000, 100, 32),
+                                   (4097, 128, 128), (513, 256, 64), (257, 64, 256), (70000, 64, 64)])
+@pytest.mark.parametrize("epi", [False, True])
+def test_gemm_xw_tcgen05_tf32(M, K, N, epi):
+    """agcn_gemm_xw (tcgen05 kind::tf32) vs the fp64 product: |y - y_ref| <= 2^-9 sum|x w| + 1e-6
+    (TF32 operands: 10-bit mantissa, fp32 accumulation)."""
+    rng = np.random.default_rng(M + K + N)
+    X = rng.uniform(-1, 1, (M, K)).astype(np.float32)
+    W = rng.uniform(-1, 1, (K, N)).astype(np.float32)
+    b = rng.uniform(-1, 1, N).astype(np.float32) if epi else None
+    Y = A.gemm_xw(cu(X), cu(np.ascontiguousarray(W.T)), bias=cu(b) if epi else None, relu=epi).cpu().numpy()
+    ref = X.astype(np.float64) @ W.astype(np.float64)
+    mag = np.abs(X).astype(np.float64) @ np.abs(W).astype(np.float64)
+    if epi:
+        ref = np.maximum(ref + b, 0.0)
+    err = np.abs(Y - ref)
+    assert np.all(err <= 2.0 ** -9 * mag + 1e-6), float((err / (2.0 ** -9 * mag + 1e-6)).max())
+    assert err.mean() > 1e-7 or M * N < 100            # it really is TF32 (not an fp32 fallback)

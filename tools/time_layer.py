@@ -12,6 +12,7 @@ import paper_2308_11825_b200 as A  # noqa: E402
 from paper_2308_11825_b200.layer import GCNLayer  # noqa: E402
 
 name, fin, fout = sys.argv[1], int(sys.argv[2]), int(sys.argv[3])
+prec = sys.argv[4] if len(sys.argv) > 4 else "fp32"
 w = gen.make_config(name)
 dev = torch.device("cuda:0")
 rp, ci, va = (torch.from_numpy(a).to(dev) for a in (w.rowptr, w.colidx, w.vals))
@@ -20,7 +21,7 @@ g = torch.Generator(device="cpu").manual_seed(0)
 W = (torch.rand((fin, fout), generator=g) - 0.5).to(dev)
 b = (torch.rand(fout, generator=g) - 0.5).to(dev)
 plan = A.Plan(rp, ci)
-layer = GCNLayer(plan, va, W, b, relu=True)
+layer = GCNLayer(plan, va, W, b, relu=True, precision=prec)
 for _ in range(3):
     Y = layer(X)
 torch.cuda.synchronize()
@@ -33,11 +34,12 @@ e1.record()
 torch.cuda.synchronize()
 ms = e0.elapsed_time(e1) / 10
 torch.backends.cuda.matmul.allow_tf32 = False
+Wt = W.t().contiguous()
 e0.record()
 for _ in range(10):
-    T = torch.mm(X, W)
+    T = A.gemm_xw(X, Wt) if prec == "tf32" else torch.mm(X, W)
 e1.record()
 torch.cuda.synchronize()
 gemm = e0.elapsed_time(e1) / 10
-print(json.dumps({"config": name, "fin": fin, "fout": fout, "order": layer.order, "layer_ms": ms,
+print(json.dumps({"config": name, "fin": fin, "fout": fout, "precision": prec, "order": layer.order, "layer_ms": ms,
                   "gemm_XW_ms": gemm, "flops": 2 * w.nnz * min(fin, fout) + 2 * w.n * fin * fout}))
