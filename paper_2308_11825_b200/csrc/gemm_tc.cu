@@ -144,6 +144,7 @@ __global__ void __launch_bounds__(kGemmThreads) k_gemm_tf32(const __grid_constan
         for (int k = 0; k < KT; ++k) tma_load_2d(sB + (size_t)k * N * kBK, &tmW, barB, k * kBK, 0);
     }
     const int64_t ntiles = (M + kBM - 1) / kBM;
+    const bool stage_out = N <= KT * kBK;            // the output tile fits in the X tile's space
     uint32_t phase = 0;
     bool w_ready = false;
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, phase ^= 1) {
@@ -174,13 +175,19 @@ __global__ void __launch_bounds__(kGemmThreads) k_gemm_tf32(const __grid_constan
         mbar_wait(barM, phase);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         // epilogue: warp w owns TMEM lanes (tile rows) [32 w, 32 w + 32)
-        const int64_t row = t * kBM + warp * 32 + lane;
+        const int r = warp * 32 + lane;                 // row inside the tile
+        const int64_t row = t * kBM + r;
+        if (stage_out) {
+            // the tile's rows are one contiguous block of Y: stage them in shared memory (the
+            // consumed X tile; 16-byte chunks XOR-swizzled by row, conflict-free both ways)
+            // and write the block out with fully coalesced 16-byte stores
+            float4* st = reinterpret_cast<float4*>(sA);
+            constexpr int NC = N / 4;                   // 16-byte chunks per row
+            constexpr int SW = NC >= 8 ? 7 : NC - 1;
 #pragma unroll 1
-        for (int c0 = 0; c0 < N; c0 += 16) {
-            float v[16];
-            tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c0, v);
-            if (row < M) {
-                float* dst = Y + row * N + c0;
+            for (int c0 = 0; c0 < N; c0 += 16) {
+                float v[16];
+                tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c0, v);
 #pragma unroll
                 for (int i = 0; i < 16; i += 4) {
                     float4 o = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
@@ -193,7 +200,38 @@ __global__ void __launch_bounds__(kGemmThreads) k_gemm_tf32(const __grid_constan
                     if (relu) {
                         o.x = fmaxf(o.x, 0.f); o.y = fmaxf(o.y, 0.f); o.z = fmaxf(o.z, 0.f); o.w = fmaxf(o.w, 0.f);
                     }
-                    __stcs(reinterpret_cast<float4*>(dst + i), o);
+                    const int c4 = (c0 + i) / 4;
+                    st[r * NC + (c4 ^ (r & SW))] = o;
+                }
+            }
+            __syncthreads();
+            const int64_t rows = M - t * kBM < kBM ? M - t * kBM : (int64_t)kBM;
+            float4* dst = reinterpret_cast<float4*>(Y + t * kBM * N);
+            for (int q = threadIdx.x; q < rows * NC; q += kGemmThreads) {
+                const int rr = q / NC, c4 = q - rr * NC;
+                __stcs(dst + q, st[rr * NC + (c4 ^ (rr & SW))]);
+            }
+        } else {
+#pragma unroll 1
+            for (int c0 = 0; c0 < N; c0 += 16) {
+                float v[16];
+                tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c0, v);
+                if (row < M) {
+                    float* dst = Y + row * N + c0;
+#pragma unroll
+                    for (int i = 0; i < 16; i += 4) {
+                        float4 o = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+                        if (bias) {
+                            o.x += __ldg(bias + c0 + i);
+                            o.y += __ldg(bias + c0 + i + 1);
+                            o.z += __ldg(bias + c0 + i + 2);
+                            o.w += __ldg(bias + c0 + i + 3);
+                        }
+                        if (relu) {
+                            o.x = fmaxf(o.x, 0.f); o.y = fmaxf(o.y, 0.f); o.z = fmaxf(o.z, 0.f); o.w = fmaxf(o.w, 0.f);
+                        }
+                        __stcs(reinterpret_cast<float4*>(dst + i), o);
+                    }
                 }
             }
         }
