@@ -56,6 +56,9 @@ def parse():
                     help="sum: GCN (the metric's workload); mean: GraphSAGE-mean (P:126)")
     ap.add_argument("--gin-eps", type=float, default=None, help="GIN self term (1 + eps) x_i (square A)")
     ap.add_argument("--bias-relu", action="store_true", help="fused bias + ReLU epilogue")
+    ap.add_argument("--fused-allgather", action="store_true",
+                    help="N>1: the SpMM epilogue stores rows into every rank's X (CUDA IPC / NVLink) "
+                         "instead of an all-gather collective (SURVEY 8(f1))")
     ap.add_argument("--dist-backend", choices=["nccl", "gloo"], default="nccl",
                     help="gloo: test mode, every rank on cuda:0, all-gather staged through the host")
     ap.add_argument("--profile", action="store_true",
@@ -195,7 +198,8 @@ def main():
 
     import agcn_inputs as gen
     import paper_2308_11825_b200 as A
-    from paper_2308_11825_b200.dist import ShardLayout, make_all_gather, propagate
+    from paper_2308_11825_b200.dist import (PeerBuffers, ShardLayout, make_all_gather, propagate,
+                                            propagate_fused)
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -250,6 +254,16 @@ def main():
     rec = {"plan": [], "spmm": [], "ag": []}
 
     gather = make_all_gather(args.dist_backend) if P > 1 else None
+    fused = args.fused_allgather and P > 1
+    peers = PeerBuffers(lay, F) if fused else None
+
+    def fused_barrier():  # the peers' stores of this layer are complete everywhere
+        e0, e1 = ev(), ev()
+        e0.record(stream)
+        torch.cuda.current_stream().synchronize()
+        dist.barrier()
+        e1.record(stream)
+        rec["ag"].append((e0, e1))
 
     def all_gather(full, slot):
         e0, e1 = ev(), ev()
@@ -274,7 +288,18 @@ def main():
             s1.record(stream)
             if record:
                 rec["spmm"].append((s0, s1))
-        out = propagate(lay, spmm, X0, bufs, layers, all_gather if P > 1 else None)
+        if fused:
+            def spmm_f(Xin, out_rows, peer_out):
+                s0, s1 = ev(), ev()
+                s0.record(stream)
+                plan.spmm(va_d, Xin, out=out_rows, kernel=args.kernel, l2_hint=args.l2_hint,
+                          col_block_mb=args.col_block_mb, peer_out=peer_out, **epi_kw(Xin))
+                s1.record(stream)
+                if record:
+                    rec["spmm"].append((s0, s1))
+            out = propagate_fused(lay, spmm_f, X0, peers, layers, fused_barrier)
+        else:
+            out = propagate(lay, spmm, X0, bufs, layers, all_gather if P > 1 else None)
         return plan, out  # plans stay alive until after the timed region (closed below)
 
     def barrier():
@@ -341,7 +366,9 @@ def main():
             "data": "synthetic",
             "config": {"workload": w.meta["desc"], "name": w.name, "n": n, "nnz": nnz, "F": F,
                        "layers": layers, "partition": args.partition, "kernel": args.kernel,
-                       "aggregation": args.aggregation, "gin_eps": args.gin_eps, "bias_relu": args.bias_relu, "parallelism": f"row-shard{P}",
+                       "aggregation": args.aggregation, "gin_eps": args.gin_eps, "bias_relu": args.bias_relu,
+                       "allgather": ("fused (SpMM epilogue peer stores)" if fused else
+                                     f"{args.dist_backend} all_gather_into_tensor") if P > 1 else None, "parallelism": f"row-shard{P}",
                        "max_block_warps": args.mbw, "max_warp_nzs": args.mwn,
                        "l2": "inputs larger than L2 (CSR + X > 126 MB)" if
                              (8 * nnz + 4 * n * F) > 126e6 else "inputs fit in L2 (warm)",

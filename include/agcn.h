@@ -168,7 +168,15 @@ typedef struct {
     const float* self;    /* DEVICE [n x F] row-major, row i pairs with output row i; 16-byte
                              aligned; required iff self_scale != 0 */
     const float* bias;    /* DEVICE [F], 16-byte aligned, or NULL */
-    int64_t reserved[4];
+    /* Fused all-gather (multi-GPU): every finished output row i is also stored to
+       peer_out[q] + i * F for q < npeer -- typically this rank's slot in each peer's next-layer X
+       buffer, mapped into this process with agcn_ipc_open (NVLink peer stores from the SpMM's
+       own epilogue instead of a separate all-gather).  DEVICE pointers, 16-byte aligned; the
+       caller orders the peers' reads (e.g. a barrier after the layer). */
+    float* peer_out[8];
+    int32_t npeer;        /* 0 (default) .. 8 */
+    int32_t pad_;
+    int64_t reserved[2];
 } agcn_spmm_opts_t;
 
 /* Fill *opts with the defaults above. */
@@ -247,6 +255,16 @@ agcn_status_t agcn_gather_vals(const float* vals, const int32_t* src, int64_t nn
  */
 agcn_status_t agcn_gemm_xw(const float* X, int64_t M, int32_t K, const float* Wt, int32_t N, float* Y,
                            const float* bias, int32_t relu, agcn_stream_t stream);
+
+/* Device buffers that other processes can map (CUDA IPC): the fused all-gather's peer X
+   buffers.  agcn_device_alloc: cudaMalloc'd (exportable) bytes; agcn_ipc_export writes a
+   64-byte handle of ptr (a pointer returned by agcn_device_alloc); agcn_ipc_open maps a
+   handle from another process (peer access enabled lazily) and agcn_ipc_close unmaps it. */
+agcn_status_t agcn_device_alloc(size_t bytes, void** ptr);
+agcn_status_t agcn_device_free(void* ptr);
+agcn_status_t agcn_ipc_export(const void* ptr, void* handle64);
+agcn_status_t agcn_ipc_open(const void* handle64, void** ptr);
+agcn_status_t agcn_ipc_close(void* ptr);
 
 agcn_status_t agcn_last_status(void);
 const char* agcn_last_error(void);

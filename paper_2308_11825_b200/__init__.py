@@ -17,7 +17,7 @@ import numpy as np
 from . import _lib
 from ._lib import FIELDS, STATUS
 
-__all__ = ["Plan", "AgcnError", "agcn_plan", "agcn_spmm", "agcn_spmm_ex", "transpose", "gather_vals", "gemm_xw", "shard_bounds", "propagate_host",
+__all__ = ["Plan", "AgcnError", "agcn_plan", "agcn_spmm", "agcn_spmm_ex", "transpose", "gather_vals", "gemm_xw", "DeviceBuffer", "ipc_open", "ipc_close", "shard_bounds", "propagate_host",
            "launch_count", "version", "library_path"]
 
 
@@ -151,7 +151,7 @@ class Plan:
 
     def spmm(self, vals, X, out=None, stream=None, kernel: str = "auto", l2_hint: int | None = None,
              col_block_mb: int | None = None, aggregation: str = "sum", self_x=None,
-             self_scale: float = 0.0, bias=None, relu: bool = False):
+             self_scale: float = 0.0, bias=None, relu: bool = False, peer_out=()):
         """Y = A.X (asynchronous on `stream`, default the current torch stream).
 
         kernel: "auto" | "general" | "wide" (agcn_kernel_t); l2_hint: None (auto: evict_last
@@ -174,7 +174,7 @@ class Plan:
         x = _dev_ptr(X, "float32", "X") if X.numel() else 0
         y = _dev_ptr(out, "float32", "out") if out.numel() else 0
         opts = _spmm_opts(kernel, l2_hint, col_block_mb, aggregation, self_x, self_scale, bias, relu,
-                          shape=(self.n, F))
+                          shape=(self.n, F), peer_out=peer_out)
         _check(_lib.lib().agcn_spmm_ex(self.handle, v or None, x or None, int(F), y or None,
                                        _stream_handle(stream), opts))
         return out
@@ -199,7 +199,7 @@ class Plan:
 
 def _spmm_opts(kernel: str = "auto", l2_hint: int | None = None, col_block_mb: int | None = None,
                aggregation: str = "sum", self_x=None, self_scale: float = 0.0, bias=None,
-               relu: bool = False, shape=None):
+               relu: bool = False, shape=None, peer_out=()):
     o = _lib.SpmmOpts()
     _lib.lib().agcn_default_spmm_opts(ctypes.byref(o))
     o.kernel = _lib.KERNELS[kernel]
@@ -216,6 +216,11 @@ def _spmm_opts(kernel: str = "auto", l2_hint: int | None = None, col_block_mb: i
         if shape is not None and tuple(bias.shape) != (shape[1],):
             raise ValueError(f"bias must be [{shape[1]}]")
         o.bias = _dev_ptr(bias, "float32", "bias")
+    if len(peer_out) > 8:
+        raise ValueError("at most 8 peer_out pointers")
+    for q, ptr in enumerate(peer_out):   # fused all-gather targets (device addresses)
+        o.peer_out[q] = int(ptr)
+    o.npeer = len(peer_out)
     return ctypes.byref(o)
 
 
@@ -290,6 +295,44 @@ def gemm_xw(X, Wt, bias=None, relu: bool = False, out=None, stream=None):
                                    int(N), _dev_ptr(out, "float32", "out"), b, int(bool(relu)),
                                    _stream_handle(stream)))
     return out
+
+
+class DeviceBuffer:
+    """A cudaMalloc'd fp32 [rows, cols] buffer from libagcn (agcn_device_alloc): exportable to
+    other processes (agcn_ipc_export); ``.tensor`` views it as a torch CUDA tensor (zero copy,
+    via __cuda_array_interface__)."""
+
+    def __init__(self, rows: int, cols: int):
+        torch = _torch()
+        ptr = ctypes.c_void_p()
+        _check(_lib.lib().agcn_device_alloc(max(1, rows * cols) * 4, ctypes.byref(ptr)))
+        self.ptr = int(ptr.value)
+        self.shape = (rows, cols)
+        self.__cuda_array_interface__ = {"shape": self.shape, "typestr": "<f4", "data": (self.ptr, False),
+                                         "version": 3, "strides": None}
+        self.tensor = torch.as_tensor(self, device="cuda")
+
+    def export(self) -> bytes:
+        h = ctypes.create_string_buffer(64)
+        _check(_lib.lib().agcn_ipc_export(self.ptr, h))
+        return h.raw
+
+    def close(self):
+        if self.ptr:
+            self.tensor = None
+            _lib.lib().agcn_device_free(self.ptr)
+            self.ptr = 0
+
+
+def ipc_open(handle: bytes) -> int:
+    """Map another process's DeviceBuffer (agcn_ipc_open); returns the device address."""
+    ptr = ctypes.c_void_p()
+    _check(_lib.lib().agcn_ipc_open(ctypes.create_string_buffer(handle, 64), ctypes.byref(ptr)))
+    return int(ptr.value)
+
+
+def ipc_close(ptr: int):
+    _check(_lib.lib().agcn_ipc_close(ptr))
 
 
 def shard_bounds(rowptr, nranks: int, stream=None) -> np.ndarray:

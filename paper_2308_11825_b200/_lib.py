@@ -28,7 +28,8 @@ KERNELS = {"auto": 0, "general": 1, "looped": 2, "wide": 3, "pipe": 4}
 class SpmmOpts(ctypes.Structure):
     _fields_ = [("kernel", c_i32), ("l2_hint", c_i32), ("col_block_mb", c_i32),
                 ("aggregation", c_i32), ("self_scale", ctypes.c_float), ("relu", c_i32),
-                ("self", c_vp), ("bias", c_vp), ("reserved", c_i64 * 4)]
+                ("self", c_vp), ("bias", c_vp), ("peer_out", c_vp * 8), ("npeer", c_i32),
+                ("pad_", c_i32), ("reserved", c_i64 * 2)]
 
 
 class Stats(ctypes.Structure):
@@ -82,6 +83,16 @@ def lib():
     L.agcn_gather_vals.restype = c_i32
     L.agcn_gemm_xw.argtypes = [c_vp, c_i64, c_i32, c_vp, c_i32, c_vp, c_vp, c_i32, c_vp]
     L.agcn_gemm_xw.restype = c_i32
+    L.agcn_device_alloc.argtypes = [c_size, ctypes.POINTER(c_vp)]
+    L.agcn_device_alloc.restype = c_i32
+    L.agcn_device_free.argtypes = [c_vp]
+    L.agcn_device_free.restype = c_i32
+    L.agcn_ipc_export.argtypes = [c_vp, c_vp]
+    L.agcn_ipc_export.restype = c_i32
+    L.agcn_ipc_open.argtypes = [c_vp, ctypes.POINTER(c_vp)]
+    L.agcn_ipc_open.restype = c_i32
+    L.agcn_ipc_close.argtypes = [c_vp]
+    L.agcn_ipc_close.restype = c_i32
     L.agcn_last_status.argtypes = []
     L.agcn_last_status.restype = c_i32
     L.agcn_last_error.argtypes = []
@@ -97,4 +108,5 @@ def lib():
 EXPORTS = ["agcn_default_opts", "agcn_plan", "agcn_plan_ex", "agcn_spmm", "agcn_default_spmm_opts",
            "agcn_spmm_ex", "agcn_plan_destroy",
            "agcn_plan_stats", "agcn_plan_copy", "agcn_shard_bounds", "agcn_propagate_host",
-           "agcn_transpose", "agcn_gather_vals", "agcn_gemm_xw", "agcn_last_status", "agcn_last_error", "agcn_launch_count", "agcn_version"]
+           "agcn_transpose", "agcn_gather_vals", "agcn_gemm_xw", "agcn_device_alloc", "agcn_device_free", "agcn_ipc_export",
+           "agcn_ipc_open", "agcn_ipc_close", "agcn_last_status", "agcn_last_error", "agcn_launch_count", "agcn_version"]

@@ -133,6 +133,10 @@ agcn_status_t agcn_spmm_ex(agcn_plan_t plan, const float* vals, const float* X, 
                    "self_scale != 0 needs the self matrix");
         AGCN_CHECK(((reinterpret_cast<uintptr_t>(o.self) | reinterpret_cast<uintptr_t>(o.bias)) & 15u) == 0,
                    AGCN_ERR_INVALID_ARG, "self and bias must be 16-byte aligned");
+        AGCN_CHECK(o.npeer >= 0 && o.npeer <= kMaxPeers, AGCN_ERR_INVALID_ARG, "npeer must be in [0, 8]");
+        for (int q = 0; q < o.npeer; ++q)
+            AGCN_CHECK(o.peer_out[q] && (reinterpret_cast<uintptr_t>(o.peer_out[q]) & 15u) == 0,
+                       AGCN_ERR_INVALID_ARG, "peer_out pointers must be non-NULL and 16-byte aligned");
         if (plan->n == 0) return;
         AGCN_CHECK(Y != nullptr, AGCN_ERR_INVALID_ARG, "Y is NULL");
         AGCN_CHECK(plan->nnz == 0 || (vals != nullptr && X != nullptr), AGCN_ERR_INVALID_ARG,
@@ -299,6 +303,45 @@ agcn_status_t agcn_gather_vals(const float* vals, const int32_t* src, int64_t nn
 agcn_status_t agcn_gemm_xw(const float* X, int64_t M, int32_t K, const float* Wt, int32_t N, float* Y,
                            const float* bias, int32_t relu, agcn_stream_t stream) {
     return guarded([&] { gemm_xw_tf32(X, M, K, Wt, N, Y, bias, relu, (cudaStream_t)stream); });
+}
+
+agcn_status_t agcn_device_alloc(size_t bytes, void** ptr) {
+    return guarded([&] {
+        AGCN_CHECK(ptr != nullptr, AGCN_ERR_INVALID_ARG, "ptr is NULL");
+        *ptr = nullptr;
+        AGCN_CUDA(cudaMalloc(ptr, bytes ? bytes : 16));
+    });
+}
+
+agcn_status_t agcn_device_free(void* ptr) {
+    return guarded([&] {
+        if (ptr) AGCN_CUDA(cudaFree(ptr));
+    });
+}
+
+agcn_status_t agcn_ipc_export(const void* ptr, void* handle64) {
+    return guarded([&] {
+        AGCN_CHECK(ptr && handle64, AGCN_ERR_INVALID_ARG, "NULL pointer");
+        static_assert(sizeof(cudaIpcMemHandle_t) == 64, "64-byte IPC handle");
+        cudaIpcMemHandle_t h;
+        AGCN_CUDA(cudaIpcGetMemHandle(&h, const_cast<void*>(ptr)));
+        memcpy(handle64, &h, sizeof(h));
+    });
+}
+
+agcn_status_t agcn_ipc_open(const void* handle64, void** ptr) {
+    return guarded([&] {
+        AGCN_CHECK(handle64 && ptr, AGCN_ERR_INVALID_ARG, "NULL pointer");
+        cudaIpcMemHandle_t h;
+        memcpy(&h, handle64, sizeof(h));
+        AGCN_CUDA(cudaIpcOpenMemHandle(ptr, h, cudaIpcMemLazyEnablePeerAccess));
+    });
+}
+
+agcn_status_t agcn_ipc_close(void* ptr) {
+    return guarded([&] {
+        if (ptr) AGCN_CUDA(cudaIpcCloseMemHandle(ptr));
+    });
 }
 
 agcn_status_t agcn_last_status(void) { return agcn::last_status(); }

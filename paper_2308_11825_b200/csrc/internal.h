@@ -88,14 +88,25 @@ void exclusive_scan_i32(const int32_t* in, int32_t* out, int64_t n, cudaStream_t
 
 // ------------------------------------------------------------------ SpMM epilogue
 // y_i = agg(i) * (mean ? 1/deg_i : 1) + self_scale * self[i] + bias; relu (agcn_spmm_opts_t)
+constexpr int kMaxPeers = 8;
 struct Epi {
     const float* self;
     const float* bias;
     float self_scale;
     int32_t mean, relu;
     int32_t F;
-    __host__ __device__ bool active() const { return mean || self || bias || relu; }
+    int32_t npeer;                 // fused all-gather: output rows also stored to peer[q] + row * F
+    float* peer[kMaxPeers];
+    __host__ __device__ bool active() const { return mean || self || bias || relu || npeer; }
 };
+
+// the fused all-gather's extra copies of a finished output row slice (16 bytes at `off`)
+__device__ __forceinline__ void fanout4(const Epi& e, int64_t off, const float4& v) {
+    for (int q = 0; q < e.npeer; ++q) __stcs(reinterpret_cast<float4*>(e.peer[q] + off), v);
+}
+__device__ __forceinline__ void fanout1(const Epi& e, int64_t off, float v) {
+    for (int q = 0; q < e.npeer; ++q) __stcs(e.peer[q] + off, v);
+}
 
 __device__ __forceinline__ float4 epi4(float4 y, int32_t deg, int64_t orow, int32_t c, const Epi& e) {
     if (e.mean) {

@@ -273,6 +273,11 @@ __global__ void __launch_bounds__(kCtaThreads, 4) k_spmm_block(const __grid_cons
     }
 }
 
+__device__ __forceinline__ void fanout_v(const Epi& e, int64_t vec_off, const float4& v) {
+    fanout4(e, 4 * vec_off, v);  // vec_off counts float4 vectors
+}
+__device__ __forceinline__ void fanout_v(const Epi& e, int64_t off, float v) { fanout1(e, off, v); }
+
 __device__ __forceinline__ float4 epi_v(float4 y, int32_t deg, int64_t orow, int32_t c, const Epi& e) {
     return epi4(y, deg, orow, 4 * c, e);  // c counts float4 vectors
 }
@@ -292,7 +297,9 @@ __global__ void k_epilogue(float* __restrict__ Y, int64_t k0, int64_t k1, int32_
         const int32_t c = (int32_t)(i % F);
         const int64_t orow = perm ? perm[k] : k;
         float* y = Y + orow * F + c;
-        *y = epi1(*y, rp[k + 1] - rp[k], orow, c, epi);
+        const float v = epi1(*y, rp[k + 1] - rp[k], orow, c, epi);
+        *y = v;
+        fanout1(epi, orow * F + c, v);
     }
 }
 
@@ -338,6 +345,7 @@ __global__ void __launch_bounds__(kReduceThreads) k_ov_reduce(
             for (int gg = 1; gg < NG; ++gg) vadd(sum, part[gg * FVc + cl]);
             if (epi.active()) sum = epi_v(sum, srp[ov_start + k + 1] - srp[ov_start + k], orow, c, epi);
             sty(Y + orow * FV + c, sum);
+            if (epi.npeer) fanout_v(epi, orow * FV + c, sum);
         }
         __syncthreads();
     }
@@ -566,8 +574,9 @@ void spmm_launch(agcn_plan_s* p, const float* vals, const float* X, int32_t F, f
     } rec{p, s, foreign};
     // LOOPED (ablation 2, Fig. 4(a) / Table II): no combined warp -- one warp of 32 scalar lanes
     // walks the columns of a row in strides of 32
-    const Epi epi{o.self_scale != 0.f ? o.self : nullptr, o.bias, o.self_scale,
-                  o.aggregation == AGCN_AGG_MEAN, o.relu != 0, F};
+    Epi epi{o.self_scale != 0.f ? o.self : nullptr, o.bias, o.self_scale,
+            o.aggregation == AGCN_AGG_MEAN, o.relu != 0, F, o.npeer, {}};
+    for (int q = 0; q < o.npeer; ++q) epi.peer[q] = o.peer_out[q];
     const bool looped = o.kernel == AGCN_KERNEL_LOOPED;
     const bool v4 = !looped && (F % 4 == 0) && aligned16(X) && aligned16(Y);
     const int32_t FV = v4 ? F / 4 : F;

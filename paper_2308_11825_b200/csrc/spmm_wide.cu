@@ -105,6 +105,10 @@ __device__ __forceinline__ void store_row(float* Y, int64_t orow, int32_t c, int
         v.b = epi4(v.b, deg, orow, c + 4, e);
     }
     st8(Y + orow * F + c, v);
+    if (EPI) {
+        fanout4(e, orow * F + c, v.a);
+        fanout4(e, orow * F + c + 4, v.b);
+    }
 }
 
 // L lanes per X row (F = 8 L), U X rows in flight per lane, MINB resident CTAs per SM

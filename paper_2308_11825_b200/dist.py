@@ -116,3 +116,56 @@ def make_all_gather(backend: str):
         full.copy_(h_full)
 
     return gloo_all_gather
+
+
+class PeerBuffers:
+    """Fused all-gather: ``n_bufs`` padded [P*S, F] next-layer X buffers per rank,
+    allocated by libagcn (DeviceBuffer) and mapped into every other rank (CUDA IPC).  The SpMM of
+    rank p stores each finished output row into its own slot AND into slot p of every peer's
+    buffer (agcn_spmm_opts_t.peer_out: NVLink peer stores from the kernel's epilogue), so no
+    separate collective runs between layers -- only a barrier."""
+
+    def __init__(self, layout: ShardLayout, F: int, n_bufs: int = 2):
+        import torch.distributed as dist
+
+        from . import DeviceBuffer, ipc_open
+        self.layout, self.F = layout, F
+        self.local = [DeviceBuffer(layout.padded_rows, F) for _ in range(n_bufs)]
+        handles = [b.export() for b in self.local]
+        everyone = [None] * layout.P
+        dist.all_gather_object(everyone, handles)
+        self.mapped = []       # mapped[b][q]: device address of rank q's buffer b (0 = own)
+        for b in range(n_bufs):
+            self.mapped.append([0 if q == layout.rank else ipc_open(everyone[q][b]) for q in range(layout.P)])
+        dist.barrier()
+
+    def tensor(self, b: int):
+        return self.local[b].tensor
+
+    def peer_out(self, b: int):
+        """Addresses of this rank's slot in every peer's buffer b."""
+        off = self.layout.rank * self.layout.slot_rows * self.F * 4
+        return [self.mapped[b][q] + off for q in range(self.layout.P) if q != self.layout.rank]
+
+    def close(self):
+        from . import ipc_close
+        for row in self.mapped:
+            for q, ptr in enumerate(row):
+                if ptr:
+                    ipc_close(ptr)
+        for b in self.local:
+            b.close()
+
+
+def propagate_fused(layout: ShardLayout, spmm, X0, peers: PeerBuffers, layers: int, barrier):
+    """``layers`` propagation layers with the fused all-gather: spmm(Xin, out_rows, peer_out)
+    writes this rank's rows locally and into every peer; ``barrier()`` orders the peers'
+    stores before the next layer reads them.  Returns the padded buffer of the last layer."""
+    cur = X0
+    nb = len(peers.local)
+    for layer in range(layers):
+        nxt = peers.tensor(layer % nb)
+        spmm(cur, layout.own_rows(nxt), peers.peer_out(layer % nb))
+        barrier()
+        cur = nxt
+    return cur

@@ -38,7 +38,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, F, q):
+def _worker(rank, world, port, F, q, fused=False):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -65,7 +65,21 @@ def _worker(rank, world, port, F, q):
             plan.spmm(va_d, Xin, out=out_rows)
             layers_out.append(Xin)
 
-        out = propagate(lay, spmm, X0, bufs, 2, make_all_gather("gloo"))
+        if fused:   # the SpMM epilogue stores every row into all ranks' buffers (CUDA IPC)
+            from paper_2308_11825_b200.dist import PeerBuffers, propagate_fused
+            peers = PeerBuffers(lay, F)
+
+            def spmm_f(Xin, out_rows, peer_out):
+                plan.spmm(va_d, Xin, out=out_rows, peer_out=peer_out)
+                layers_out.append(Xin)
+
+            def barrier():
+                torch.cuda.synchronize()
+                dist.barrier()
+
+            out = propagate_fused(lay, spmm_f, X0, peers, 2, barrier)
+        else:
+            out = propagate(lay, spmm, X0, bufs, 2, make_all_gather("gloo"))
         torch.cuda.synchronize()
         if rank == 0:
             Y1 = lay.unpad(layers_out[1]).cpu().numpy()     # layer-2 input = layer-1 output
@@ -73,6 +87,9 @@ def _worker(rank, world, port, F, q):
             r1 = oracle.spmm_check(w.rowptr, w.colidx, w.vals, X, Y1)
             r2 = oracle.spmm_check(w.rowptr, w.colidx, w.vals, Y1, Y2)
             q.put(("ok", r1["nfail"], r2["nfail"], r1["max_ratio"], r2["max_ratio"]))
+        dist.barrier()
+        if fused:
+            peers.close()
         plan.close()
     except Exception as e:  # pragma: no cover
         q.put(("err", repr(e), 0, 0, 0))
@@ -81,12 +98,14 @@ def _worker(rank, world, port, F, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,F", [(2, 64), (3, 16)])
-def test_sharded_propagation_on_gpu(world, F):
+@pytest.mark.parametrize("world,F,fused", [(2, 64, False), (3, 16, False), (2, 64, True), (3, 128, True)])
+def test_sharded_propagation_on_gpu(world, F, fused):
+    """fused=True: the fused all-gather -- peer stores from the SpMM epilogue
+    into IPC-mapped buffers of every rank instead of a collective."""
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, F, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, F, q, fused)) for r in range(world)]
     for p in procs:
         p.start()
     status, n1, n2, m1, m2 = q.get(timeout=600)
@@ -96,13 +115,14 @@ def test_sharded_propagation_on_gpu(world, F):
     assert n1 == 0 and n2 == 0, (m1, m2)
 
 
-def test_bench_multi_rank_mode():
+@pytest.mark.parametrize("fused", [False, True])
+def test_bench_multi_rank_mode(fused):
     """bench.py under torchrun, 2 ranks (gloo test mode on one GPU): one JSON line from rank 0."""
     port = _free_port()
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
            "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.join(ROOT, "bench.py"),
            "--gpus", "2", "--steps", "2", "--warmup", "3", "--config", "c3", "--dist-backend", "gloo",
-           "--e2e-steps", "1"]
+           "--e2e-steps", "1"] + (["--fused-allgather"] if fused else [])
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT)
     assert r.returncode == 0, r.stderr[-3000:]
     lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
