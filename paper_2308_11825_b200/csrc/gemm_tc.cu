@@ -16,6 +16,7 @@
 #include <cuda.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <mutex>
 
 #include "internal.h"
@@ -246,6 +247,149 @@ __global__ void __launch_bounds__(kGemmThreads) k_gemm_tf32(const __grid_constan
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kTmemCols));
 }
 
+// ---------------------------------------------------------------- pipelined (warp-specialized)
+// One persistent CTA per SM streaming 128-row tiles: warp 0 (one lane) keeps NS X tiles in
+// flight with TMA; warp 1 (one lane) issues the tcgen05.mma chain of a tile into one of two
+// TMEM accumulators and commits it to "tile full" and "stage free" mbarriers; warps 2-5 drain
+// the other accumulator (tcgen05.ld, bias / ReLU) and write the rows, so loads, MMAs and
+// stores of consecutive tiles overlap inside the CTA.
+constexpr int kWsThreads = 192;
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+template <int N, int NS>
+__global__ void __launch_bounds__(kWsThreads, 1) k_gemm_tf32_ws(const __grid_constant__ CUtensorMap tmX,
+                                                               const __grid_constant__ CUtensorMap tmW,
+                                                               float* __restrict__ Y, int64_t M, int32_t KT,
+                                                               const float* __restrict__ bias, int32_t relu) {
+    constexpr uint32_t kAcc = N <= 32 ? 32 : N <= 64 ? 64 : N <= 128 ? 128 : 256;  // columns per accumulator
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    const size_t a_bytes = (size_t)KT * kBM * kBK * 4;        // one X tile (all k stages)
+    float* sA = reinterpret_cast<float*>(smem);                // [NS][KT][128][32]
+    float* sB = reinterpret_cast<float*>(smem + NS * a_bytes); // [KT][N][32]
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + NS * a_bytes + (size_t)KT * N * kBK * 4);
+    uint64_t* full = bars;            // [NS] X tile landed
+    uint64_t* empty = bars + NS;      // [NS] X tile consumed by the MMAs
+    uint64_t* acc_full = bars + 2 * NS;       // [2] accumulator ready
+    uint64_t* acc_empty = bars + 2 * NS + 2;  // [2] accumulator drained (4 epilogue warps)
+    uint64_t* barB = bars + 2 * NS + 4;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * NS + 5);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < NS; ++i) {
+            mbar_init(full + i, 1);
+            mbar_init(empty + i, 1);
+        }
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(acc_full + i, 1);
+            mbar_init(acc_empty + i, 4);
+        }
+        mbar_init(barB, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "n"(2 * kAcc));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tmem = *tmem_slot;
+    const int64_t ntiles = (M + kBM - 1) / kBM;
+
+    if (warp == 0) {
+        if (lane == 0) {  // ---- TMA producer
+            mbar_expect_tx(barB, (uint32_t)(KT * N * kBK * 4));
+            for (int k = 0; k < KT; ++k) tma_load_2d(sB + (size_t)k * N * kBK, &tmW, barB, k * kBK, 0);
+            int st = 0;
+            uint32_t ph = 0;
+            for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+                mbar_wait(empty + st, ph ^ 1);            // first pass: free
+                mbar_expect_tx(full + st, (uint32_t)a_bytes);
+                float* dst = reinterpret_cast<float*>(reinterpret_cast<unsigned char*>(sA) + st * a_bytes);
+                for (int k = 0; k < KT; ++k)
+                    tma_load_2d(dst + (size_t)k * kBM * kBK, &tmX, full + st, k * kBK, (int)(t * kBM));
+                if (++st == NS) { st = 0; ph ^= 1; }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {  // ---- MMA issuer
+            mbar_wait(barB, 0);
+            const uint32_t idesc = idesc_tf32<N>();
+            int st = 0;
+            uint32_t ph = 0, aph[2] = {0, 0};
+            int acc = 0;
+            for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+                mbar_wait(acc_empty + acc, aph[acc] ^ 1);  // accumulator drained (first use: free)
+                mbar_wait(full + st, ph);
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                const uint32_t a_base = smem_u32(reinterpret_cast<unsigned char*>(sA) + st * a_bytes);
+                for (int k = 0; k < KT; ++k) {
+                    const uint32_t a0 = a_base + (uint32_t)(k * kBM * kBK * 4);
+                    const uint32_t b0 = smem_u32(sB + (size_t)k * N * kBK);
+#pragma unroll
+                    for (int kk = 0; kk < kBK / 8; ++kk)
+                        umma_tf32(tmem + acc * kAcc, umma_desc_sw128(a0 + kk * 32), umma_desc_sw128(b0 + kk * 32),
+                                  idesc, (k | kk) != 0);
+                }
+                asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                                 smem_u32(empty + st))
+                             : "memory");
+                asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                                 smem_u32(acc_full + acc))
+                             : "memory");
+                aph[acc] ^= 1;
+                acc ^= 1;
+                if (++st == NS) { st = 0; ph ^= 1; }
+            }
+        }
+    } else {  // ---- epilogue: warps 2..5 -> TMEM lane quadrant warp % 4
+        const int quad = warp & 3;
+        uint32_t aph[2] = {0, 0};
+        int acc = 0;
+        for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+            mbar_wait(acc_full + acc, aph[acc]);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            const int64_t row = t * kBM + quad * 32 + lane;
+#pragma unroll 1
+            for (int c0 = 0; c0 < N; c0 += 16) {
+                float v[16];
+                tmem_ld16(tmem + acc * kAcc + ((uint32_t)(quad * 32) << 16) + (uint32_t)c0, v);
+                if (row < M) {
+                    float* dst = Y + row * N + c0;
+#pragma unroll
+                    for (int i = 0; i < 16; i += 4) {
+                        float4 o = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+                        if (bias) {
+                            o.x += __ldg(bias + c0 + i);
+                            o.y += __ldg(bias + c0 + i + 1);
+                            o.z += __ldg(bias + c0 + i + 2);
+                            o.w += __ldg(bias + c0 + i + 3);
+                        }
+                        if (relu) {
+                            o.x = fmaxf(o.x, 0.f); o.y = fmaxf(o.y, 0.f); o.z = fmaxf(o.z, 0.f); o.w = fmaxf(o.w, 0.f);
+                        }
+                        __stcs(reinterpret_cast<float4*>(dst + i), o);
+                    }
+                }
+            }
+            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) mbar_arrive(acc_empty + acc);
+            aph[acc] ^= 1;
+            acc ^= 1;
+        }
+    }
+    __syncthreads();
+    if (warp == 1)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(2 * kAcc));
+}
+
 // ---------------------------------------------------------------- host: tensor maps
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
@@ -279,9 +423,32 @@ CUtensorMap make_map(const float* base, int64_t rows, int64_t cols, uint32_t box
     return m;
 }
 
+template <int N, int NS>
+bool try_launch_ws(const CUtensorMap& mx, const CUtensorMap& mw, float* Y, int64_t M, int32_t KT, const float* bias,
+                   int32_t relu, cudaStream_t s) {
+    const size_t smem = 1024 + (size_t)NS * KT * kBM * kBK * 4 + (size_t)KT * N * kBK * 4 + 128;
+    if (smem > 227 * 1024) return false;
+    auto kern = k_gemm_tf32_ws<N, NS>;
+    AGCN_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    const int64_t ntiles = (M + kBM - 1) / kBM;
+    const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(ntiles, (int64_t)num_sms()));
+    kern<<<(unsigned)grid, kWsThreads, smem, s>>>(mx, mw, Y, M, KT, bias, relu);
+    post_launch();
+    return true;
+}
+
+int gemm_variant() {  // A/B switch: 0 pipelined (default when it fits), 1 one tile per CTA
+    static const int v = [] { const char* e = getenv("AGCN_GEMM_VARIANT"); return e ? atoi(e) : 0; }();
+    return v;
+}
+
 template <int N>
 void launch_gemm(const CUtensorMap& mx, const CUtensorMap& mw, float* Y, int64_t M, int32_t KT, const float* bias,
                  int32_t relu, cudaStream_t s) {
+    if (gemm_variant() == 0 && (try_launch_ws<N, 4>(mx, mw, Y, M, KT, bias, relu, s) ||
+                                try_launch_ws<N, 3>(mx, mw, Y, M, KT, bias, relu, s) ||
+                                try_launch_ws<N, 2>(mx, mw, Y, M, KT, bias, relu, s)))
+        return;
     const size_t smem = 1024 + (size_t)KT * (kBM + N) * kBK * 4 + 64;
     AGCN_CHECK(smem <= 227 * 1024, AGCN_ERR_UNSUPPORTED, "F_in x F_out too large for the tcgen05 GEMM");
     auto kern = k_gemm_tf32<N>;
