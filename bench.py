@@ -380,6 +380,9 @@ def main():
                                                    "n_oversized_blocks", "max_deg")},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                          "frac": achieved / peaks["hbm_gbs"], "traffic": traffic,
+                         # the DRAM bytes ncu measured for this kernel, moved in the event time
+                         "traffic_gbs": traffic / (spmm_max * 1e-3) / 1e9 if traffic else None,
+                         "traffic_frac": traffic / (spmm_max * 1e-3) / 1e9 / peaks["hbm_gbs"] if traffic else None,
                          "kernel": "agcn_spmm (%s + k_ov_reduce)" % (
                              "k_spmm_pipe" if args.kernel == "pipe" else
                              "k_spmm_wide" if args.kernel in ("auto", "wide") and F in (8, 16, 32, 64, 128, 256)
