@@ -143,12 +143,14 @@ struct PlanFlags {          // device-written, read back once (validation + size
     int32_t max_deg;
     int32_t rowptr_first;
     int32_t rowptr_last;
-    int32_t pad[3];
+    int32_t n_ov_heavy;     // oversized rows of more than kHeavyChunks deg_bound chunks
+    int32_t pad[2];
     int64_t ov_chunks;      // sum over oversized rows of ceil(deg / deg_bound)
     int64_t ov_chunks_heavy;  // the part of ov_chunks from rows of degree >= kColBlockMinDeg
 };
 
 // Column-blocked execution schedule of the oversized rows (sched.cu), per block width.
+constexpr int32_t kHeavyChunks = 16;     // oversized rows above this many chunks: CTA-wide merge
 constexpr int32_t kColBlockMinDeg = 2048;  // rows of at least this degree are cut at blocks
 constexpr int32_t kMaxPieces = 16;         // pieces per deg_bound chunk at most
 struct ColSched {
@@ -174,6 +176,7 @@ struct agcn_plan_s {
     // AGCN_PARTITION_BLOCK
     int64_t nblocks = 0, nb_small = 0, n_zero = 0, n_ov = 0, ov_start = 0, ov_chunks = 0;
     int64_t ov_chunks_heavy = 0;       // chunks of rows of degree >= kColBlockMinDeg
+    int64_t n_ov_heavy = 0;            // oversized rows of more than kHeavyChunks chunks (a suffix)
     int64_t max_deg = 0;
     int32_t* perm = nullptr;           // [n]   sorted position -> original row
     int32_t* sorted_rowptr = nullptr;  // [n+1] row pointer of the degree-sorted CSR (P:295 (3))

@@ -45,6 +45,7 @@ __global__ void __launch_bounds__(kThreads) k_deg_hist(const int32_t* __restrict
     const int64_t lo = (int64_t)blockIdx.x * kTile, hi = min(n, lo + kTile);
     int32_t maxd = 0, bad = 0;
     long long ovc = 0, ovh = 0;
+    int32_t nhv = 0;
     for (int64_t i = lo + threadIdx.x; i < hi; i += kThreads) {
         int32_t d = rowptr[i + 1] - rowptr[i];
         if (d < 0) bad = 1;
@@ -53,6 +54,7 @@ __global__ void __launch_bounds__(kThreads) k_deg_hist(const int32_t* __restrict
         maxd = max(maxd, d);
         if (d > db) ovc += (d + db - 1) / db;
         if (d > db && d >= kColBlockMinDeg) ovh += (d + db - 1) / db;
+        if ((int64_t)d > (int64_t)kHeavyChunks * db) ++nhv;
     }
 #pragma unroll
     for (int o = 16; o; o >>= 1) {
@@ -60,12 +62,14 @@ __global__ void __launch_bounds__(kThreads) k_deg_hist(const int32_t* __restrict
         bad |= __shfl_xor_sync(0xffffffffu, bad, o);
         ovc += __shfl_xor_sync(0xffffffffu, ovc, o);
         ovh += __shfl_xor_sync(0xffffffffu, ovh, o);
+        nhv += __shfl_xor_sync(0xffffffffu, nhv, o);
     }
     if ((threadIdx.x & 31) == 0) {
         if (maxd) atomicMax(&flags->max_deg, maxd);
         if (bad) flags->bad_rowptr = 1;
         if (ovc) atomicAdd((unsigned long long*)&flags->ov_chunks, (unsigned long long)ovc);
         if (ovh) atomicAdd((unsigned long long*)&flags->ov_chunks_heavy, (unsigned long long)ovh);
+        if (nhv) atomicAdd(&flags->n_ov_heavy, nhv);
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         flags->rowptr_first = rowptr[0];
@@ -519,6 +523,7 @@ void build_block_plan(agcn_plan_s* p, const int32_t* rowptr, const int32_t* coli
     p->ov_start = n - p->n_ov;
     p->ov_chunks = hf.ov_chunks;
     p->ov_chunks_heavy = hf.ov_chunks_heavy;
+    p->n_ov_heavy = hf.n_ov_heavy;
     p->max_deg = hf.max_deg;
     p->nb_small = blk;
     p->nblocks = blk + hf.ov_chunks;

@@ -273,6 +273,12 @@ __global__ void __launch_bounds__(kCtaThreads, 4) k_spmm_block(const __grid_cons
     }
 }
 
+__device__ __forceinline__ float shfl_vt(float v, int src) { return __shfl_sync(0xffffffffu, v, src); }
+__device__ __forceinline__ float4 shfl_vt(float4 v, int src) {
+    return make_float4(__shfl_sync(0xffffffffu, v.x, src), __shfl_sync(0xffffffffu, v.y, src),
+                       __shfl_sync(0xffffffffu, v.z, src), __shfl_sync(0xffffffffu, v.w, src));
+}
+
 __device__ __forceinline__ void fanout_v(const Epi& e, int64_t vec_off, const float4& v) {
     fanout4(e, 4 * vec_off, v);  // vec_off counts float4 vectors
 }
@@ -348,6 +354,71 @@ __global__ void __launch_bounds__(kReduceThreads) k_ov_reduce(
             if (epi.npeer) fanout_v(epi, orow * FV + c, sum);
         }
         __syncthreads();
+    }
+}
+
+// Same level-3 merge, sized to the chunk counts (C5: median 3 chunks per oversized row, the
+// heaviest 633).  Oversized rows sit in ascending degree order, so the n_heavy rows with more
+// than kHeavyChunks chunks are the suffix: CTAs [0, n_heavy) take one of them each, heaviest
+// first, with all 256 threads; the other CTAs take 8 rows each, one warp per row.  Lane or
+// thread (g, c) sums chunks c0+g, c0+g+NG, ... of vector column c into its own accumulator in
+// chunk order; the NG group sums are then added in group order (shuffles / shared memory).
+// Every summation order is a function of the plan alone: deterministic.
+constexpr int kReduceWarps = 8;
+template <bool V4>
+__global__ void __launch_bounds__(kReduceWarps * 32) k_ov_reduce_h(
+    const float* __restrict__ ovp_f, const int32_t* __restrict__ chunk_start,
+    const int32_t* __restrict__ perm, int64_t ov_start, int64_t n_ov, int64_t n_heavy,
+    float* __restrict__ Y_f, int32_t FV, const int32_t* __restrict__ srp, const Epi epi) {
+    using VT = typename VecT<V4>::T;
+    const VT* ovp = reinterpret_cast<const VT*>(ovp_f);
+    VT* Y = reinterpret_cast<VT*>(Y_f);
+    const bool cta = blockIdx.x < n_heavy;
+    const int nthr = cta ? kReduceWarps * 32 : 32;
+    const int t = cta ? threadIdx.x : (threadIdx.x & 31);
+    const int64_t k = cta ? n_ov - 1 - blockIdx.x
+                          : (int64_t)(blockIdx.x - n_heavy) * kReduceWarps + (threadIdx.x >> 5);
+    if (!cta && k >= n_ov - n_heavy) return;   // whole warps only: no CTA barrier below
+    __shared__ VT part[kReduceWarps * 32];
+    const int32_t c0 = chunk_start[k], c1 = chunk_start[k + 1];
+    const int64_t orow = perm[ov_start + k];
+    const int FVc = FV < nthr ? FV : nthr;   // vector columns per pass
+    const int NG = nthr / FVc;               // chunk groups
+    const int g = t / FVc, cl = t - g * FVc;
+    for (int32_t cb = 0; cb < FV; cb += FVc) {
+        const int32_t c = cb + cl;
+        VT acc;
+        vzero(acc);
+        if (g < NG && c < FV) {
+            int32_t j = c0 + g;
+            for (; j + 3 * NG < c1; j += 4 * NG) {
+                const VT x0 = ovp[(int64_t)j * FV + c], x1 = ovp[(int64_t)(j + NG) * FV + c];
+                const VT x2 = ovp[(int64_t)(j + 2 * NG) * FV + c], x3 = ovp[(int64_t)(j + 3 * NG) * FV + c];
+                vadd(acc, x0);
+                vadd(acc, x1);
+                vadd(acc, x2);
+                vadd(acc, x3);
+            }
+            for (; j < c1; j += NG) vadd(acc, ovp[(int64_t)j * FV + c]);
+        }
+        if (cta) {
+            part[t] = acc;
+            __syncthreads();
+            if (g == 0) {
+                for (int gg = 1; gg < NG; ++gg) vadd(acc, part[gg * FVc + cl]);
+            }
+            __syncthreads();
+        } else {
+            for (int gg = 1; gg < NG; ++gg) {  // group 0 adds groups 1.. in order
+                const VT o = shfl_vt(acc, cl + gg * FVc);
+                if (g == 0) vadd(acc, o);
+            }
+        }
+        if (g == 0 && c < FV) {
+            if (epi.active()) acc = epi_v(acc, srp[ov_start + k + 1] - srp[ov_start + k], orow, c, epi);
+            sty(Y + orow * FV + c, acc);
+            if (epi.npeer) fanout_v(epi, orow * FV + c, acc);
+        }
     }
 }
 
@@ -658,7 +729,16 @@ void spmm_launch(agcn_plan_s* p, const float* vals, const float* X, int32_t F, f
         const unsigned grid = (unsigned)p->n_ov;
         const float* part = blocked ? p->sched.partial : p->ov_partial;
         const int32_t* slots = blocked ? p->sched.slot_base : p->ov_chunk_start;
-        if (v4)
+        static const int red = env_int("AGCN_OV_REDUCE", 1);  // 1: sized (default), 0: CTA per row
+        const int64_t nh = p->n_ov_heavy;
+        const unsigned hgrid = (unsigned)(nh + (p->n_ov - nh + kReduceWarps - 1) / kReduceWarps);
+        if (red && v4)
+            k_ov_reduce_h<true><<<hgrid, kReduceWarps * 32, 0, s>>>(part, slots, p->perm, p->ov_start, p->n_ov,
+                                                                   nh, Y, FV, p->sorted_rowptr, epi);
+        else if (red)
+            k_ov_reduce_h<false><<<hgrid, kReduceWarps * 32, 0, s>>>(part, slots, p->perm, p->ov_start,
+                                                                    p->n_ov, nh, Y, FV, p->sorted_rowptr, epi);
+        else if (v4)
             k_ov_reduce<true><<<grid, kReduceThreads, 0, s>>>(part, slots, p->perm, p->ov_start, Y, FV,
                                                               p->sorted_rowptr, epi);
         else
