@@ -41,7 +41,8 @@ def parse():
     ap.add_argument("--layers", type=int, default=None)
     ap.add_argument("--partition", choices=["block", "warp"], default="block")
     ap.add_argument("--kernel", choices=["auto", "general", "looped", "wide", "pipe"], default="auto")
-    ap.add_argument("--mbw", type=int, default=12, help="Alg. 1 max_block_warps (P:318; paper: 12)")
+    ap.add_argument("--mbw", type=int, default=12, help="Alg. 1 max_block_warps (P:318; paper: 12; "
+                    "0 with --mwn 0: agcn_auto_partition's per-graph choice)")
     ap.add_argument("--mwn", type=int, default=32, help="Alg. 1 max_warp_nzs (P:318; SPEC default 32)")
     ap.add_argument("--l2-hint", type=int, default=None, help="None: auto; 0: never; 1: always")
     ap.add_argument("--col-block-mb", type=int, default=None,
@@ -369,7 +370,9 @@ def main():
                        "aggregation": args.aggregation, "gin_eps": args.gin_eps, "bias_relu": args.bias_relu,
                        "allgather": ("fused (SpMM epilogue peer stores)" if fused else
                                      f"{args.dist_backend} all_gather_into_tensor") if P > 1 else None, "parallelism": f"row-shard{P}",
-                       "max_block_warps": args.mbw, "max_warp_nzs": args.mwn,
+                       "max_block_warps": st_plan["max_block_warps"], "max_warp_nzs": st_plan["max_warp_nzs"],
+                       "partition_params": "auto (agcn_auto_partition)" if args.mbw == 0 and args.mwn == 0
+                                           else "given",
                        "l2": "inputs larger than L2 (CSR + X > 126 MB)" if
                              (8 * nnz + 4 * n * F) > 126e6 else "inputs fit in L2 (warm)",
                        "step": "agcn_plan + layers x agcn_spmm (+ all-gather if N>1)"},

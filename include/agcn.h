@@ -51,7 +51,9 @@ typedef enum {
 
 typedef struct {
     int32_t max_block_warps;   /* Alg. 1 max_block_warps; default 12 */
-    int32_t max_warp_nzs;      /* Alg. 1 max_warp_nzs; default 32 */
+    int32_t max_warp_nzs;      /* Alg. 1 max_warp_nzs; default 32.
+                                  Both 0: chosen from n and nnz (measured rule, DESIGN.md 9;
+                                  agcn_plan_stats reports the values used) */
     int32_t partition;         /* agcn_partition_t; default AGCN_PARTITION_BLOCK */
     int32_t validate;          /* 1 (default): check the CSR on device -> AGCN_ERR_BAD_CSR */
     int64_t n_cols;            /* columns of A (rows of X); 0 -> n */
@@ -194,6 +196,17 @@ agcn_status_t agcn_spmm_ex(agcn_plan_t plan, const float* vals, const float* X, 
    and after the most recent agcn_spmm issued on another stream); never synchronises the host.
    Work on further streams must be ordered by the caller.  NULL is a no-op. */
 agcn_status_t agcn_plan_destroy(agcn_plan_t plan);
+
+/*
+ * The Alg. 1 parameters agcn_plan_ex uses when opts.max_block_warps == opts.max_warp_nzs == 0:
+ * a host-only rule in n, nnz and the SM count (sms <= 0: the current device's), measured on
+ * B200 (profiles/r01at_auto_partition.md).  With share = nnz / (sms * 24):
+ * share < 8 -> (12, 32); nnz >= 256 n -> (24, 32); share < 960 -> (4, 16), (8, 16) or (8, 32)
+ * for share / 2.5 below 128, below 256, at least 256; else (12, 32).  Never fails for
+ * n, nnz >= 0 and non-NULL outputs (else AGCN_ERR_INVALID_ARG).
+ */
+agcn_status_t agcn_auto_partition(int64_t n, int64_t nnz, int32_t sms, int32_t* max_block_warps,
+                                  int32_t* max_warp_nzs);
 
 /* Plan statistics (host struct, filled without device synchronisation). */
 agcn_status_t agcn_plan_stats(agcn_plan_t plan, agcn_plan_stats_t* out);

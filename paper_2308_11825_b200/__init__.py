@@ -335,6 +335,14 @@ def ipc_close(ptr: int):
     _check(_lib.lib().agcn_ipc_close(ptr))
 
 
+def auto_partition(n: int, nnz: int, sms: int = 0) -> tuple[int, int]:
+    """agcn_auto_partition: the (max_block_warps, max_warp_nzs) a plan built with (0, 0) uses
+    (host-only rule; sms <= 0 means the current device's SM count)."""
+    mbw, mwn = ctypes.c_int32(0), ctypes.c_int32(0)
+    _check(_lib.lib().agcn_auto_partition(int(n), int(nnz), int(sms), ctypes.byref(mbw), ctypes.byref(mwn)))
+    return mbw.value, mwn.value
+
+
 def shard_bounds(rowptr, nranks: int, stream=None) -> np.ndarray:
     """agcn_shard_bounds: nnz-balanced row shard bounds (int64 [nranks+1])."""
     rp = _dev_ptr(rowptr, "int32", "rowptr")

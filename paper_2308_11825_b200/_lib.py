@@ -72,6 +72,8 @@ def lib():
     L.agcn_plan_stats.restype = c_i32
     L.agcn_plan_copy.argtypes = [c_vp, c_i32, c_vp, c_size]
     L.agcn_plan_copy.restype = c_i32
+    L.agcn_auto_partition.argtypes = [c_i64, c_i64, c_i32, ctypes.POINTER(c_i32), ctypes.POINTER(c_i32)]
+    L.agcn_auto_partition.restype = c_i32
     L.agcn_shard_bounds.argtypes = [c_vp, c_i64, c_i32, ctypes.POINTER(c_i64), c_vp]
     L.agcn_shard_bounds.restype = c_i32
     L.agcn_propagate_host.argtypes = [c_vp, c_vp, c_vp, c_i64, c_i64, c_vp, c_i32, c_i32, c_vp,
@@ -107,6 +109,6 @@ def lib():
 
 EXPORTS = ["agcn_default_opts", "agcn_plan", "agcn_plan_ex", "agcn_spmm", "agcn_default_spmm_opts",
            "agcn_spmm_ex", "agcn_plan_destroy",
-           "agcn_plan_stats", "agcn_plan_copy", "agcn_shard_bounds", "agcn_propagate_host",
+           "agcn_plan_stats", "agcn_plan_copy", "agcn_auto_partition", "agcn_shard_bounds", "agcn_propagate_host",
            "agcn_transpose", "agcn_gather_vals", "agcn_gemm_xw", "agcn_device_alloc", "agcn_device_free", "agcn_ipc_export",
            "agcn_ipc_open", "agcn_ipc_close", "agcn_last_status", "agcn_last_error", "agcn_launch_count", "agcn_version"]

@@ -33,6 +33,7 @@ agcn_status_t cuda_status(cudaError_t e) {
 agcn_plan_s* build_plan(const int32_t* rowptr, const int32_t* colidx, int64_t n, int64_t nnz,
                         const agcn_opts_t& o);
 void free_plan_arrays(agcn_plan_s* p);
+void auto_partition(int64_t n, int64_t nnz, int32_t sms, int32_t* mbw, int32_t* mwn);
 void plan_copy_sorted_colidx(agcn_plan_s* p, int32_t* host_dst);
 
 namespace {
@@ -218,6 +219,15 @@ agcn_status_t agcn_plan_copy(agcn_plan_t plan, int32_t field, void* host_dst, si
             return;
         }
         if (want) AGCN_CUDA(cudaMemcpy(host_dst, src, want, cudaMemcpyDeviceToHost));
+    });
+}
+
+agcn_status_t agcn_auto_partition(int64_t n, int64_t nnz, int32_t sms, int32_t* max_block_warps,
+                                  int32_t* max_warp_nzs) {
+    return guarded([&] {
+        AGCN_CHECK(n >= 0 && nnz >= 0 && max_block_warps && max_warp_nzs, AGCN_ERR_INVALID_ARG,
+                   "n, nnz must be >= 0 and the outputs non-NULL");
+        auto_partition(n, nnz, sms, max_block_warps, max_warp_nzs);
     });
 }
 

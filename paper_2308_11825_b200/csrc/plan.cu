@@ -37,7 +37,6 @@ __device__ __forceinline__ int32_t row_key(const int32_t* rowptr, int64_t i, int
 __global__ void __launch_bounds__(kThreads) k_deg_hist(const int32_t* __restrict__ rowptr, int64_t n,
                                                       int32_t db, int32_t nbins, int64_t ntiles,
                                                       int32_t* __restrict__ table,
-                                                      int32_t* __restrict__ bin_cnt,
                                                       PlanFlags* __restrict__ flags) {
     extern __shared__ int32_t hist[];
     for (int b = threadIdx.x; b < nbins; b += kThreads) hist[b] = 0;
@@ -50,7 +49,11 @@ __global__ void __launch_bounds__(kThreads) k_deg_hist(const int32_t* __restrict
         int32_t d = rowptr[i + 1] - rowptr[i];
         if (d < 0) bad = 1;
         int32_t key = d <= 0 ? 0 : (d <= db ? d : db + 1);
-        atomicAdd(&hist[key], 1);
+        // power-law degrees: most lanes of a warp share a few keys (C5: 54 % degree 0) ->
+        // one shared-memory atomic per distinct key per warp
+        const unsigned act = __activemask();
+        const unsigned same = __match_any_sync(act, key);
+        if ((threadIdx.x & 31) == __ffs(same) - 1) atomicAdd(&hist[key], __popc(same));
         maxd = max(maxd, d);
         if (d > db) ovc += (d + db - 1) / db;
         if (d > db && d >= kColBlockMinDeg) ovh += (d + db - 1) / db;
@@ -76,10 +79,16 @@ __global__ void __launch_bounds__(kThreads) k_deg_hist(const int32_t* __restrict
         flags->rowptr_last = rowptr[n];
     }
     __syncthreads();
-    for (int b = threadIdx.x; b < nbins; b += kThreads) {
-        int32_t c = hist[b];
-        table[(int64_t)b * ntiles + blockIdx.x] = c;
-        if (c) atomicAdd(&bin_cnt[b], c);
+    for (int b = threadIdx.x; b < nbins; b += kThreads) table[(int64_t)b * ntiles + blockIdx.x] = hist[b];
+}
+
+// Bucket totals from the exclusive-scanned (bucket-major) tile table.
+__global__ void k_bin_totals(const int32_t* __restrict__ table, int64_t ntiles, int32_t nbins, int64_t n,
+                             int32_t* __restrict__ bin_cnt) {
+    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b < nbins) {
+        const int64_t hi = b + 1 < nbins ? table[(int64_t)(b + 1) * ntiles] : n;
+        bin_cnt[b] = (int32_t)(hi - table[(int64_t)b * ntiles]);
     }
 }
 
@@ -473,16 +482,17 @@ void build_block_plan(agcn_plan_s* p, const int32_t* rowptr, const int32_t* coli
     int32_t* bin_cnt = tmp.alloc<int32_t>(nbins);
     int32_t* table = tmp.alloc<int32_t>((size_t)nbins * ntiles + 1);
     AGCN_CUDA(cudaMemsetAsync(d_flags, 0, sizeof(PlanFlags), s));
-    AGCN_CUDA(cudaMemsetAsync(bin_cnt, 0, sizeof(int32_t) * nbins, s));
 
     // colidx validation on a second stream, overlapping the histogram and scan below
     Overlap ov(s, o.validate && nnz > 0 ? aux_stream(p->device) : nullptr);
     if (o.validate) validate_cols(rowptr, colidx, nnz, p->n_cols, d_flags, ov.side ? ov.side : s);
     // (1)+(2a) per-tile bucket histograms, bucket totals, max degree, rowptr validation
     k_deg_hist<<<(unsigned)ntiles, kThreads, nbins * sizeof(int32_t), s>>>(rowptr, n, db, nbins, ntiles,
-                                                                         table, bin_cnt, d_flags);
+                                                                         table, d_flags);
     post_launch();
     exclusive_scan_i32(table, table, (int64_t)nbins * ntiles, s);
+    k_bin_totals<<<(nbins + 255) / 256, 256, 0, s>>>(table, ntiles, nbins, n, bin_cnt);
+    post_launch();
     ov.finish();
 
     std::vector<int32_t> h_cnt(nbins);
@@ -673,8 +683,43 @@ static void keep_pool_cached(int dev) {
     done[dev] = true;
 }
 
+// Alg. 1 parameters chosen from the graph's size when the caller passes (0, 0).  The paper
+// fixes max_block_warps = 12 only for its storage example and never states
+// max_warp_nzs (Q18); the rule below is the B200 measurement of
+// profiles/r01at_auto_partition.md, in terms of share = nnz per resident warp of the default
+// SpMM kernel (SMs x 24):
+//   * share < 8 (tiny graphs, launch-bound):          (12, 32) -- the paper's values
+//   * mean degree >= 256 (dense hubs, Reddit-shaped):  (24, 32) -- deg_bound 768, rows stay whole
+//   * share < 960 (small graphs):  deg_bound = largest of 64/128/256 <= max(64, share / 2.5) --
+//     oversized-row chunks short against a warp's share, so the chunk tail (processed last,
+//     degree order ascending) does not set the critical path: (4,16) / (8,16) / (8,32)
+//   * otherwise:                                       (12, 32)
+void auto_partition(int64_t n, int64_t nnz, int32_t sms, int32_t* mbw, int32_t* mwn) {
+    if (sms <= 0) {
+        int dev = 0;
+        sms = 148;
+        if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    }
+    const double share = (double)nnz / ((double)sms * 24.0);
+    *mbw = 12;
+    *mwn = 32;
+    if (share < 8) return;
+    if (n > 0 && nnz >= 256 * n) {
+        *mbw = 24;
+        return;
+    }
+    if (share < 960) {
+        const double t = share / 2.5;
+        if (t >= 256) { *mbw = 8; *mwn = 32; }
+        else if (t >= 128) { *mbw = 8; *mwn = 16; }
+        else { *mbw = 4; *mwn = 16; }
+    }
+}
+
 agcn_plan_s* build_plan(const int32_t* rowptr, const int32_t* colidx, int64_t n, int64_t nnz,
-                        const agcn_opts_t& o) {
+                        const agcn_opts_t& oin) {
+    agcn_opts_t o = oin;
+    if (o.max_block_warps == 0 && o.max_warp_nzs == 0) auto_partition(n, nnz, 0, &o.max_block_warps, &o.max_warp_nzs);
     AGCN_CHECK(n >= 0 && nnz >= 0, AGCN_ERR_INVALID_ARG, "n and nnz must be >= 0");
     AGCN_CHECK(nnz < (1ll << 31) && n < (1ll << 31) - 1, AGCN_ERR_INVALID_ARG, "n, nnz must be < 2^31");
     AGCN_CHECK(rowptr != nullptr, AGCN_ERR_INVALID_ARG, "rowptr is NULL");

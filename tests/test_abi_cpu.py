@@ -69,6 +69,28 @@ def test_argument_errors_without_device():
     assert L.agcn_plan_destroy(None) == 0
 
 
+def test_auto_partition_rule():
+    """agcn_auto_partition (host-only): the per-graph Alg. 1 parameters of DESIGN.md 9 at the
+    five BASELINE configs on a 148-SM B200, the rule's branch edges, and argument errors."""
+    import paper_2308_11825_b200 as A
+    from paper_2308_11825_b200 import _lib
+    cfg = {"c1": (2708, 10556, (12, 32)), "c2": (19717, 88648, (4, 16)),
+           "c3": (169343, 1166243, (8, 16)), "c4": (232965, 114615891, (24, 32)),
+           "c5": (8388608, 134217728, (12, 32))}
+    for name, (n, nnz, want) in cfg.items():
+        assert A.auto_partition(n, nnz, 148) == want, name
+    slots = 148 * 24
+    assert A.auto_partition(10 ** 6, 8 * slots - 1, 148) == (12, 32)     # launch-bound: paper's
+    assert A.auto_partition(10 ** 6, 8 * slots, 148) == (4, 16)
+    assert A.auto_partition(10 ** 6, 320 * slots, 148) == (8, 16)        # share / 2.5 = 128
+    assert A.auto_partition(10 ** 6, 640 * slots, 148) == (8, 32)        # share / 2.5 = 256
+    assert A.auto_partition(10 ** 6, 960 * slots, 148) == (12, 32)
+    assert A.auto_partition(1000, 256 * 1000, 148) == (24, 32)            # mean degree 256
+    assert A.auto_partition(0, 0, 148) == (12, 32)
+    L = _lib.lib()
+    assert L.agcn_auto_partition(-1, 0, 148, None, None) == 1
+
+
 def test_product_package_does_not_import_oracle():
     pkg = os.path.join(ROOT, "paper_2308_11825_b200")
     for dirpath, _, files in os.walk(pkg):

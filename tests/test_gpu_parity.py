@@ -105,6 +105,34 @@ def test_metadata_edge_cases(degs):
     check_spmm(p, rowptr, colidx, vals, X)
 
 
+@pytest.mark.parametrize("F", [37, 132, 1040])
+def test_oversized_merge_shapes(F):
+    """The level-3 merge of oversized rows at column counts that need several passes: rows of
+    few chunks (one warp each) and rows of more than 16 chunks (one CTA each), F/4 or F
+    vector columns above 32 and above 256."""
+    rowptr, colidx = _rows_csr(np.array([5, 9, 40, 3, 200, 0, 17, 64, 1]), 300, F)
+    rng = np.random.default_rng(F)
+    vals = rng.uniform(-1, 1, colidx.size).astype(np.float32)
+    X = rng.uniform(-1, 1, (300, F)).astype(np.float32)
+    for mbw, mwn in [(2, 2), (1, 1), (12, 32)]:
+        p = make_plan(rowptr, colidx, max_block_warps=mbw, max_warp_nzs=mwn, n_cols=300)
+        check_spmm(p, rowptr, colidx, vals, X)
+
+
+@pytest.mark.parametrize("name", ["c1", "c2", "c3"])
+def test_auto_partition_plans(name):
+    """max_block_warps = max_warp_nzs = 0: the plan takes agcn_auto_partition's parameters,
+    reports them in its stats, and its metadata and SpMM match the oracle at those values."""
+    w = gen.make_config(name, vals_kind="uniform")
+    p = make_plan(w.rowptr, w.colidx, max_block_warps=0, max_warp_nzs=0)
+    st = p.stats()
+    mbw, mwn = A.auto_partition(w.n, w.rowptr[-1])
+    assert (st["max_block_warps"], st["max_warp_nzs"]) == (mbw, mwn)
+    check_plan_vs_oracle(w.rowptr, w.colidx, mbw, mwn)
+    for F in (16, 64, 128):
+        check_spmm(p, w.rowptr, w.colidx, w.vals, w.X(F))
+
+
 def test_empty_plans():
     for rowptr in (np.zeros(1, np.int32), np.zeros(5, np.int32)):
         p = make_plan(rowptr, np.zeros(0, np.int32), n_cols=3)
