@@ -236,6 +236,35 @@ agcn_status_t agcn_propagate_host(const int32_t* rowptr_host, const int32_t* col
                                   const agcn_opts_t* opts);
 
 /*
+ * Pipelined executor of agcn_propagate_host jobs (the serving path): job k's host->device
+ * copies run while job k-1's result is copied back, so the PCIe link carries both directions
+ * at once.  Each job computes exactly what agcn_propagate_host computes (same plan, same
+ * kernels, bit-identical Y): copy the CSR + X in, agcn_plan (degree sort + Alg. 1/2, P:295,
+ * P:314-382), `layers` x agcn_spmm, copy Y out.
+ *
+ * agcn_pipe_create: `depth` (>= 1, default 2 when <= 0) device buffer sets, reused round-robin;
+ *   opts as for agcn_plan_ex (NULL = defaults; opts->stream is ignored: the executor owns one
+ *   copy-in, one compute and one copy-out stream on the current device).  NULL on failure.
+ * agcn_pipe_submit: enqueue one job on HOST buffers (as agcn_propagate_host: rowptr[n+1],
+ *   colidx / vals indexed by rowptr values, X [n_cols x F], Y [n x F]; n_cols = opts->n_cols
+ *   or n).  Returns once the job's inputs are on the device and its plan is built (the plan
+ *   reads its bucket counts back); the SpMM and the copy of Y run asynchronously.  The caller
+ *   keeps every host buffer of the job alive and unmodified, and reads Y_host only after
+ *   agcn_pipe_wait.  Host buffers should be pinned (page-locked): pageable memory works but
+ *   the copies then do not overlap.  A failed submit leaves the executor usable.
+ * agcn_pipe_wait: blocks until every submitted job has finished (Y_host written); returns the
+ *   first asynchronous CUDA error, if any.
+ * agcn_pipe_destroy: waits, then frees the device buffers and streams.  NULL is a no-op.
+ */
+typedef struct agcn_pipe_s* agcn_pipe_t;
+agcn_pipe_t   agcn_pipe_create(int32_t depth, const agcn_opts_t* opts);
+agcn_status_t agcn_pipe_submit(agcn_pipe_t pipe, const int32_t* rowptr_host, const int32_t* colidx_host,
+                               const float* vals_host, int64_t n, int64_t nnz, const float* X_host,
+                               int32_t F, int32_t layers, float* Y_host);
+agcn_status_t agcn_pipe_wait(agcn_pipe_t pipe);
+agcn_status_t agcn_pipe_destroy(agcn_pipe_t pipe);
+
+/*
  * CSR of A^T on the device, for the backward pass of a GCN layer (dX = A^T . dY).  A stable
  * counting sort of the nonzeros by column (the degree sort's machinery): row j of A^T
  * lists the rows i with a_ij != 0 in increasing i.

@@ -17,7 +17,7 @@ import numpy as np
 from . import _lib
 from ._lib import FIELDS, STATUS
 
-__all__ = ["Plan", "AgcnError", "agcn_plan", "agcn_spmm", "agcn_spmm_ex", "transpose", "gather_vals", "gemm_xw", "DeviceBuffer", "ipc_open", "ipc_close", "shard_bounds", "propagate_host",
+__all__ = ["Plan", "AgcnError", "agcn_plan", "agcn_spmm", "agcn_spmm_ex", "transpose", "gather_vals", "gemm_xw", "DeviceBuffer", "ipc_open", "ipc_close", "shard_bounds", "propagate_host", "Pipeline",
            "launch_count", "version", "library_path"]
 
 
@@ -388,3 +388,63 @@ def propagate_host(rowptr, colidx, vals, X, layers: int = 1, out=None, *, max_bl
                                  _host_ptr(X, np.float32), int(F), int(layers),
                                  _host_ptr(out, np.float32), ctypes.byref(opts)))
     return out
+
+
+class Pipeline:
+    """agcn_pipe_*: pipelined executor of propagate_host jobs (copy-in of job k overlaps the
+    copy-out of job k-1 on the full-duplex PCIe link; results identical to propagate_host).
+
+    submit() returns once the job's inputs are on the device and its plan is built; the host
+    arrays of every submitted job are kept referenced here until wait() (the caller must not
+    modify them, nor read `out`, before wait()).  Pinned host memory gives the overlap."""
+
+    def __init__(self, depth: int = 2, *, n_cols: int = 0, max_block_warps=12, max_warp_nzs=32,
+                 partition="block"):
+        L = _lib.lib()
+        opts = _lib.Opts()
+        L.agcn_default_opts(ctypes.byref(opts))
+        opts.max_block_warps, opts.max_warp_nzs = max_block_warps, max_warp_nzs
+        opts.partition = {"block": 0, "warp": 1}[partition]
+        opts.n_cols = int(n_cols)
+        h = L.agcn_pipe_create(int(depth), ctypes.byref(opts))
+        if not h:
+            _raise_last()
+        self._h = h
+        self._keep = []
+
+    def submit(self, rowptr, colidx, vals, X, layers: int = 1, out=None):
+        n = (rowptr.shape[0] if hasattr(rowptr, "shape") else len(rowptr)) - 1
+        nnz = int(rowptr[-1]) - int(rowptr[0])
+        F = X.shape[1]
+        if out is None:
+            out = np.empty((n, F), dtype=np.float32)
+        args = (rowptr, colidx, vals, X, out)
+        _check(_lib.lib().agcn_pipe_submit(self._h, _host_ptr(rowptr, np.int32),
+                                           _host_ptr(colidx, np.int32) or None,
+                                           _host_ptr(vals, np.float32) or None, n, nnz,
+                                           _host_ptr(X, np.float32), int(F), int(layers),
+                                           _host_ptr(out, np.float32)))
+        self._keep.append(args)
+        return out
+
+    def wait(self):
+        _check(_lib.lib().agcn_pipe_wait(self._h))
+        self._keep.clear()
+
+    def close(self):
+        if self._h:
+            h, self._h = self._h, None
+            _check(_lib.lib().agcn_pipe_destroy(h))
+            self._keep.clear()
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -55,24 +55,6 @@ __global__ void k_shard_bounds(const int32_t* __restrict__ rowptr, int64_t n, in
     out[p] = lo;
 }
 
-template <class F>
-agcn_status_t guarded(F&& f) {
-    try {
-        clear_error();
-        f();
-        return AGCN_OK;
-    } catch (const Error& e) {
-        set_error(e.code, e.msg);
-        return e.code;
-    } catch (const std::bad_alloc&) {
-        set_error(AGCN_ERR_OOM, "host allocation failed");
-        return AGCN_ERR_OOM;
-    } catch (...) {
-        set_error(AGCN_ERR_CUDA, "unknown exception");
-        return AGCN_ERR_CUDA;
-    }
-}
-
 bool ranges_overlap(const void* a, size_t na, const void* b, size_t nb) {
     auto x = reinterpret_cast<uintptr_t>(a), y = reinterpret_cast<uintptr_t>(b);
     return x < y + nb && y < x + na;

@@ -5,6 +5,7 @@
 #include <stdint.h>
 
 #include <atomic>
+#include <new>
 #include <string>
 #include <vector>
 
@@ -37,6 +38,30 @@ struct Error {
     do {                                                             \
         if (!(cond)) throw ::agcn::Error{(code), std::string(msg)};  \
     } while (0)
+
+// run f() behind the C ABI: exceptions become a status code + the thread's error message
+template <class F>
+agcn_status_t guarded(F&& f) {
+    try {
+        clear_error();
+        f();
+        return AGCN_OK;
+    } catch (const Error& e) {
+        set_error(e.code, e.msg);
+        return e.code;
+    } catch (const std::bad_alloc&) {
+        set_error(AGCN_ERR_OOM, "host allocation failed");
+        return AGCN_ERR_OOM;
+    } catch (...) {
+        set_error(AGCN_ERR_CUDA, "unknown exception");
+        return AGCN_ERR_CUDA;
+    }
+}
+
+// plan construction / release (plan.cu)
+agcn_plan_s* build_plan(const int32_t* rowptr, const int32_t* colidx, int64_t n, int64_t nnz,
+                        const agcn_opts_t& o);
+void free_plan_arrays(agcn_plan_s* p);
 
 // ------------------------------------------------------------------ launch accounting
 extern std::atomic<uint64_t> g_launches;

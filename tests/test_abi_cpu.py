@@ -67,6 +67,9 @@ def test_argument_errors_without_device():
     assert L.agcn_last_status() == 5                               # AGCN_ERR_OVERFLOW
     assert L.agcn_spmm(None, None, None, 4, None, None) == 1
     assert L.agcn_plan_destroy(None) == 0
+    assert L.agcn_pipe_submit(None, None, None, None, 4, 3, None, 4, 1, None) == 1
+    assert L.agcn_pipe_wait(None) == 1
+    assert L.agcn_pipe_destroy(None) == 0
 
 
 def test_auto_partition_rule():

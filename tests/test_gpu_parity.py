@@ -527,3 +527,47 @@ def test_gemm_xw_tcgen05_tf32(M, K, N, epi):
     err = np.abs(Y - ref)
     assert np.all(err <= 2.0 ** -9 * mag + 1e-6), float((err / (2.0 ** -9 * mag + 1e-6)).max())
     assert err.mean() > 1e-7 or M * N < 100            # it really is TF32 (not an fp32 fallback)
+
+
+def test_pipeline_matches_propagate_host():
+    """agcn_pipe_*: interleaved jobs of different graphs, widths and layer counts through a
+    depth-2 executor (slots reused, buffers grown) give exactly propagate_host's Y, and the
+    single-layer jobs pass the oracle check."""
+    jobs = []
+    for name, F, layers in (("c1", 16, 2), ("c2", 64, 1), ("c3", 32, 2), ("c1", 8, 1),
+                            ("c2", 128, 2), ("c3", 64, 1), ("c1", 16, 1)):
+        w = gen.make_config(name)
+        jobs.append((w, w.X(F), layers))
+    pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()  # noqa: E731
+    with A.Pipeline(depth=2) as pipe:
+        outs = []
+        for w, X, layers in jobs:
+            Y = torch.empty((w.n, X.shape[1]), dtype=torch.float32).pin_memory()
+            pipe.submit(pin(w.rowptr), pin(w.colidx), pin(w.vals), pin(X), layers, out=Y)
+            outs.append(Y)
+        pipe.wait()
+    for (w, X, layers), Y in zip(jobs, outs):
+        ref = A.propagate_host(w.rowptr, w.colidx, w.vals, X, layers)
+        assert np.array_equal(Y.numpy(), ref)
+        if layers == 1:
+            assert oracle.spmm_check(w.rowptr, w.colidx, w.vals, X, Y.numpy())["nfail"] == 0
+
+
+def test_pipeline_error_leaves_executor_usable():
+    w = gen.make_config("c1")
+    X = w.X(16)
+    pipe = A.Pipeline(depth=1)
+    bad = w.colidx.copy()
+    bad[5] = w.n + 3                                   # column out of range: plan rejects it
+    with pytest.raises(A.AgcnError) as e:
+        pipe.submit(w.rowptr, bad, w.vals, X, 1)
+    assert e.value.status == "AGCN_ERR_BAD_CSR"
+    from paper_2308_11825_b200 import _lib
+    Yb = np.empty((w.n, 16), np.float32)               # rowptr[n] - rowptr[0] != nnz
+    assert _lib.lib().agcn_pipe_submit(pipe._h, w.rowptr.ctypes.data, w.colidx.ctypes.data,
+                                       w.vals.ctypes.data, w.n, w.nnz + 1, X.ctypes.data, 16, 1,
+                                       Yb.ctypes.data) == 2
+    Y = pipe.submit(w.rowptr, w.colidx, w.vals, X, 1)
+    pipe.wait()
+    pipe.close()
+    assert np.array_equal(Y, A.propagate_host(w.rowptr, w.colidx, w.vals, X, 1))
