@@ -94,6 +94,7 @@ struct WideArgs {
     float* piece_partial; // [pieces][F] partial rows (slot-indexed)
     int64_t piece_cap;    // upper bound of the piece count (grid sizing)
     Epi epi;              // output epilogue (EPI)
+    int32_t L;            // lanes per X row (F / 8); used when the kernel's LT is 0
 };
 
 // a finished output row slice of 8 floats at column c of original row orow (degree deg)
@@ -113,13 +114,18 @@ __device__ __forceinline__ void store_row(float* Y, int64_t orow, int32_t c, int
 
 // L lanes per X row (F = 8 L), U X rows in flight per lane, MINB resident CTAs per SM
 // (register budget), KEEP: X-row loads carry an L2 evict_last hint.
-template <int L, int U, int MINB, bool KEEP, bool PIECES, bool EPI>
+// LT = 0: L is a runtime value (a.L), for the F = 8 L with L not a power of two.
+template <int LT, int U, int MINB, bool KEEP, bool PIECES, bool EPI>
 __global__ void __launch_bounds__(kThreads, MINB) k_spmm_wide(const __grid_constant__ WideArgs a) {
-    constexpr int G = 32 / L;
-    constexpr int F = 8 * L;
-    static_assert(L % U == 0, "U must divide L");
+    const int L = LT ? LT : a.L;
+    const int G = 32 / L;                     // combined warps per warp; lanes >= G L idle
+    const int F = 8 * L;
+    constexpr bool UDIV = LT && LT % U == 0;  // else the last round of a batch may be partial
+    constexpr bool FULL = LT && 32 % LT == 0; // every lane in a combined warp
+    constexpr bool POW2 = LT && (LT & (LT - 1)) == 0;
     const int lane = threadIdx.x & 31;
     const int s = lane / L, li = lane % L;
+    const bool act = FULL || s < G;           // an idle lane (s == G) only joins the shuffles
     const int32_t gw = blockIdx.x * kWarps + (threadIdx.x >> 5);
     const int32_t W = gridDim.x * kWarps;
 
@@ -131,8 +137,8 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_wide(const __grid_const
             const int32_t pr = r0 + lane < a.n_zero ? __ldg(a.perm + r0 + lane) : -1;
 #pragma unroll 4
             for (int i = 0; i < 32; i += G) {
-                const int32_t o = __shfl_sync(0xffffffffu, pr, i + s);
-                if (o >= 0) store_row<EPI>(a.Y, o, li * 8, F, 0, z, a.epi);
+                const int32_t o = __shfl_sync(0xffffffffu, pr, FULL ? i + s : (i + s) & 31);
+                if (act && (FULL || i + s < 32) && o >= 0) store_row<EPI>(a.Y, o, li * 8, F, 0, z, a.epi);
             }
         }
     }
@@ -172,7 +178,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_wide(const __grid_const
             // flushing the accumulator at every row boundary (all rows have d entries, so the
             // boundaries are warp-uniform).
             const int32_t T = ((R + G - 1) / G) * d;              // sub-warp 0's entries (bound)
-            const int32_t Ts = s < R ? ((R - s + G - 1) / G) * d : 0;
+            const int32_t Ts = act && s < R ? ((R - s + G - 1) / G) * d : 0;
             int32_t c, cn;
             float v, vn;
             auto pair = [&](int32_t t, int32_t& cc, float& vv) {  // entry t of this sub-warp
@@ -197,19 +203,20 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_wide(const __grid_const
                     f8 x[U];
 #pragma unroll
                     for (int u = 0; u < U; ++u) {
-                        const int32_t cu = __shfl_sync(0xffffffffu, c, s * L + q + u);
-                        if (q + u < nb)
+                        const int32_t cu = __shfl_sync(0xffffffffu, c, FULL ? s * L + q + u : (s * L + q + u) & 31);
+                        if (q + u < nb && (UDIV || q + u < L))
                             ld8(x[u], a.X + ((int64_t)cu * F + li * 8), KEEP ? 1 : 0);
                         else
                             x[u].a = x[u].b = make_float4(0.f, 0.f, 0.f, 0.f);
                     }
 #pragma unroll
                     for (int u = 0; u < U; ++u) {
-                        fma8(acc, __shfl_sync(0xffffffffu, v, s * L + q + u), x[u]);
+                        const float vu = __shfl_sync(0xffffffffu, v, FULL ? s * L + q + u : (s * L + q + u) & 31);
+                        fma8(acc, UDIV || q + u < L ? vu : 0.f, x[u]);
                         if (q + u < nbu && --left == 0) {         // row boundary: store, restart
                             const int32_t r = s + rowi * G;
                             const int32_t o = __shfl_sync(0xffffffffu, dst_l, min(r, 31));
-                            if (r < R) {
+                            if (act && r < R) {
                                 if (!ov)
                                     store_row<EPI>(a.Y, o, li * 8, F, d, acc, a.epi);
                                 else
@@ -235,7 +242,8 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_wide(const __grid_const
         const int32_t len_k = max(0, min(d, p0 + part) - p0);
         for (int32_t r0 = 0; r0 < R; r0 += NG) {
             const int32_t r = r0 + g;
-            const int32_t mylen = r < R ? len_k : 0;
+            const bool gact = (FULL || g < NG) && r < R;           // idle groups / lanes: no work
+            const int32_t mylen = gact ? len_k : 0;
             const int32_t e0 = __shfl_sync(0xffffffffu, rso_l, r & 31) + p0;  // first entry
             acc.a = acc.b = make_float4(0.f, 0.f, 0.f, 0.f);
             // (colidx, val) pairs, L per batch, one per lane; the next batch is prefetched
@@ -261,31 +269,49 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_wide(const __grid_const
                     f8 x[U];
 #pragma unroll
                     for (int u = 0; u < U; ++u) {
-                        const int32_t cu = __shfl_sync(0xffffffffu, c, s * L + q + u);
-                        if (q + u < nb)
+                        const int32_t cu = __shfl_sync(0xffffffffu, c, FULL ? s * L + q + u : (s * L + q + u) & 31);
+                        if (q + u < nb && (UDIV || q + u < L))
                             ld8(x[u], a.X + ((int64_t)cu * F + li * 8), KEEP ? 1 : 0);
                         else
                             x[u].a = x[u].b = make_float4(0.f, 0.f, 0.f, 0.f);
                     }
 #pragma unroll
-                    for (int u = 0; u < U; ++u) fma8(acc, __shfl_sync(0xffffffffu, v, s * L + q + u), x[u]);
+                    for (int u = 0; u < U; ++u) {
+                        const float vu = __shfl_sync(0xffffffffu, v, FULL ? s * L + q + u : (s * L + q + u) & 31);
+                        fma8(acc, UDIV || q + u < L ? vu : 0.f, x[u]);
+                    }
                 }
                 c = cn;
                 v = vn;
             }
-            // combine the K partial rows of a group (fixed xor tree: deterministic)
-            for (int o = L; o < K * L; o <<= 1) {
-                acc.a.x = shfl_xor_add(acc.a.x, o);
-                acc.a.y = shfl_xor_add(acc.a.y, o);
-                acc.a.z = shfl_xor_add(acc.a.z, o);
-                acc.a.w = shfl_xor_add(acc.a.w, o);
-                acc.b.x = shfl_xor_add(acc.b.x, o);
-                acc.b.y = shfl_xor_add(acc.b.y, o);
-                acc.b.z = shfl_xor_add(acc.b.z, o);
-                acc.b.w = shfl_xor_add(acc.b.w, o);
+            // combine the K partial rows of a group (fixed tree: deterministic).  Power-of-two
+            // L: xor butterflies; otherwise member k adds member k + o's partial (member 0
+            // ends with ((p0 + p1) + (p2 + p3)) ..., the same order as the butterfly).
+            if (POW2) {
+                for (int o = L; o < K * L; o <<= 1) {
+                    acc.a.x = shfl_xor_add(acc.a.x, o);
+                    acc.a.y = shfl_xor_add(acc.a.y, o);
+                    acc.a.z = shfl_xor_add(acc.a.z, o);
+                    acc.a.w = shfl_xor_add(acc.a.w, o);
+                    acc.b.x = shfl_xor_add(acc.b.x, o);
+                    acc.b.y = shfl_xor_add(acc.b.y, o);
+                    acc.b.z = shfl_xor_add(acc.b.z, o);
+                    acc.b.w = shfl_xor_add(acc.b.w, o);
+                }
+            } else {
+                for (int o = L; o < K * L; o <<= 1) {
+                    acc.a.x += __shfl_down_sync(0xffffffffu, acc.a.x, o);
+                    acc.a.y += __shfl_down_sync(0xffffffffu, acc.a.y, o);
+                    acc.a.z += __shfl_down_sync(0xffffffffu, acc.a.z, o);
+                    acc.a.w += __shfl_down_sync(0xffffffffu, acc.a.w, o);
+                    acc.b.x += __shfl_down_sync(0xffffffffu, acc.b.x, o);
+                    acc.b.y += __shfl_down_sync(0xffffffffu, acc.b.y, o);
+                    acc.b.z += __shfl_down_sync(0xffffffffu, acc.b.z, o);
+                    acc.b.w += __shfl_down_sync(0xffffffffu, acc.b.w, o);
+                }
             }
             const int32_t rd = __shfl_sync(0xffffffffu, dst_l, r & 31);
-            if (k == 0 && r < R) {
+            if (k == 0 && gact) {
                 if (!ov)
                     store_row<EPI>(a.Y, rd, li * 8, F, d, acc, a.epi);
                 else
@@ -304,7 +330,7 @@ void launch_t(const WideArgs& a, cudaStream_t s) {
         AGCN_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kThreads, 0));
         if (occ < 1) occ = 1;
     }
-    constexpr int G = 32 / L;
+    const int G = 32 / (L ? L : a.L);
     const int64_t work = std::max<int64_t>(a.n_desc + (a.pieces ? a.piece_cap : 0), (a.n_zero + G - 1) / G);
     const int64_t want = (work + kWarps - 1) / kWarps;
     const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)num_sms() * occ));
@@ -352,7 +378,7 @@ void launch(const WideArgs& a, bool keep, cudaStream_t s) {
 }  // namespace
 
 bool wide_supported(const agcn_plan_s* p, const float* X, const float* Y, int32_t F) {
-    const bool shape = F == 8 || F == 16 || F == 32 || F == 64 || F == 128 || F == 256;
+    const bool shape = F >= 8 && F <= 256 && F % 8 == 0;   // L = F / 8 lanes of 32 bytes per row
     const bool al = ((reinterpret_cast<uintptr_t>(X) | reinterpret_cast<uintptr_t>(Y)) & 31u) == 0;
     return shape && al && p->mbw <= 32;
 }
@@ -365,13 +391,19 @@ void launch_wide(agcn_plan_s* p, const float* vals, const float* X, int32_t F, f
                p->deg_bound, blocked ? cs.seg : nullptr, blocked ? cs.slot_base + p->n_ov : nullptr,
                blocked ? cs.partial : nullptr, blocked ? cs.cap : 0, epi};
     AGCN_CHECK(a.n_desc + a.piece_cap < (1ll << 31), AGCN_ERR_OVERFLOW, "too many descriptors");
+    a.L = F / 8;
     switch (F) {
         case 8: launch<1>(a, l2_keep, s); break;
         case 16: launch<2>(a, l2_keep, s); break;
         case 32: launch<4>(a, l2_keep, s); break;
         case 64: launch<8>(a, l2_keep, s); break;
         case 128: launch<16>(a, l2_keep, s); break;
-        default: launch<32>(a, l2_keep, s); break;
+        case 256: launch<32>(a, l2_keep, s); break;
+        default: {  // F = 8 L, L not a power of two: one kernel with L at run time
+            static const int minb = env_int("AGCN_WIDE_RT_MINB", 3);
+            minb == 2 ? launch_k<0, 4, 2>(a, l2_keep, s) : launch_k<0, 4, 3>(a, l2_keep, s);
+            break;
+        }
     }
 }
 

@@ -175,7 +175,7 @@ def test_spmm_c2_F(F):
 
 KERNEL_F = [("general", F) for F in (3, 4, 16, 64, 128, 100)] + \
     [("looped", F) for F in (1, 16, 33, 64, 100, 128)] + \
-    [("wide", F) for F in (8, 16, 32, 64, 128, 256)] + \
+    [("wide", F) for F in (8, 16, 24, 32, 40, 64, 96, 128, 200, 248, 256)] + \
     [("pipe", F) for F in (32, 64, 128, 256)]
 
 
@@ -195,7 +195,7 @@ def test_spmm_every_kernel(kernel, F):
         check_spmm(p, rowptr, colidx, vals, X, kernel=kernel)
 
 
-@pytest.mark.parametrize("F", [8, 64, 128, 256])
+@pytest.mark.parametrize("F", [8, 64, 96, 128, 256])
 def test_column_blocked_oversized_rows(F):
     """Oversized rows executed as column-blocked pieces (agcn_spmm_opts_t.col_block_mb) give
     the oracle's result; unsorted rows (plain chunks) and sorted rows mixed; deterministic."""
@@ -273,11 +273,12 @@ def test_spmm_random(seed):
     check_spmm(p, rowptr, colidx, vals, X)
 
 
-def test_spmm_integer_exact_and_deterministic():
+@pytest.mark.parametrize("F", [64, 40, 96, 200])
+def test_spmm_integer_exact_and_deterministic(F):
     rng = np.random.default_rng(5)
     rowptr, colidx = _rows_csr(np.array([0, 1, 5, 40, 384, 385, 2000, 3, 900]), 300, 5)
     vals = rng.integers(-4, 5, colidx.size).astype(np.float32)
-    X = rng.integers(-4, 5, (300, 64)).astype(np.float32)
+    X = rng.integers(-4, 5, (300, F)).astype(np.float32)
     p = make_plan(rowptr, colidx, n_cols=300)
     Y1 = p.spmm(cu(vals), cu(X)).cpu().numpy()
     Y2 = p.spmm(cu(vals), cu(X)).cpu().numpy()
@@ -417,7 +418,7 @@ EPI_CASES = [
 ]
 
 
-@pytest.mark.parametrize("kernel,F", [("auto", 64), ("wide", 128), ("general", 100), ("general", 64),
+@pytest.mark.parametrize("kernel,F", [("auto", 64), ("wide", 128), ("wide", 40), ("general", 100), ("general", 64),
                                       ("looped", 16), ("pipe", 64)])
 @pytest.mark.parametrize("case", range(len(EPI_CASES)))
 def test_spmm_epilogue(kernel, F, case):
