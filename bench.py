@@ -134,6 +134,65 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(rows)}
 
 
+class NvmlClockSampler:
+    """SM clock and clock-event reasons sampled every `period` s by NVML from a thread, only
+    while the timed region runs (start() right before it, stop() right after the closing
+    synchronize).  The nvidia-smi sampler above is the fallback when NVML is unavailable."""
+
+    BITS = {"hw_slowdown": "nvmlClocksEventReasonHwSlowdown",
+            "hw_thermal_slowdown": "nvmlClocksEventReasonHwThermalSlowdown",
+            "sw_thermal_slowdown": "nvmlClocksEventReasonSwThermalSlowdown",
+            "sw_power_cap": "nvmlClocksEventReasonSwPowerCap"}
+
+    def __init__(self, cuda_index: int, period: float = 0.005):
+        import threading
+        import pynvml as N
+        N.nvmlInit()
+        self.N, self.period, self.rows = N, period, []
+        h = None
+        try:
+            import torch
+            uuid = str(torch.cuda.get_device_properties(cuda_index).uuid)
+            h = N.nvmlDeviceGetHandleByUUID(uuid if uuid.startswith("GPU-") else "GPU-" + uuid)
+        except Exception:
+            vis = os.environ.get("CUDA_VISIBLE_DEVICES", "")
+            ids = [x for x in vis.split(",") if x.strip().isdigit()]
+            h = N.nvmlDeviceGetHandleByIndex(int(ids[cuda_index]) if cuda_index < len(ids) else cuda_index)
+        self.h = h
+        self.max_mhz = N.nvmlDeviceGetMaxClockInfo(h, N.NVML_CLOCK_SM)
+        self.bits = {k: getattr(N, v) for k, v in self.BITS.items()}
+        self.stop_ev = threading.Event()
+        self.t = threading.Thread(target=self._run, daemon=True)
+        self.t.start()
+
+    def _run(self):
+        N = self.N
+        while not self.stop_ev.is_set():
+            try:
+                mhz = N.nvmlDeviceGetClockInfo(self.h, N.NVML_CLOCK_SM)
+                rs = N.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                self.rows.append((mhz, rs))
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def stop(self):
+        self.stop_ev.set()
+        self.t.join(timeout=2)
+        if not self.rows:
+            return None
+        reasons = sorted(k for k, b in self.bits.items() if any(rs & b for _, rs in self.rows))
+        return {"sm_mhz": statistics.median(r[0] for r in self.rows), "sm_max_mhz": self.max_mhz,
+                "reasons": reasons, "samples": len(self.rows), "sampler": "nvml 5 ms, timed region only"}
+
+
+def clock_sampler(cuda_index: int):
+    try:
+        return NvmlClockSampler(cuda_index)
+    except Exception:
+        return ClockSampler(cuda_index)
+
+
 def cpu_sample_gflops(w, X, budget_s: float):
     """Time the fp64 CPU oracle (as it stands) on a bounded contiguous row sample."""
     import oracle
@@ -314,9 +373,9 @@ def main():
     torch.cuda.synchronize()
     rec = {"plan": [], "spmm": [], "ag": []}
 
-    clocks = None if args.profile else ClockSampler(local)
     barrier()
     torch.cuda.synchronize()
+    clocks = None if args.profile else clock_sampler(local)
     l0 = A.launch_count()
     t_start, t_end = ev(), ev()
     t_start.record(stream)
@@ -328,9 +387,9 @@ def main():
         plan.close()
     t_end.record(stream)
     torch.cuda.synchronize()
+    clk = clocks.stop() if clocks else None
     barrier()
     launches = A.launch_count() - l0
-    clk = clocks.stop() if clocks else None
     ms_local = t_start.elapsed_time(t_end) / args.steps
     spmm_ms = [a.elapsed_time(b) for a, b in rec["spmm"]]
     plan_ms = [a.elapsed_time(b) for a, b in rec["plan"]]
