@@ -277,6 +277,9 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_gemm_tf32_ws(const __grid_con
     uint64_t* acc_empty = bars + 2 * NS + 2;  // [2] accumulator drained (4 epilogue warps)
     uint64_t* barB = bars + 2 * NS + 4;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * NS + 5);
+    // epilogue staging: per epilogue warp 32 rows x CW columns, rows padded to CW + 4 floats
+    constexpr int CW = N < 64 ? N : 64, SP = CW + 4;
+    float* staging = reinterpret_cast<float*>(smem + NS * a_bytes + (size_t)KT * N * kBK * 4 + 128);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
     if (threadIdx.x == 0) {
@@ -355,28 +358,41 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_gemm_tf32_ws(const __grid_con
         for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
             mbar_wait(acc_full + acc, aph[acc]);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-            const int64_t row = t * kBM + quad * 32 + lane;
+            // TMEM row `lane` -> padded shared-memory rows -> coalesced row-segment stores (a
+            // lane per TMEM row would store 16 B into 32 different rows per instruction)
+            const int64_t row0 = t * kBM + quad * 32;
+            float* stg = staging + quad * 32 * SP;
 #pragma unroll 1
-            for (int c0 = 0; c0 < N; c0 += 16) {
-                float v[16];
-                tmem_ld16(tmem + acc * kAcc + ((uint32_t)(quad * 32) << 16) + (uint32_t)c0, v);
-                if (row < M) {
-                    float* dst = Y + row * N + c0;
+            for (int cb = 0; cb < N; cb += CW) {
+#pragma unroll 1
+                for (int c0 = 0; c0 < CW; c0 += 16) {
+                    float v[16];
+                    tmem_ld16(tmem + acc * kAcc + ((uint32_t)(quad * 32) << 16) + (uint32_t)(cb + c0), v);
 #pragma unroll
                     for (int i = 0; i < 16; i += 4) {
                         float4 o = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
                         if (bias) {
-                            o.x += __ldg(bias + c0 + i);
-                            o.y += __ldg(bias + c0 + i + 1);
-                            o.z += __ldg(bias + c0 + i + 2);
-                            o.w += __ldg(bias + c0 + i + 3);
+                            o.x += __ldg(bias + cb + c0 + i);
+                            o.y += __ldg(bias + cb + c0 + i + 1);
+                            o.z += __ldg(bias + cb + c0 + i + 2);
+                            o.w += __ldg(bias + cb + c0 + i + 3);
                         }
                         if (relu) {
                             o.x = fmaxf(o.x, 0.f); o.y = fmaxf(o.y, 0.f); o.z = fmaxf(o.z, 0.f); o.w = fmaxf(o.w, 0.f);
                         }
-                        __stcs(reinterpret_cast<float4*>(dst + i), o);
+                        *reinterpret_cast<float4*>(stg + lane * SP + c0 + i) = o;
                     }
                 }
+                __syncwarp();
+                constexpr int nv = CW / 4;
+#pragma unroll 4
+                for (int e = lane; e < 32 * nv; e += 32) {
+                    const int r = e / nv, c = e - r * nv;
+                    if (row0 + r < M)
+                        __stcs(reinterpret_cast<float4*>(Y + (row0 + r) * N + cb) + c,
+                               *reinterpret_cast<const float4*>(stg + r * SP + 4 * c));
+                }
+                __syncwarp();
             }
             asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
             __syncwarp();
@@ -426,7 +442,9 @@ CUtensorMap make_map(const float* base, int64_t rows, int64_t cols, uint32_t box
 template <int N, int NS>
 bool try_launch_ws(const CUtensorMap& mx, const CUtensorMap& mw, float* Y, int64_t M, int32_t KT, const float* bias,
                    int32_t relu, cudaStream_t s) {
-    const size_t smem = 1024 + (size_t)NS * KT * kBM * kBK * 4 + (size_t)KT * N * kBK * 4 + 128;
+    constexpr int CW = N < 64 ? N : 64;
+    const size_t smem = 1024 + (size_t)NS * KT * kBM * kBK * 4 + (size_t)KT * N * kBK * 4 + 128 +
+                        (size_t)4 * 32 * (CW + 4) * 4;
     if (smem > 227 * 1024) return false;
     auto kern = k_gemm_tf32_ws<N, NS>;
     AGCN_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
