@@ -259,7 +259,7 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
-template <int N, int NS>
+template <int N, int NS, int CWT>
 __global__ void __launch_bounds__(kWsThreads, 1) k_gemm_tf32_ws(const __grid_constant__ CUtensorMap tmX,
                                                                const __grid_constant__ CUtensorMap tmW,
                                                                float* __restrict__ Y, int64_t M, int32_t KT,
@@ -278,7 +278,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_gemm_tf32_ws(const __grid_con
     uint64_t* barB = bars + 2 * NS + 4;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * NS + 5);
     // epilogue staging: per epilogue warp 32 rows x CW columns, rows padded to CW + 4 floats
-    constexpr int CW = N < 64 ? N : 64, SP = CW + 4;
+    constexpr int CW = N < CWT ? N : CWT, SP = CW + 4;
     float* staging = reinterpret_cast<float*>(smem + NS * a_bytes + (size_t)KT * N * kBK * 4 + 128);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
@@ -439,14 +439,14 @@ CUtensorMap make_map(const float* base, int64_t rows, int64_t cols, uint32_t box
     return m;
 }
 
-template <int N, int NS>
+template <int N, int NS, int CWT = 64>
 bool try_launch_ws(const CUtensorMap& mx, const CUtensorMap& mw, float* Y, int64_t M, int32_t KT, const float* bias,
                    int32_t relu, cudaStream_t s) {
-    constexpr int CW = N < 64 ? N : 64;
+    constexpr int CW = N < CWT ? N : CWT;
     const size_t smem = 1024 + (size_t)NS * KT * kBM * kBK * 4 + (size_t)KT * N * kBK * 4 + 128 +
                         (size_t)4 * 32 * (CW + 4) * 4;
     if (smem > 227 * 1024) return false;
-    auto kern = k_gemm_tf32_ws<N, NS>;
+    auto kern = k_gemm_tf32_ws<N, NS, CWT>;
     AGCN_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     const int64_t ntiles = (M + kBM - 1) / kBM;
     const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(ntiles, (int64_t)num_sms()));
@@ -465,7 +465,8 @@ void launch_gemm(const CUtensorMap& mx, const CUtensorMap& mw, float* Y, int64_t
                  int32_t relu, cudaStream_t s) {
     if (gemm_variant() == 0 && (try_launch_ws<N, 4>(mx, mw, Y, M, KT, bias, relu, s) ||
                                 try_launch_ws<N, 3>(mx, mw, Y, M, KT, bias, relu, s) ||
-                                try_launch_ws<N, 2>(mx, mw, Y, M, KT, bias, relu, s)))
+                                try_launch_ws<N, 2>(mx, mw, Y, M, KT, bias, relu, s) ||
+                                try_launch_ws<N, 1, 32>(mx, mw, Y, M, KT, bias, relu, s)))
         return;
     const size_t smem = 1024 + (size_t)KT * (kBM + N) * kBK * 4 + 64;
     AGCN_CHECK(smem <= 227 * 1024, AGCN_ERR_UNSUPPORTED, "F_in x F_out too large for the tcgen05 GEMM");
