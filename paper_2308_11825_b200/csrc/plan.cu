@@ -470,6 +470,334 @@ void radix_sort_pairs(int32_t*& ka, int32_t*& va, int32_t*& kb, int32_t*& vb, in
 
 namespace {
 
+// ---------------------------------------------------------------- small graphs: one CTA
+// For n <= kSmallRows the whole block plan (steps (1)-(5) above, the same algorithm and the
+// same stable order) runs in ONE 1024-thread CTA with one host synchronisation at the end:
+// C1 / C2-sized graphs are bound by launch and synchronisation latency (~20 launches +
+// allocations + a mid-course readback in the general path), not by work.  Warp w owns rows
+// [w R, (w+1) R); the stable counting sort is per-warp histograms -> (bin, warp) offsets ->
+// match_any ranks, exactly the tile scheme of k_bucket_scatter with one tile.  Oversized rows
+// (at most kSmallOv) are ranked by (degree, row) directly.  If there are more, the kernel
+// reports it before writing anything and the general path runs instead.
+constexpr int64_t kSmallRows = 32768;
+constexpr int64_t kSmallNnz = 1 << 20;
+constexpr int32_t kSmallDb = 512;
+constexpr int32_t kSmallOv = 1024;
+constexpr int kSmallThreads = 1024;
+
+struct SmallOut {
+    int32_t fallback, bad_rowptr, bad_colidx, max_deg;
+    int32_t rowptr_first, rowptr_last, n_ov_heavy, pad;
+    int64_t nb_small, n_zero, n_ov, ov_chunks, ov_chunks_heavy;
+};
+
+// exclusive scan of v over the block (1024 threads); returns the prefix, *total the sum
+__device__ __forceinline__ int64_t block_exscan(int64_t v, int64_t* wsum, int64_t* total) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    int64_t x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int64_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) wsum[w] = x;
+    __syncthreads();
+    if (w == 0) {
+        int64_t t = wsum[lane];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int64_t y = __shfl_up_sync(0xffffffffu, t, o);
+            if (lane >= o) t += y;
+        }
+        wsum[32 + lane] = t;  // inclusive over warps
+    }
+    __syncthreads();
+    const int64_t before = (w ? wsum[32 + w - 1] : 0) + x - v;
+    *total = wsum[32 + 31];
+    __syncthreads();
+    return before;
+}
+
+__global__ void __launch_bounds__(kSmallThreads, 1)
+k_plan_small(const int32_t* __restrict__ rowptr, const int32_t* __restrict__ colidx_g, int64_t n, int64_t nnz,
+             int64_t n_cols, int32_t db, int32_t mbw, int32_t mwn, int32_t validate, int32_t* __restrict__ perm,
+             int32_t* __restrict__ srp, int32_t* __restrict__ rso, int4* __restrict__ desc,
+             int32_t* __restrict__ ov_chunk_start, SmallOut* __restrict__ out) {
+    extern __shared__ int32_t sm[];
+    const int32_t nbins = db + 2;
+    int32_t* wh = sm;                                    // [32][nbins]: counts, then offsets
+    int32_t* tot = wh + 32 * nbins;                      // [nbins]
+    int32_t* blk = tot + nbins;                          // [db + 2] first descriptor of degree d
+    int32_t* ovd = blk + db + 2;                         // [kSmallOv]
+    int32_t* ovr = ovd + kSmallOv;                       // [kSmallOv]
+    int32_t* rs = ovr + kSmallOv;                        // [nbins] first sorted row of bucket b
+    int64_t* wsum = reinterpret_cast<int64_t*>(sm + ((33 * nbins + db + 2 + 2 * kSmallOv + nbins + 1) & ~1));  // [64]
+    int16_t* keys = reinterpret_cast<int16_t*>(wsum + 64);  // [n] bucket of every row
+    __shared__ int32_t s_max, s_bad, s_badc, s_nhv;
+    __shared__ unsigned long long s_ovc, s_ovh;
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    for (int i = tid; i < 32 * nbins; i += kSmallThreads) wh[i] = 0;
+    if (tid == 0) { s_max = 0; s_bad = 0; s_badc = 0; s_nhv = 0; s_ovc = 0; s_ovh = 0; }
+    __syncthreads();
+    const int32_t base = rowptr[0];
+    const int64_t R = (n + 31) / 32, lo = w * R, hi = min(n, lo + R);
+    int32_t* hw = wh + w * nbins;
+    // (1) degrees -> bucket keys in shared memory (independent coalesced loads) + flags
+    int32_t maxd = 0, bad = 0, nhv = 0;
+    long long ovc = 0, ovh = 0;
+#pragma unroll 4
+    for (int64_t i = tid; i < n; i += kSmallThreads) {
+        const int32_t d = rowptr[i + 1] - rowptr[i];
+        keys[i] = (int16_t)(d <= 0 ? 0 : (d <= db ? d : db + 1));
+        bad |= d < 0;
+        maxd = max(maxd, d);
+        if (d > db) ovc += (d + db - 1) / db;
+        if (d > db && d >= kColBlockMinDeg) ovh += (d + db - 1) / db;
+        if ((int64_t)d > (int64_t)kHeavyChunks * db) ++nhv;
+    }
+    __syncthreads();
+    // (2a) per-warp bucket counts over the warp's row range
+    for (int64_t c0 = lo; c0 < hi; c0 += 32) {
+        const int64_t i = c0 + lane;
+        const bool valid = i < hi;
+        const int32_t key = valid ? keys[i] : -1;
+        const unsigned peers = __match_any_sync(0xffffffffu, key);
+        if (valid && lane == __ffs(peers) - 1) hw[key] += __popc(peers);
+        __syncwarp();
+    }
+    int32_t badc = 0;
+    if (validate) {
+        const int32_t* colidx = colidx_g + base;
+#pragma unroll 8
+        for (int64_t q = tid; q < nnz; q += kSmallThreads) {
+            const int32_t j = colidx[q];
+            badc |= (j < 0) | ((int64_t)j >= n_cols);
+        }
+    }
+    if (maxd) atomicMax(&s_max, maxd);
+    if (bad) s_bad = 1;
+    if (badc) s_badc = 1;
+    if (nhv) atomicAdd(&s_nhv, nhv);
+    if (ovc) atomicAdd(&s_ovc, (unsigned long long)ovc);
+    if (ovh) atomicAdd(&s_ovh, (unsigned long long)ovh);
+    __syncthreads();
+    // (2b) bucket totals, bucket starts, (bin, warp) offsets in item order
+    for (int b = tid; b < nbins; b += kSmallThreads) {
+        int32_t t = 0;
+        for (int ww = 0; ww < 32; ++ww) t += wh[ww * nbins + b];
+        tot[b] = t;
+    }
+    __syncthreads();
+    {
+        // nbins <= 514 < 1024: one bin per thread
+        const int64_t v = tid < nbins ? tot[tid] : 0;
+        int64_t all;
+        const int64_t start = block_exscan(v, wsum, &all);
+        if (tid < nbins) {
+            rs[tid] = (int32_t)start;
+            int32_t run = (int32_t)start;
+            for (int ww = 0; ww < 32; ++ww) {
+                const int32_t c = wh[ww * nbins + tid];
+                wh[ww * nbins + tid] = run;
+                run += c;
+            }
+        }
+    }
+    const int64_t n_ov = tot[db + 1], n_zero = tot[0], ov_start = n - n_ov;
+    if (n_ov > kSmallOv) {
+        if (tid == 0) out->fallback = 1;
+        return;
+    }
+    __syncthreads();
+    // (2c) stable scatter
+    const unsigned lt = (1u << lane) - 1u;
+    for (int64_t c0 = lo; c0 < hi; c0 += 32) {
+        const int64_t i = c0 + lane;
+        const bool valid = i < hi;
+        const int32_t key = valid ? keys[i] : -1;
+        const unsigned peers = __match_any_sync(0xffffffffu, key);
+        int32_t b0 = 0;
+        if (valid) {
+            b0 = hw[key];
+            perm[b0 + __popc(peers & lt)] = (int32_t)i;
+        }
+        __syncwarp();
+        if (valid && lane == __ffs(peers) - 1) hw[key] = b0 + __popc(peers);
+        __syncwarp();
+    }
+    __syncthreads();
+    // (2d) oversized rows (kept in row order by the scatter): rank by (degree, row)
+    if (tid < n_ov) {
+        const int32_t r = perm[ov_start + tid];
+        ovr[tid] = r;
+        ovd[tid] = rowptr[r + 1] - rowptr[r];
+    }
+    __syncthreads();
+    if (tid < n_ov) {
+        const int32_t d = ovd[tid];
+        int32_t rank = 0;
+        for (int j = 0; j < (int)n_ov; ++j) rank += (ovd[j] < d) | ((ovd[j] == d) & (j < tid));
+        perm[ov_start + rank] = ovr[tid];
+    }
+    __syncthreads();
+    // (3) sorted degrees and row offsets (independent strided iterations), then the exclusive
+    // scan -> sorted_rowptr (contiguous segment per thread)
+#pragma unroll 4
+    for (int64_t r = tid; r < n; r += kSmallThreads) {
+        const int32_t i = perm[r];
+        const int32_t a = rowptr[i];
+        srp[r] = rowptr[i + 1] - a;
+        rso[r] = a - base;
+    }
+    __syncthreads();
+    const int64_t per = (n + kSmallThreads - 1) / kSmallThreads;
+    const int64_t a0 = min(n, tid * per), a1 = min(n, a0 + per);
+    int64_t sum = 0;
+    for (int64_t r = a0; r < a1; ++r) sum += srp[r];
+    {
+        int64_t all;
+        int64_t run = block_exscan(sum, wsum, &all);
+        for (int64_t r = a0; r < a1; ++r) {
+            const int32_t d = srp[r];
+            srp[r] = (int32_t)run;
+            run += d;
+        }
+        if (tid == 0) srp[n] = (int32_t)all;
+    }
+    __syncthreads();
+    // (4) Alg. 1 per degree and the descriptor count of each bucket, scanned
+    {
+        const int32_t d = tid + 1;
+        int64_t nb = 0;
+        if (d <= db) {
+            int32_t f = 1;
+            while (!(mbw % f == 0 && (int64_t)f * mwn >= d)) ++f;
+            const int32_t br = mbw / f;
+            nb = (tot[d] + br - 1) / br;
+        }
+        int64_t all;
+        const int64_t st = block_exscan(nb, wsum, &all);
+        if (d <= db) blk[d] = (int32_t)st;
+        if (tid == 0) blk[db + 1] = (int32_t)all;
+    }
+    __syncthreads();
+    const int32_t nb_small = blk[db + 1];
+    // (5) descriptors of the degree <= db part: descriptor b is block i of bucket d
+    for (int32_t b = tid; b < nb_small; b += kSmallThreads) {
+        int32_t lo_d = 1, hi_d = db + 1;  // last d in [1, db] with blk[d] <= b
+        while (lo_d < hi_d) {
+            const int32_t mid = (lo_d + hi_d) >> 1;
+            if (blk[mid] <= b) lo_d = mid + 1; else hi_d = mid;
+        }
+        const int32_t d = lo_d - 1;
+        int32_t f = 1;
+        while (!(mbw % f == 0 && (int64_t)f * mwn >= d)) ++f;
+        const int32_t br = mbw / f, wn = (d + f - 1) / f;
+        const int32_t i = b - blk[d];
+        const int32_t row = rs[d] + i * br;
+        const int32_t rows = min(br, tot[d] - i * br);
+        desc[b] = make_int4(d, srp[row], row, (int32_t)(((uint32_t)wn << 16) | (uint32_t)rows));
+    }
+    // oversized chunks: row k of the suffix -> ceil(d / db) chunks
+    {
+        int64_t nc = 0, loc = 0, d = 0;
+        const int64_t row = ov_start + tid;
+        if (tid < n_ov) {
+            loc = srp[row];
+            d = srp[row + 1] - loc;
+            nc = (d + db - 1) / db;
+        }
+        int64_t all;
+        const int64_t c0 = block_exscan(nc, wsum, &all);
+        if (tid < n_ov) {
+            ov_chunk_start[tid] = (int32_t)c0;
+            for (int64_t j = 0; j < nc; ++j)
+                desc[nb_small + c0 + j] = make_int4((int32_t)d, (int32_t)(loc + j * db), (int32_t)row,
+                                                    (int32_t)(d - j * db < db ? d - j * db : db));
+        }
+        if (tid == 0) {
+            ov_chunk_start[n_ov] = (int32_t)all;
+            out->fallback = 0;
+            out->bad_rowptr = s_bad;
+            out->bad_colidx = s_badc;
+            out->max_deg = s_max;
+            out->rowptr_first = base;
+            out->rowptr_last = rowptr[n];
+            out->n_ov_heavy = s_nhv;
+            out->nb_small = nb_small;
+            out->n_zero = n_zero;
+            out->n_ov = n_ov;
+            out->ov_chunks = (int64_t)s_ovc;
+            out->ov_chunks_heavy = (int64_t)s_ovh;
+        }
+    }
+}
+
+// Returns false (nothing allocated) when the graph is outside the one-CTA limits or has more
+// than kSmallOv oversized rows; errors (bad CSR) are thrown as in the general path.
+bool build_block_plan_small(agcn_plan_s* p, const int32_t* rowptr, const int32_t* colidx,
+                            const agcn_opts_t& o, cudaStream_t s) {
+    const char* env = getenv("AGCN_SMALL_PLAN");  // read per plan (tests switch it)
+    if (env && atoi(env) == 0) return false;
+    const int64_t n = p->n, nnz = p->nnz;
+    const int32_t db = p->deg_bound;
+    if (n <= 0 || n > kSmallRows || nnz > kSmallNnz || db > kSmallDb) return false;
+    const int32_t nbins = db + 2;
+    const size_t smem = sizeof(int32_t) * (size_t)(33 * nbins + db + 2 + 2 * kSmallOv + nbins + 2) +
+                        sizeof(int64_t) * 64 + sizeof(int16_t) * (size_t)n + 16;
+    const int64_t desc_cap = n + nnz / db + kSmallOv + 1;
+    const int64_t ovc_cap = std::min<int64_t>(n, kSmallOv) + 1;
+    Scratch tmp(s);
+    SmallOut* d_out = tmp.alloc<SmallOut>(1);
+    AGCN_CUDA(cudaMemsetAsync(d_out, 0, sizeof(SmallOut), s));
+    p->perm = dalloc<int32_t>(n, s);
+    p->sorted_rowptr = dalloc<int32_t>(n + 1, s);
+    p->row_src_off = dalloc<int32_t>(n, s);
+    p->desc = dalloc<int4>(desc_cap, s);
+    p->ov_chunk_start = dalloc<int32_t>(ovc_cap, s);
+    static bool attr = false;
+    if (!attr) {
+        AGCN_CUDA(cudaFuncSetAttribute(k_plan_small, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)(sizeof(int32_t) * (35 * (kSmallDb + 2) + 2 * kSmallOv + 2) +
+                                             sizeof(int64_t) * 64 + sizeof(int16_t) * kSmallRows + 16)));
+        attr = true;
+    }
+    k_plan_small<<<1, kSmallThreads, smem, s>>>(rowptr, colidx, n, nnz, p->n_cols, db, p->mbw, p->mwn,
+                                                o.validate, p->perm, p->sorted_rowptr, p->row_src_off,
+                                                p->desc, p->ov_chunk_start, d_out);
+    post_launch();
+    SmallOut h{};
+    AGCN_CUDA(cudaMemcpyAsync(&h, d_out, sizeof(SmallOut), cudaMemcpyDeviceToHost, s));
+    AGCN_CUDA(cudaStreamSynchronize(s));
+    if (h.fallback) {
+        for (void* q : {(void*)p->perm, (void*)p->sorted_rowptr, (void*)p->row_src_off, (void*)p->desc,
+                        (void*)p->ov_chunk_start})
+            cudaFreeAsync(q, s);
+        p->perm = p->sorted_rowptr = p->row_src_off = p->ov_chunk_start = nullptr;
+        p->desc = nullptr;
+        return false;
+    }
+    PlanFlags f{};
+    f.bad_rowptr = h.bad_rowptr;
+    f.rowptr_first = h.rowptr_first;
+    f.rowptr_last = h.rowptr_last;
+    check_csr_flags(f, nnz);
+    AGCN_CHECK(!h.bad_colidx, AGCN_ERR_BAD_CSR, "colidx out of [0, n_cols)");
+    p->rp_base = h.rowptr_first;
+    p->n_zero = h.n_zero;
+    p->n_ov = h.n_ov;
+    p->ov_start = n - h.n_ov;
+    p->ov_chunks = h.ov_chunks;
+    p->ov_chunks_heavy = h.ov_chunks_heavy;
+    p->n_ov_heavy = h.n_ov_heavy;
+    p->max_deg = h.max_deg;
+    p->nb_small = h.nb_small;
+    p->nblocks = h.nb_small + h.ov_chunks;
+    p->device_bytes = sizeof(int32_t) * (size_t)(3 * n + 1 + ovc_cap) + sizeof(int4) * (size_t)desc_cap;
+    set_spmm_cols(p, colidx, s);
+    return true;
+}
+
 // ---------------------------------------------------------------- block-partition plan
 void build_block_plan(agcn_plan_s* p, const int32_t* rowptr, const int32_t* colidx,
                       const agcn_opts_t& o, cudaStream_t s) {
@@ -752,7 +1080,9 @@ agcn_plan_s* build_plan(const int32_t* rowptr, const int32_t* colidx, int64_t n,
         p->stream = s;
         p->colidx = colidx;
         if (o.partition == AGCN_PARTITION_BLOCK)
-            build_block_plan(p, rowptr, colidx, o, s);
+        {
+            if (!build_block_plan_small(p, rowptr, colidx, o, s)) build_block_plan(p, rowptr, colidx, o, s);
+        }
         else
             build_warp_plan(p, rowptr, colidx, o, s);
         AGCN_CUDA(cudaEventCreateWithFlags(&p->ready, cudaEventDisableTiming));

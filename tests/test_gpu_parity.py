@@ -85,6 +85,40 @@ def test_metadata_bit_exact_random(seed):
     check_plan_vs_oracle(rowptr, colidx, mbw, mwn, n_cols=nc)
 
 
+def _plan_fields(p):
+    return {f: p.copy(f) for f in ("perm", "sorted_rowptr", "row_src_off", "blocks")}, p.stats()
+
+
+@pytest.mark.parametrize("seed", range(24))
+def test_small_plan_equals_general_plan(seed):
+    """The one-CTA plan (graphs of <= 32768 rows) and the general multi-kernel plan give
+    identical metadata (both are also checked against the oracle), incl. the fallback when a
+    small graph has more than 1024 oversized rows."""
+    rng = np.random.default_rng(1000 + seed)
+    mbw, mwn = [(12, 32), (2, 2), (1, 1), (4, 16), (8, 16), (3, 5)][seed % 6]
+    if seed % 8 == 7:          # > 1024 oversized rows: the small path falls back
+        degs = np.concatenate([np.full(1500, mbw * mwn + 1), rng.integers(0, 5, 300)])
+        rowptr, colidx = _rows_csr(rng.permutation(degs), 500, seed)
+        nc = 500
+    else:
+        n, nc = int(rng.integers(1, 32768)), int(rng.integers(1, 5000))
+        rowptr, colidx = gen.random_csr(n, nc, seed, max_deg=int(rng.choice([4, 60, 700])),
+                                        dup=bool(seed % 2))
+    got = {}
+    for small in ("1", "0"):
+        os.environ["AGCN_SMALL_PLAN"] = small
+        try:
+            p = check_plan_vs_oracle(rowptr, colidx, mbw, mwn, n_cols=nc)
+        finally:
+            os.environ.pop("AGCN_SMALL_PLAN", None)
+        got[small] = _plan_fields(p)
+    for f in got["1"][0]:
+        assert np.array_equal(got["1"][0][f], got["0"][0][f]), f
+    s1, s0 = got["1"][1], got["0"][1]
+    for k in ("nblocks", "n_zero_rows", "n_oversized_rows", "n_oversized_blocks", "max_deg", "deg_bound"):
+        assert s1[k] == s0[k], k
+
+
 def _rows_csr(degs, n_cols, seed=0):
     rng = np.random.default_rng(seed)
     rowptr = np.concatenate([[0], np.cumsum(degs)]).astype(np.int32)
