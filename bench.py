@@ -244,10 +244,12 @@ def per_graph_table(A, gen, torch, dev, skip: str, hbm_gbs: float):
             st = plan.stats()
             ms = graph_ms(lambda: plan.spmm(va, X, out=Y, stream=S), S)
             bc = 4 * (n + 1) + 8 * nnz + 8 * n * F
+            bg = 4 * (n + 1) + 8 * nnz + 4 * nnz * F + 4 * n * F   # every referenced X row moved
             row = {"n": n, "nnz": nnz, "F": F, "max_block_warps": st["max_block_warps"],
                    "max_warp_nzs": st["max_warp_nzs"], "plan_ms": plan_ms, "spmm_ms": ms,
                    "gflops": 2.0 * nnz * F / (ms * 1e-3) / 1e9, "b_comp_gbs": bc / (ms * 1e-3) / 1e9,
-                   "b_comp_frac_of_hbm": bc / (ms * 1e-3) / 1e9 / hbm_gbs}
+                   "b_comp_frac_of_hbm": bc / (ms * 1e-3) / 1e9 / hbm_gbs,
+                   "b_gather_gbs": bg / (ms * 1e-3) / 1e9}
             plan.close()
             try:
                 Acsr = torch.sparse_csr_tensor(rp, ci, va, size=(n, n))
