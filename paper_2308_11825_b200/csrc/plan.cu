@@ -755,12 +755,12 @@ bool build_block_plan_small(agcn_plan_s* p, const int32_t* rowptr, const int32_t
     p->row_src_off = dalloc<int32_t>(n, s);
     p->desc = dalloc<int4>(desc_cap, s);
     p->ov_chunk_start = dalloc<int32_t>(ovc_cap, s);
-    static bool attr = false;
-    if (!attr) {
+    static bool attr[64] = {};  // the shared-memory opt-in is per device
+    if (p->device < 0 || p->device >= 64 || !attr[p->device]) {
         AGCN_CUDA(cudaFuncSetAttribute(k_plan_small, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)(sizeof(int32_t) * (35 * (kSmallDb + 2) + 2 * kSmallOv + 2) +
                                              sizeof(int64_t) * 64 + sizeof(int16_t) * kSmallRows + 16)));
-        attr = true;
+        if (p->device >= 0 && p->device < 64) attr[p->device] = true;
     }
     k_plan_small<<<1, kSmallThreads, smem, s>>>(rowptr, colidx, n, nnz, p->n_cols, db, p->mbw, p->mwn,
                                                 o.validate, p->perm, p->sorted_rowptr, p->row_src_off,
