@@ -588,6 +588,23 @@ def test_pipeline_matches_propagate_host():
             assert oracle.spmm_check(w.rowptr, w.colidx, w.vals, X, Y.numpy())["nfail"] == 0
 
 
+def test_pipeline_degenerate_jobs():
+    """Edgeless graphs (Y = 0) and a 1-row graph through the executor, between real jobs."""
+    w = gen.make_config("c1")
+    X = w.X(16)
+    with A.Pipeline(depth=2) as pipe:
+        Y0 = np.full((7, 16), 5.0, np.float32)
+        pipe.submit(np.zeros(8, np.int32), np.zeros(0, np.int32), np.zeros(0, np.float32),
+                    np.ones((7, 16), np.float32), 2, out=Y0)
+        Y1 = pipe.submit(w.rowptr, w.colidx, w.vals, X, 1)
+        Yr = pipe.submit(np.array([0, 2], np.int32), np.array([0, 0], np.int32),
+                         np.array([1.5, -0.5], np.float32), np.full((1, 16), 2.0, np.float32), 3)
+        pipe.wait()
+    assert not Y0.any()
+    assert np.array_equal(Y1, A.propagate_host(w.rowptr, w.colidx, w.vals, X, 1))
+    assert np.allclose(Yr, 2.0)                        # (1.5 - 0.5) ** 3 * 2
+
+
 def test_pipeline_error_leaves_executor_usable():
     w = gen.make_config("c1")
     X = w.X(16)
