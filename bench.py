@@ -47,7 +47,7 @@ def parse():
     ap.add_argument("--l2-hint", type=int, default=None, help="None: auto; 0: never; 1: always")
     ap.add_argument("--col-block-mb", type=int, default=None,
                     help="None: auto; 0: off (paper chunks); MiB of X per column block")
-    ap.add_argument("--e2e-steps", type=int, default=6)
+    ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="CPU-oracle sample budget")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
