@@ -48,7 +48,7 @@ def parse():
     ap.add_argument("--col-block-mb", type=int, default=None,
                     help="None: auto; 0: off (paper chunks); MiB of X per column block")
     ap.add_argument("--e2e-steps", type=int, default=10)
-    ap.add_argument("--cpu-seconds", type=float, default=15.0, help="CPU-oracle sample budget")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0, help="CPU-oracle sample budget")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cusparse", action="store_true")
@@ -292,9 +292,14 @@ def cpu_sample_gflops(w, X, budget_s: float):
     hi = int(np.searchsorted(w.rowptr, w.rowptr[lo] + want_nnz))
     hi = max(lo + 1, min(hi, n))
     t, nz = run(lo, hi)
+    passes = 1
+    while t < 0.9 * budget_s:        # the sample is capped at 2/3 of the graph: repeat it
+        dt, dn = run(lo, hi)
+        t, nz, passes = t + dt, nz + dn, passes + 1
     return {"value": 2.0 * nz * F / t / 1e9, "unit": UNIT, "cores": cores, "kind": "oracle",
-            "sample": f"rows [{lo},{hi}) of {w.name} ({nz} nnz = {100.0 * nz / w.nnz:.2f}% of nnz), "
-                      f"one fp64 SpMM layer, F={F}, {t:.1f} s"}, t
+            "sample": f"rows [{lo},{hi}) of {w.name} ({nz // passes} nnz = "
+                      f"{100.0 * nz / passes / w.nnz:.2f}% of nnz) x {passes} passes, "
+                      f"one fp64 SpMM layer each, F={F}, {t:.1f} s"}, t
 
 
 # ---------------------------------------------------------------- reference arm (the oracle)
