@@ -49,6 +49,8 @@ def parse():
                     help="None: auto; 0: off (paper chunks); MiB of X per column block")
     ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="CPU-oracle sample budget")
+    ap.add_argument("--ref-seconds", type=float, default=120.0,
+                    help="--impl reference: total CPU budget over warm-up + timed steps")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cusparse", action="store_true")
@@ -312,7 +314,7 @@ def run_reference(args):
     F = args.F or w.F
     X = w.X(F)
     times, vals = [], []
-    budget = max(2.0, 120.0 / max(1, args.steps + args.warmup))
+    budget = max(min(2.0, args.ref_seconds), args.ref_seconds / max(1, args.steps + args.warmup))
     for i in range(args.warmup + args.steps):
         cb, t = cpu_sample_gflops(w, X, budget)
         if i >= args.warmup:
