@@ -106,6 +106,8 @@ void agcn_default_opts(agcn_opts_t* opts);
  * cuSPARSE CSR descriptor).  The AGCN_PARTITION_WARP plan copies colidx.  Synchronises the
  * plan stream once mid-way (bucket counts, validation flags); the last kernels run
  * asynchronously on opts.stream, and agcn_spmm on another stream waits for them (event).
+ * Block plans of graphs with n <= 32768, nnz <= 2^20, deg_bound <= 512 and at most 1024
+ * oversized rows run as one CTA and synchronise once at its end (same metadata).
  * Limits: deg_bound = max_block_warps*max_warp_nzs <= 2048,
  * max_block_warps < 65536 and max_warp_nzs < 65536 (16-bit info halves) -> otherwise
  * AGCN_ERR_UNSUPPORTED / AGCN_ERR_OVERFLOW.  Returns NULL on error.
@@ -247,13 +249,16 @@ agcn_status_t agcn_propagate_host(const int32_t* rowptr_host, const int32_t* col
  *   copy-in, one compute and one copy-out stream on the current device).  NULL on failure.
  * agcn_pipe_submit: enqueue one job on HOST buffers (as agcn_propagate_host: rowptr[n+1],
  *   colidx / vals indexed by rowptr values, X [n_cols x F], Y [n x F]; n_cols = opts->n_cols
- *   or n).  Returns once the job's inputs are on the device and its plan is built (the plan
- *   reads its bucket counts back); the SpMM and the copy of Y run asynchronously.  The caller
- *   keeps every host buffer of the job alive and unmodified, and reads Y_host only after
+ *   or n).  Enqueues the job's copy-in and returns; a worker thread owned by the executor
+ *   builds the plan (it waits for the inputs), enqueues the SpMMs and the copy of Y.  Blocks
+ *   only while the job's buffer slot still belongs to an earlier job the worker has not
+ *   enqueued yet.  Argument errors (and rowptr[n] - rowptr[0] != nnz) are returned here; errors
+ *   found later (a bad CSR, a CUDA error) are returned by agcn_pipe_wait.  The caller keeps
+ *   every host buffer of the job alive and unmodified, and reads Y_host only after
  *   agcn_pipe_wait.  Host buffers should be pinned (page-locked): pageable memory works but
- *   the copies then do not overlap.  A failed submit leaves the executor usable.
+ *   the copies then do not overlap.  A failed job leaves the executor usable.
  * agcn_pipe_wait: blocks until every submitted job has finished (Y_host written); returns the
- *   first asynchronous CUDA error, if any.
+ *   first error of the jobs since the previous wait (that job's Y_host is not written), if any.
  * agcn_pipe_destroy: waits, then frees the device buffers and streams.  NULL is a no-op.
  */
 typedef struct agcn_pipe_s* agcn_pipe_t;

@@ -611,8 +611,9 @@ def test_pipeline_error_leaves_executor_usable():
     pipe = A.Pipeline(depth=1)
     bad = w.colidx.copy()
     bad[5] = w.n + 3                                   # column out of range: plan rejects it
+    pipe.submit(w.rowptr, bad, w.vals, X, 1)          # the plan (worker) finds it
     with pytest.raises(A.AgcnError) as e:
-        pipe.submit(w.rowptr, bad, w.vals, X, 1)
+        pipe.wait()
     assert e.value.status == "AGCN_ERR_BAD_CSR"
     from paper_2308_11825_b200 import _lib
     Yb = np.empty((w.n, 16), np.float32)               # rowptr[n] - rowptr[0] != nnz
