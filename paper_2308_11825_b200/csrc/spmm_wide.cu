@@ -95,6 +95,7 @@ struct WideArgs {
     int64_t piece_cap;    // upper bound of the piece count (grid sizing)
     Epi epi;              // output epilogue (EPI)
     int32_t L;            // lanes per X row (F / 8); used when the kernel's LT is 0
+    int32_t zero_last;    // write the degree-0 rows after the descriptors (A/B: AGCN_ZERO_LAST)
 };
 
 // a finished output row slice of 8 floats at column c of original row orow (degree deg)
@@ -129,8 +130,10 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_wide(const __grid_const
     const int32_t gw = blockIdx.x * kWarps + (threadIdx.x >> 5);
     const int32_t W = gridDim.x * kWarps;
 
-    // degree-0 rows: Y row = 0 (reading Q16); 32 rows per warp step, one perm load per lane
-    {
+    // degree-0 rows: Y row = 0 (reading Q16); 32 rows per warp step, one perm load per lane.
+    // Before the descriptors, or after them (a.zero_last: the stores then fill the tail left by
+    // the last, longest descriptors instead of preceding the gathers)
+    auto zero_rows = [&]() {
         f8 z;
         z.a = z.b = make_float4(0.f, 0.f, 0.f, 0.f);
         for (int64_t r0 = (int64_t)gw * 32; r0 < a.n_zero; r0 += (int64_t)W * 32) {
@@ -141,7 +144,8 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_wide(const __grid_const
                 if (act && (FULL || i + s < 32) && o >= 0) store_row<EPI>(a.Y, o, li * 8, F, 0, z, a.epi);
             }
         }
-    }
+    };
+    if (!a.zero_last) zero_rows();
 
     // execution list: the plan's descriptors [0, n_desc), then (when the column-blocked
     // schedule replaces the oversized chunks) its pieces, block-major
@@ -320,6 +324,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_wide(const __grid_const
             }
         }
     }
+    if (a.zero_last) zero_rows();
 }
 
 template <int L, int U, int MINB, bool KEEP, bool PIECES, bool EPI>
@@ -392,6 +397,8 @@ void launch_wide(agcn_plan_s* p, const float* vals, const float* X, int32_t F, f
                blocked ? cs.partial : nullptr, blocked ? cs.cap : 0, epi};
     AGCN_CHECK(a.n_desc + a.piece_cap < (1ll << 31), AGCN_ERR_OVERFLOW, "too many descriptors");
     a.L = F / 8;
+    static const int zero_last = env_int("AGCN_ZERO_LAST", 1);  // C5 -1 %, C3/C4 even (profiles r01bj)
+    a.zero_last = zero_last;
     switch (F) {
         case 8: launch<1>(a, l2_keep, s); break;
         case 16: launch<2>(a, l2_keep, s); break;
