@@ -366,16 +366,14 @@ void launch_k(const WideArgs& a, bool keep, cudaStream_t s) {
 
 template <int L>
 void launch(const WideArgs& a, bool keep, cudaStream_t s) {
-    // register budget vs rows in flight (AGCN_WIDE_VARIANT, A/B only; profiles/r01k_wide_ab.md):
-    //   0: U 4 at 3 CTAs/SM (80 regs, no spills; the default)   3: U 4 at 4 CTAs/SM (64 regs)
+    // register budget vs rows in flight (AGCN_WIDE_VARIANT, A/B only; profiles/r01k_wide_ab.md,
+    // r01bc_kernel_shapes.md; the measured-and-dropped shapes -- U 4 at 4 CTAs/SM with spills,
+    // U 2 at 5 CTAs/SM, U 8 at 2 CTAs/SM -- are no longer instantiated):
+    //   0: U 4 at 3 CTAs/SM (80 regs; the default)   4: U 2 at 4 CTAs/SM (64 regs)
     static const int variant = env_int("AGCN_WIDE_VARIANT", 0);
     constexpr int U4 = L >= 4 ? 4 : L, U2 = L >= 2 ? 2 : L;
-    if (variant == 3)
-        launch_k<L, U4, 4>(a, keep, s);
-    else if (variant == 4)
+    if (variant == 4)
         launch_k<L, U2, 4>(a, keep, s);
-    else if (variant == 5)
-        launch_k<L, U2, 5>(a, keep, s);
     else
         launch_k<L, U4, 3>(a, keep, s);
 }
