@@ -222,6 +222,7 @@ struct agcn_plan_s {
     // SpMM scratch (oversized-row partial sums, chunk-major [ov_chunks][F])
     float* ov_partial = nullptr;
     size_t ov_partial_floats = 0;
+    int32_t* ov_cnt = nullptr;         // [n_ov] finished-chunk counters of the fused level 3 (zero at rest)
     agcn::ColSched sched;              // column-blocked schedule of the oversized rows (WIDE)
 
     size_t device_bytes = 0;
@@ -236,7 +237,7 @@ void spmm_launch(agcn_plan_s* p, const float* vals, const float* X, int32_t F, f
 // spmm_wide.cu: 256-bit-per-lane kernel for F in {8,...,256}
 bool wide_supported(const agcn_plan_s* p, const float* X, const float* Y, int32_t F);
 void launch_wide(agcn_plan_s* p, const float* vals, const float* X, int32_t F, float* Y,
-                 bool l2_keep, bool blocked, const Epi& epi, cudaStream_t s);
+                 bool l2_keep, bool blocked, bool fuse_ov, const Epi& epi, cudaStream_t s);
 // spmm_pipe.cu: cp.async shared-memory gather pipeline, F in {32,64,128,256}
 bool pipe_supported(const agcn_plan_s* p, const float* X, const float* Y, int32_t F);
 void launch_pipe(agcn_plan_s* p, const float* vals, const float* X, int32_t F, float* Y, cudaStream_t s);

@@ -973,7 +973,7 @@ void build_warp_plan(agcn_plan_s* p, const int32_t* rowptr, const int32_t* colid
 
 void free_plan_arrays(agcn_plan_s* p) {
     void* ptrs[] = {p->perm,  p->sorted_rowptr, p->row_src_off, p->desc,       p->ov_chunk_start,
-                    p->tasks, p->rowptr_copy,   p->cols_copy,   p->ov_partial};
+                    p->tasks, p->rowptr_copy,   p->cols_copy,   p->ov_partial, p->ov_cnt};
     // Stream-ordered release on the plan's stream, after the last SpMM that used the plan on
     // another stream (p->last_use); no host synchronisation.
     if (p->last_use) cudaStreamWaitEvent(p->stream, p->last_use, 0);

@@ -365,6 +365,7 @@ __global__ void __launch_bounds__(kReduceThreads) k_ov_reduce(
 // chunk order; the NG group sums are then added in group order (shuffles / shared memory).
 // Every summation order is a function of the plan alone: deterministic.
 constexpr int kReduceWarps = 8;
+constexpr int64_t kFuseOvMaxChunks = 16384;  // fused level 3 up to this many oversized chunks
 template <bool V4>
 __global__ void __launch_bounds__(kReduceWarps * 32) k_ov_reduce_h(
     const float* __restrict__ ovp_f, const int32_t* __restrict__ chunk_start,
@@ -715,23 +716,36 @@ void spmm_launch(agcn_plan_s* p, const float* vals, const float* X, int32_t F, f
     const double x_bytes = 4.0 * (double)p->x_rows * F;
     const bool keep = o.l2_hint < 0 ? x_bytes <= kL2KeepBytes : o.l2_hint > 0;
     a.keep = keep;
+    // level 3 of the oversized rows of <= kHeavyChunks chunks fused into the WIDE kernel when
+    // there are few chunks (saves the reduction launch on small graphs: C2 -4..7 %, C3 -7 %;
+    // with C5's 201K chunks the per-chunk fence + counter costs more than the launch: +3 %;
+    // profiles/r01bk_fused_level3.md).  AGCN_FUSE_OV: -1 auto (default), 0 never, 1 always.
+    static const int fuse_env = [] { const char* e = getenv("AGCN_FUSE_OV"); return e ? atoi(e) : -1; }();
+    const bool fuse = kernel == AGCN_KERNEL_WIDE && !blocked && p->n_ov > 0 && fuse_env != 0 &&
+                      (fuse_env > 0 || p->ov_chunks <= kFuseOvMaxChunks) && env_int("AGCN_OV_REDUCE", 1) != 0;
+    if (fuse && !p->ov_cnt) {
+        p->ov_cnt = dalloc<int32_t>(p->n_ov, s);
+        AGCN_CUDA(cudaMemsetAsync(p->ov_cnt, 0, sizeof(int32_t) * p->n_ov, s));
+    }
     if (kernel == AGCN_KERNEL_PIPE)
         launch_pipe(p, vals, X, F, Y, s);
     else if (kernel == AGCN_KERNEL_WIDE)
-        launch_wide(p, vals, X, F, Y, keep, blocked, epi, s);  // epilogue fused
+        launch_wide(p, vals, X, F, Y, keep, blocked, fuse, epi, s);  // epilogue fused
     else if (v4)
         AGCN_DISPATCH_LT(sh, block_v4, a, s, smem);
     else
         AGCN_DISPATCH_LT(sh, block_v1, a, s, smem);
     if (kernel != AGCN_KERNEL_WIDE && epi.active())  // rows of degree <= deg_bound
         launch_epilogue(Y, 0, p->ov_start, F, p->perm, p->sorted_rowptr, epi, s);
-    if (p->n_ov > 0) {  // level 3: oversized rows = fixed-order sums of their partial rows
+    if (p->n_ov > 0 && !(fuse && p->n_ov_heavy == 0)) {  // level 3: fixed-order sums of partial rows
         const unsigned grid = (unsigned)p->n_ov;
         const float* part = blocked ? p->sched.partial : p->ov_partial;
         const int32_t* slots = blocked ? p->sched.slot_base : p->ov_chunk_start;
         static const int red = env_int("AGCN_OV_REDUCE", 1);  // 1: sized (default), 0: CTA per row
         const int64_t nh = p->n_ov_heavy;
-        const unsigned hgrid = (unsigned)(nh + (p->n_ov - nh + kReduceWarps - 1) / kReduceWarps);
+        // fused: only the heavy rows (CTAs [0, nh) of the kernel) are left
+        const unsigned hgrid = fuse ? (unsigned)nh
+                                    : (unsigned)(nh + (p->n_ov - nh + kReduceWarps - 1) / kReduceWarps);
         if (red && v4)
             k_ov_reduce_h<true><<<hgrid, kReduceWarps * 32, 0, s>>>(part, slots, p->perm, p->ov_start, p->n_ov,
                                                                    nh, Y, FV, p->sorted_rowptr, epi);

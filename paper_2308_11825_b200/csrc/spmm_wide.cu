@@ -96,7 +96,12 @@ struct WideArgs {
     Epi epi;              // output epilogue (EPI)
     int32_t L;            // lanes per X row (F / 8); used when the kernel's LT is 0
     int32_t zero_last;    // write the degree-0 rows after the descriptors (A/B: AGCN_ZERO_LAST)
+    int32_t fuse_ov;      // level 3 of rows of <= kHeavyChunks chunks done by the last warp
+    const int32_t* ov_cs; // [n_ov + 1] first chunk of oversized row k
+    int32_t* ov_cnt;      // [n_ov] chunks of row k finished (zero between launches)
+    int64_t ov_start;     // sorted position of the first oversized row
 };
+
 
 // a finished output row slice of 8 floats at column c of original row orow (degree deg)
 template <bool EPI>
@@ -111,6 +116,40 @@ __device__ __forceinline__ void store_row(float* Y, int64_t orow, int32_t c, int
         fanout4(e, orow * F + c, v.a);
         fanout4(e, orow * F + c + 4, v.b);
     }
+}
+
+// Level 3 fused (deterministic): after a warp has written the partial row of an
+// oversized chunk, it counts the chunk in; the warp that completes a row of at most
+// kHeavyChunks chunks sums that row's partials in chunk order (L2 loads: they were written by
+// other SMs), applies the epilogue, stores the output row and re-arms the counter.  Heavier rows
+// keep their CTA-wide reduction kernel.
+template <bool EPI>
+__device__ __noinline__ void ov_finish(const WideArgs& a, int32_t row, int32_t deg, int32_t F, int lane,
+                                       int s, int li) {
+    __threadfence();                 // publish this warp's partial-row stores
+    __syncwarp();
+    const int64_t k = row - a.ov_start;
+    const int32_t c0 = __ldg(a.ov_cs + k), nc = __ldg(a.ov_cs + k + 1) - c0;
+    if (nc > kHeavyChunks) return;
+    int last = 0;
+    if (lane == 0) last = atomicAdd(a.ov_cnt + k, 1) == nc - 1;
+    last = __shfl_sync(0xffffffffu, last, 0);
+    if (!last) return;
+    __threadfence();                 // the other chunks' partials are visible from here on
+    if (s == 0) {
+        f8 acc;
+        acc.a = acc.b = make_float4(0.f, 0.f, 0.f, 0.f);
+        const float* base = a.ovp + (int64_t)c0 * F + li * 8;
+#pragma unroll 4
+        for (int32_t j = 0; j < nc; ++j) {
+            const float4 x0 = __ldcg(reinterpret_cast<const float4*>(base + (int64_t)j * F));
+            const float4 x1 = __ldcg(reinterpret_cast<const float4*>(base + (int64_t)j * F) + 1);
+            acc.a.x += x0.x; acc.a.y += x0.y; acc.a.z += x0.z; acc.a.w += x0.w;
+            acc.b.x += x1.x; acc.b.y += x1.y; acc.b.z += x1.z; acc.b.w += x1.w;
+        }
+        store_row<EPI>(a.Y, __ldg(a.perm + row), li * 8, F, deg, acc, a.epi);
+    }
+    if (lane == 0) a.ov_cnt[k] = 0;
 }
 
 // L lanes per X row (F = 8 L), U X rows in flight per lane, MINB resident CTAs per SM
@@ -236,6 +275,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_wide(const __grid_const
                 c = cn;
                 v = vn;
             }
+            if (ov && !piece && a.fuse_ov) ov_finish<EPI>(a, m.z, m.x, F, lane, s, li);
             continue;
         }
         // ---- rows split over K combined warps (R <= G/2): contiguous parts, xor-tree merge
@@ -323,6 +363,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_wide(const __grid_const
                                : a.ovp + (int64_t)(b - a.first_ov) * F) + li * 8, acc);
             }
         }
+        if (ov && !piece && a.fuse_ov) ov_finish<EPI>(a, m.z, m.x, F, lane, s, li);
     }
     if (a.zero_last) zero_rows();
 }
@@ -387,7 +428,7 @@ bool wide_supported(const agcn_plan_s* p, const float* X, const float* Y, int32_
 }
 
 void launch_wide(agcn_plan_s* p, const float* vals, const float* X, int32_t F, float* Y,
-                 bool l2_keep, bool blocked, const Epi& epi, cudaStream_t s) {
+                 bool l2_keep, bool blocked, bool fuse_ov, const Epi& epi, cudaStream_t s) {
     const ColSched& cs = p->sched;
     WideArgs a{p->desc, blocked ? p->nb_small : p->nblocks, p->nb_small, p->n_zero, p->cols,
                p->sorted_rowptr, p->row_src_off, p->perm, vals + p->rp_base, X, Y, p->ov_partial,
@@ -397,6 +438,10 @@ void launch_wide(agcn_plan_s* p, const float* vals, const float* X, int32_t F, f
     a.L = F / 8;
     static const int zero_last = env_int("AGCN_ZERO_LAST", 1);  // C5 -1 %, C3/C4 even (profiles r01bj)
     a.zero_last = zero_last;
+    a.fuse_ov = fuse_ov && !blocked && p->n_ov > 0 && p->ov_cnt != nullptr;
+    a.ov_cs = p->ov_chunk_start;
+    a.ov_cnt = p->ov_cnt;
+    a.ov_start = p->ov_start;
     switch (F) {
         case 8: launch<1>(a, l2_keep, s); break;
         case 16: launch<2>(a, l2_keep, s); break;
