@@ -363,6 +363,24 @@ ColMap make_colmap(const agcn_opts_t& o, int64_t n_cols) {
 
 namespace {
 
+// Pinned host staging for the plan's readbacks (a pageable destination makes the driver bounce
+// the copy through its own pinned buffer); one per host thread, grown on demand.
+void* pinned_staging(size_t bytes) {
+    thread_local void* buf = nullptr;
+    thread_local size_t cap = 0;
+    if (bytes > cap) {
+        if (buf) cudaFreeHost(buf);
+        buf = nullptr;
+        cap = 0;
+        if (cudaMallocHost(&buf, bytes) != cudaSuccess) {
+            cudaGetLastError();
+            return nullptr;
+        }
+        cap = bytes;
+    }
+    return buf;
+}
+
 void read_flags(PlanFlags* d_flags, PlanFlags* h, cudaStream_t s) {
     AGCN_CUDA(cudaMemcpyAsync(h, d_flags, sizeof(PlanFlags), cudaMemcpyDeviceToHost, s));
     AGCN_CUDA(cudaStreamSynchronize(s));
@@ -767,8 +785,10 @@ bool build_block_plan_small(agcn_plan_s* p, const int32_t* rowptr, const int32_t
                                                 p->desc, p->ov_chunk_start, d_out);
     post_launch();
     SmallOut h{};
-    AGCN_CUDA(cudaMemcpyAsync(&h, d_out, sizeof(SmallOut), cudaMemcpyDeviceToHost, s));
+    auto* pin = static_cast<SmallOut*>(pinned_staging(sizeof(SmallOut)));
+    AGCN_CUDA(cudaMemcpyAsync(pin ? pin : &h, d_out, sizeof(SmallOut), cudaMemcpyDeviceToHost, s));
     AGCN_CUDA(cudaStreamSynchronize(s));
+    if (pin) h = *pin;
     if (h.fallback) {
         for (void* q : {(void*)p->perm, (void*)p->sorted_rowptr, (void*)p->row_src_off, (void*)p->desc,
                         (void*)p->ov_chunk_start})
@@ -825,8 +845,18 @@ void build_block_plan(agcn_plan_s* p, const int32_t* rowptr, const int32_t* coli
 
     std::vector<int32_t> h_cnt(nbins);
     PlanFlags hf{};
-    AGCN_CUDA(cudaMemcpyAsync(h_cnt.data(), bin_cnt, sizeof(int32_t) * nbins, cudaMemcpyDeviceToHost, s));
-    read_flags(d_flags, &hf, s);  // the plan's mid-course synchronisation (bucket counts)
+    // the plan's mid-course synchronisation (bucket counts, flags), through pinned staging
+    if (auto* pin = static_cast<unsigned char*>(pinned_staging(sizeof(PlanFlags) + sizeof(int32_t) * nbins))) {
+        AGCN_CUDA(cudaMemcpyAsync(pin, d_flags, sizeof(PlanFlags), cudaMemcpyDeviceToHost, s));
+        AGCN_CUDA(cudaMemcpyAsync(pin + sizeof(PlanFlags), bin_cnt, sizeof(int32_t) * nbins,
+                                  cudaMemcpyDeviceToHost, s));
+        AGCN_CUDA(cudaStreamSynchronize(s));
+        memcpy(&hf, pin, sizeof(PlanFlags));
+        memcpy(h_cnt.data(), pin + sizeof(PlanFlags), sizeof(int32_t) * nbins);
+    } else {
+        AGCN_CUDA(cudaMemcpyAsync(h_cnt.data(), bin_cnt, sizeof(int32_t) * nbins, cudaMemcpyDeviceToHost, s));
+        read_flags(d_flags, &hf, s);
+    }
     check_csr_flags(hf, nnz);
     AGCN_CHECK(!hf.bad_colidx, AGCN_ERR_BAD_CSR, "colidx out of [0, n_cols)");
     p->rp_base = hf.rowptr_first;
