@@ -139,7 +139,7 @@ typedef enum {
     AGCN_KERNEL_LOOPED = 2,  /* ablation 2 of the paper (Fig. 4(a), Table II):
                                 no combined warp -- GENERAL with one warp of 32 scalar lanes per
                                 row that loops over the columns in strides of 32; any F */
-    AGCN_KERNEL_WIDE = 3,    /* F in {8,16,32,64,128,256}, 32-B aligned X/Y, max_block_warps
+    AGCN_KERNEL_WIDE = 3,    /* F = 8 L <= 256 (any L), 32-B aligned X/Y, max_block_warps
                                 <= 32: one 256-bit row slice per lane, shuffle-broadcast CSR */
     AGCN_KERNEL_PIPE = 4     /* F in {32,64,128,256}, 32-B aligned X/Y, max_block_warps <= 32:
                                 as WIDE, X rows gathered through a cp.async shared-memory ring */

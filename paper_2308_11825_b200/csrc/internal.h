@@ -234,7 +234,7 @@ struct agcn_plan_s {
 namespace agcn {
 void spmm_launch(agcn_plan_s* p, const float* vals, const float* X, int32_t F, float* Y,
                  cudaStream_t s, const agcn_spmm_opts_t& o);
-// spmm_wide.cu: 256-bit-per-lane kernel for F in {8,...,256}
+// spmm_wide.cu: 256-bit-per-lane kernel for F = 8 L <= 256
 bool wide_supported(const agcn_plan_s* p, const float* X, const float* Y, int32_t F);
 void launch_wide(agcn_plan_s* p, const float* vals, const float* X, int32_t F, float* Y,
                  bool l2_keep, bool blocked, bool fuse_ov, const Epi& epi, cudaStream_t s);

@@ -671,7 +671,7 @@ void spmm_launch(agcn_plan_s* p, const float* vals, const float* X, int32_t F, f
     if (kernel == AGCN_KERNEL_AUTO) kernel = wide_ok ? AGCN_KERNEL_WIDE : AGCN_KERNEL_GENERAL;
     if (kernel == AGCN_KERNEL_LOOPED) kernel = AGCN_KERNEL_GENERAL;  // with the {32 lanes, scalar} shape
     AGCN_CHECK(kernel != AGCN_KERNEL_WIDE || wide_ok, AGCN_ERR_UNSUPPORTED,
-               "WIDE kernel needs F in {8,16,32,64,128,256}, 32-byte aligned X/Y, max_block_warps <= 32");
+               "WIDE kernel needs F = 8 L <= 256, 32-byte aligned X/Y, max_block_warps <= 32");
     AGCN_CHECK(kernel != AGCN_KERNEL_PIPE || pipe_supported(p, X, Y, F), AGCN_ERR_UNSUPPORTED,
                "PIPE kernel needs F in {32,64,128,256}, 32-byte aligned X/Y, max_block_warps <= 32");
     // column-blocked oversized rows (WIDE kernel, sched.cu): X slice per block ~ col_block_mb

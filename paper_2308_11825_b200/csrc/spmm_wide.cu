@@ -1,4 +1,4 @@
-// spmm_wide.cu -- the occupancy-first SpMM kernel for F in {8, 16, 32, 64, 128, 256}.
+// spmm_wide.cu -- the occupancy-first SpMM kernel for F = 8 L <= 256 (L lanes of 32 B per X row).
 //
 // Same work decomposition and results contract as k_spmm_block (spmm.cu): one 128-bit
 // descriptor {deg, loc, row, info} per warp at a time, a "combined warp"
