@@ -588,6 +588,26 @@ def test_pipeline_matches_propagate_host():
             assert oracle.spmm_check(w.rowptr, w.colidx, w.vals, X, Y.numpy())["nfail"] == 0
 
 
+@pytest.mark.parametrize("depth", [1, 3])
+def test_pipeline_many_jobs_random_sizes(depth):
+    """20 jobs of random size / width / layer count (buffers grow and shrink) through one
+    executor: every Y equals agcn_propagate_host's."""
+    rng = np.random.default_rng(77 + depth)
+    jobs = []
+    for i in range(20):
+        n = int(rng.integers(1, 40000))
+        rowptr, colidx = gen.random_csr(n, n, 500 + i, max_deg=int(rng.choice([3, 50, 700])))
+        F = int(rng.choice([8, 16, 40, 64, 100]))
+        vals = rng.uniform(-1, 1, colidx.size).astype(np.float32)
+        X = rng.uniform(-1, 1, (n, F)).astype(np.float32)
+        jobs.append((rowptr, colidx, vals, X, int(rng.integers(1, 3))))
+    with A.Pipeline(depth=depth) as pipe:
+        outs = [pipe.submit(*j) for j in jobs]
+        pipe.wait()
+    for (rowptr, colidx, vals, X, layers), Y in zip(jobs, outs):
+        assert np.array_equal(Y, A.propagate_host(rowptr, colidx, vals, X, layers))
+
+
 def test_pipeline_degenerate_jobs():
     """Edgeless graphs (Y = 0) and a 1-row graph through the executor, between real jobs."""
     w = gen.make_config("c1")
