@@ -644,3 +644,32 @@ def test_pipeline_error_leaves_executor_usable():
     pipe.wait()
     pipe.close()
     assert np.array_equal(Y, A.propagate_host(w.rowptr, w.colidx, w.vals, X, 1))
+
+
+@pytest.mark.parametrize("name,F,layers", [("c1", 16, 2), ("c2", 64, 3), ("c3", 40, 1)])
+def test_graphed_propagation(name, F, layers):
+    """Layers captured in a CUDA graph give exactly the eager layers; replay after writing new
+    features into the captured X buffer recomputes from them."""
+    w = gen.make_config(name)
+    X = cu(w.X(F))
+    rp, ci, va = cu(w.rowptr), cu(w.colidx), cu(w.vals)
+    g = A.GraphedPropagation(rp, ci, va, X, layers)
+    p = A.Plan(rp, ci)
+    ref = X
+    for _ in range(layers):
+        ref = p.spmm(va, ref)
+    torch.cuda.synchronize()
+    assert torch.equal(g.out, ref)
+    X2 = torch.from_numpy(gen.uniform_f32(9, (w.n, F))).to(DEV)
+    g.X.copy_(X2)
+    torch.cuda.synchronize()
+    Y = g.replay()
+    torch.cuda.synchronize()
+    ref = X2
+    for _ in range(layers):
+        ref = p.spmm(va, ref)
+    torch.cuda.synchronize()
+    assert torch.equal(Y, ref)
+    if layers == 1:
+        assert oracle.spmm_check(w.rowptr, w.colidx, w.vals, X2.cpu().numpy(), Y.cpu().numpy())["nfail"] == 0
+    g.close()
