@@ -261,6 +261,26 @@ agcn_status_t agcn_propagate_host(const int32_t* rowptr_host, const int32_t* col
  *   first error of the jobs since the previous wait (that job's Y_host is not written), if any.
  * agcn_pipe_destroy: waits, then frees the device buffers and streams.  NULL is a no-op.
  */
+/*
+ * CUDA-graph propagation: `layers` x agcn_spmm (Y_{l+1} = A.Y_l, Y_0 = X; the SpMM of P:124-126
+ * with the plan's partition) captured once and replayed with one launch -- for small
+ * graphs, whose layers are bound by launch latency.
+ * agcn_graph_create: X DEVICE [n_cols x F]; ybuf0, ybuf1 DEVICE [n x F] (ybuf1 unused and may be
+ *   NULL when layers == 1); layer l writes ybuf[l % 2], so the result is ybuf[(layers-1) % 2].
+ *   Runs the layers once eagerly (synchronously; it also grows the plan's scratch), then
+ *   captures them on a private stream.  The graph keeps the pointers: every launch reads X and
+ *   vals and writes the ybufs at these addresses (write new features into X in place).
+ *   layers > 1 needs a square A.  NULL on failure.
+ * agcn_graph_launch: asynchronous on `stream` (any stream; launches on one graph must be
+ *   stream-ordered, as agcn_spmm calls on one plan).
+ * agcn_graph_destroy: frees the graph.  The plan must outlive the graph and its launches.
+ */
+typedef struct agcn_graph_s* agcn_graph_t;
+agcn_graph_t  agcn_graph_create(agcn_plan_t plan, const float* vals, const float* X, int32_t F, int32_t layers,
+                                float* ybuf0, float* ybuf1);
+agcn_status_t agcn_graph_launch(agcn_graph_t graph, agcn_stream_t stream);
+agcn_status_t agcn_graph_destroy(agcn_graph_t graph);
+
 typedef struct agcn_pipe_s* agcn_pipe_t;
 agcn_pipe_t   agcn_pipe_create(int32_t depth, const agcn_opts_t* opts);
 agcn_status_t agcn_pipe_submit(agcn_pipe_t pipe, const int32_t* rowptr_host, const int32_t* colidx_host,

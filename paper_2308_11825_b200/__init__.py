@@ -451,52 +451,43 @@ class Pipeline:
 
 
 class GraphedPropagation:
-    """`layers` x agcn_spmm (Y_{l+1} = A.Y_l, Y_0 = X) captured once in a CUDA graph and replayed:
-    for small graphs the layers are bound by launch latency, not by the GPU (C1: ~5 us of kernel
-    per layer).  The plan is built on the executor's own stream (capture needs the plan's
-    stream: no cross-stream event waits inside the graph) and warmed up before capture, so the
-    plan's scratch is allocated outside the graph.  The graph reads `self.X` and `vals` at
-    their captured addresses: write new features into `self.X` in place, then `replay()`.
-    layers > 1 needs a square A."""
+    """agcn_graph_*: `layers` x agcn_spmm (Y_{l+1} = A.Y_l, Y_0 = X) captured once in a CUDA graph
+    and replayed with one launch -- small graphs are bound by launch latency, not by the GPU.
+    The graph reads `self.X` and `vals` at their captured addresses: write new features into
+    `self.X` in place, then `replay()`.  layers > 1 needs a square A."""
 
     def __init__(self, rowptr, colidx, vals, X, layers: int = 2, **plan_kw):
         torch = _torch()
-        dev = X.device
-        self.stream = torch.cuda.Stream(device=dev)
-        self.X = X
-        self.vals = vals
-        self.layers = int(layers)
-        with torch.cuda.stream(self.stream):
-            self.plan = Plan(rowptr, colidx, stream=self.stream, **plan_kw)
-            n = self.plan.stats()["n"]
-            if self.layers > 1 and n != X.shape[0]:
-                raise ValueError("layers > 1 needs a square A")
-            self.bufs = [torch.empty((n, X.shape[1]), dtype=torch.float32, device=dev)
-                         for _ in range(min(self.layers, 2))]
-            self.out = self._run()            # warm-up: plan scratch grows here, not in the graph
-        self.stream.synchronize()
-        self.graph = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(self.graph, stream=self.stream):
-            self.out = self._run()
+        self.X, self.vals, self.layers = X, vals, int(layers)
+        self.plan = Plan(rowptr, colidx, **plan_kw)
+        n, F = self.plan.stats()["n"], X.shape[1]
+        self.bufs = [torch.empty((n, F), dtype=torch.float32, device=X.device)
+                     for _ in range(min(self.layers, 2))]
+        self.out = self.bufs[(self.layers - 1) % 2]
+        h = _lib.lib().agcn_graph_create(self.plan.handle, _dev_ptr(vals, "float32", "vals") if vals.numel() else None,
+                                         _dev_ptr(X, "float32", "X"), int(F), self.layers,
+                                         self.bufs[0].data_ptr(),
+                                         self.bufs[1].data_ptr() if len(self.bufs) > 1 else None)
+        if not h:
+            _raise_last()
+        self._h = h
 
-    def _run(self):
-        cur = self.X
-        for layer in range(self.layers):
-            nxt = self.bufs[layer % len(self.bufs)]
-            self.plan.spmm(self.vals, cur, out=nxt, stream=self.stream)
-            cur = nxt
-        return cur
-
-    def replay(self):
-        """Launch the captured layers on the executor's stream; returns the output buffer
-        (valid once that stream has reached this point, e.g. after torch.cuda.synchronize())."""
-        torch = _torch()
-        with torch.cuda.stream(self.stream):
-            self.graph.replay()
+    def replay(self, stream=None):
+        """One launch of the captured layers on `stream` (default: the current torch stream);
+        returns the output buffer."""
+        _check(_lib.lib().agcn_graph_launch(self._h, _stream_handle(stream)))
         return self.out
 
     def close(self):
-        self.graph = None
-        if self.plan is not None:
+        if getattr(self, "_h", None):
+            h, self._h = self._h, None
+            _check(_lib.lib().agcn_graph_destroy(h))
+        if getattr(self, "plan", None) is not None:
             self.plan.close()
             self.plan = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -79,6 +79,12 @@ def lib():
     L.agcn_propagate_host.argtypes = [c_vp, c_vp, c_vp, c_i64, c_i64, c_vp, c_i32, c_i32, c_vp,
                                       ctypes.POINTER(Opts)]
     L.agcn_propagate_host.restype = c_i32
+    L.agcn_graph_create.argtypes = [c_vp, c_vp, c_vp, c_i32, c_i32, c_vp, c_vp]
+    L.agcn_graph_create.restype = c_vp
+    L.agcn_graph_launch.argtypes = [c_vp, c_vp]
+    L.agcn_graph_launch.restype = c_i32
+    L.agcn_graph_destroy.argtypes = [c_vp]
+    L.agcn_graph_destroy.restype = c_i32
     L.agcn_pipe_create.argtypes = [c_i32, ctypes.POINTER(Opts)]
     L.agcn_pipe_create.restype = c_vp
     L.agcn_pipe_submit.argtypes = [c_vp, c_vp, c_vp, c_vp, c_i64, c_i64, c_vp, c_i32, c_i32, c_vp]
@@ -119,5 +125,6 @@ EXPORTS = ["agcn_default_opts", "agcn_plan", "agcn_plan_ex", "agcn_spmm", "agcn_
            "agcn_spmm_ex", "agcn_plan_destroy",
            "agcn_plan_stats", "agcn_plan_copy", "agcn_auto_partition", "agcn_shard_bounds", "agcn_propagate_host",
            "agcn_pipe_create", "agcn_pipe_submit", "agcn_pipe_wait", "agcn_pipe_destroy",
+           "agcn_graph_create", "agcn_graph_launch", "agcn_graph_destroy",
            "agcn_transpose", "agcn_gather_vals", "agcn_gemm_xw", "agcn_device_alloc", "agcn_device_free", "agcn_ipc_export",
            "agcn_ipc_open", "agcn_ipc_close", "agcn_last_status", "agcn_last_error", "agcn_launch_count", "agcn_version"]

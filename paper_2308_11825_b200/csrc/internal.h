@@ -226,6 +226,7 @@ struct agcn_plan_s {
     agcn::ColSched sched;              // column-blocked schedule of the oversized rows (WIDE)
 
     size_t device_bytes = 0;
+    bool capturing = false;         // agcn_graph_create: SpMMs being captured (plan complete)
     cudaStream_t stream = nullptr;  // stream the plan was built on
     cudaEvent_t ready = nullptr;    // recorded on `stream` when the plan is complete
     cudaEvent_t last_use = nullptr; // recorded after an SpMM issued on a stream != `stream`

@@ -635,7 +635,7 @@ int num_sms() {
 void spmm_launch(agcn_plan_s* p, const float* vals, const float* X, int32_t F, float* Y,
                  cudaStream_t s, const agcn_spmm_opts_t& o) {
     if (p->n == 0) return;
-    const bool foreign = s != p->stream;
+    const bool foreign = s != p->stream && !p->capturing;  // (capture: the plan is complete)
     if (foreign) {  // plan built on another stream: wait for it; remember this use for destroy
         AGCN_CUDA(cudaStreamWaitEvent(s, p->ready, 0));
         if (!p->last_use) AGCN_CUDA(cudaEventCreateWithFlags(&p->last_use, cudaEventDisableTiming));

@@ -20,18 +20,16 @@ for name, F, layers in (("c1", 16, 2), ("c2", 64, 2), ("c3", 64, 2)):
     def eager():
         cur = X
         for _ in range(layers):
-            cur = p.spmm(va, cur, stream=g.stream)
+            cur = p.spmm(va, cur)
         return cur
 
     for fn, tag in ((eager, "eager"), (g.replay, "graph")):
-        with torch.cuda.stream(g.stream):
-            for _ in range(10):
-                fn()
+        for _ in range(10):
+            fn()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        with torch.cuda.stream(g.stream):
-            for _ in range(reps):
-                fn()
+        for _ in range(reps):
+            fn()
         torch.cuda.synchronize()
         print(f"{name} F={F} layers={layers} {tag}: {1e6 * (time.perf_counter() - t0) / reps:.1f} us per propagation")
     g.close()
