@@ -70,6 +70,10 @@ def test_argument_errors_without_device():
     assert L.agcn_pipe_submit(None, None, None, None, 4, 3, None, 4, 1, None) == 1
     assert L.agcn_pipe_wait(None) == 1
     assert L.agcn_pipe_destroy(None) == 0
+    assert not L.agcn_graph_create(None, None, None, 4, 2, None, None)
+    assert L.agcn_last_status() == 1
+    assert L.agcn_graph_launch(None, None) == 1
+    assert L.agcn_graph_destroy(None) == 0
 
 
 def test_auto_partition_rule():
