@@ -97,7 +97,8 @@ void agcn_default_opts(agcn_opts_t* opts);
  *   rowptr: DEVICE int32[n+1], non-decreasing; rowptr[0] may be nonzero (a row shard of a
  *           larger CSR) -- then colidx is indexed by the rowptr values (global arrays).
  *   colidx: DEVICE int32, entries rowptr[0] .. rowptr[n]-1 are read; 0 <= colidx < n_cols.
- *   n, nnz: rows of A and rowptr[n] - rowptr[0]; 0 <= n, 0 <= nnz < 2^31.
+ *   n, nnz: rows of A and rowptr[n] - rowptr[0]; 0 <= n, 0 <= nnz < 2^31.  nnz < 0 means
+ *           "read it from rowptr" (one extra readback of rowptr[0] and rowptr[n]).
  * Degree order is ascending and stable (ties keep original row order); degree-0 rows come
  * first and get no descriptor.  Step (3) of P:295 is the O(n) row-pointer update: the plan
  * stores the degree-sorted row pointer and, per sorted row, where its entries start in the

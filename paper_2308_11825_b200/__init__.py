@@ -101,8 +101,8 @@ class Plan:
         ci = _dev_ptr(colidx, "int32", "colidx") if colidx.numel() else 0
         if n is None:
             n = rowptr.numel() - 1
-        if nnz is None:
-            nnz = int(rowptr[-1].item() - rowptr[0].item()) if n >= 0 else 0
+        if nnz is None:  # agcn_plan_ex reads rowptr[0], rowptr[n] itself (one readback)
+            nnz = -1
         opts = _lib.Opts()
         L.agcn_default_opts(ctypes.byref(opts))
         opts.max_block_warps = max_block_warps

@@ -82,6 +82,15 @@ agcn_plan_t agcn_plan_ex(const int32_t* rowptr, const int32_t* colidx, int64_t n
     guarded([&] {
         agcn_opts_t o;
         if (opts) o = *opts; else agcn_default_opts(&o);
+        if (nnz < 0 && n >= 0 && rowptr) {  // "derive nnz": one readback of rowptr[0], rowptr[n]
+            int32_t ends[2];
+            cudaStream_t s = (cudaStream_t)o.stream;
+            AGCN_CUDA(cudaMemcpyAsync(ends, rowptr, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+            AGCN_CUDA(cudaMemcpyAsync(ends + 1, rowptr + n, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+            AGCN_CUDA(cudaStreamSynchronize(s));
+            nnz = (int64_t)ends[1] - ends[0];
+            AGCN_CHECK(nnz >= 0, AGCN_ERR_BAD_CSR, "rowptr[n] < rowptr[0]");
+        }
         out = build_plan(rowptr, colidx, n, nnz, o);
     });
     return out;
