@@ -100,6 +100,7 @@ struct WideArgs {
     const int32_t* ov_cs; // [n_ov + 1] first chunk of oversized row k
     int32_t* ov_cnt;      // [n_ov] chunks of row k finished (zero between launches)
     int64_t ov_start;     // sorted position of the first oversized row
+    int32_t lean;         // auto shape choice: U 2 at 4 CTAs/SM (see launch<L>)
 };
 
 
@@ -410,8 +411,10 @@ void launch(const WideArgs& a, bool keep, cudaStream_t s) {
     // register budget vs rows in flight (AGCN_WIDE_VARIANT, A/B only; profiles/r01k_wide_ab.md,
     // r01bc_kernel_shapes.md; the measured-and-dropped shapes -- U 4 at 4 CTAs/SM with spills,
     // U 2 at 5 CTAs/SM, U 8 at 2 CTAs/SM -- are no longer instantiated):
-    //   0: U 4 at 3 CTAs/SM (80 regs; the default)   4: U 2 at 4 CTAs/SM (64 regs)
-    static const int variant = env_int("AGCN_WIDE_VARIANT", 0);
+    //   0: U 4 at 3 CTAs/SM (80 regs)   4: U 2 at 4 CTAs/SM (64 regs)
+    //  -1 (default): 4 for mid-size graphs at F <= 64 (a.lean: C3 F32/F64 -5..9 %), else 0
+    static const int venv = env_int("AGCN_WIDE_VARIANT", -1);
+    const int variant = venv >= 0 ? venv : (a.lean ? 4 : 0);
     constexpr int U4 = L >= 4 ? 4 : L, U2 = L >= 2 ? 2 : L;
     if (variant == 4)
         launch_k<L, U2, 4>(a, keep, s);
@@ -442,6 +445,11 @@ void launch_wide(agcn_plan_s* p, const float* vals, const float* X, int32_t F, f
     a.ov_cs = p->ov_chunk_start;
     a.ov_cnt = p->ov_cnt;
     a.ov_start = p->ov_start;
+    {   // nnz per resident warp of the default shape: mid-size graphs (C3: 328) are latency-
+        // bound with few descriptors per warp, where 32 warps/SM at U 2 win (profiles r01bl)
+        const double share = (double)p->nnz / ((double)num_sms() * 24.0);
+        a.lean = F <= 64 && share >= 100.0 && share <= 4000.0;
+    }
     switch (F) {
         case 8: launch<1>(a, l2_keep, s); break;
         case 16: launch<2>(a, l2_keep, s); break;
