@@ -48,6 +48,7 @@ def parse():
     ap.add_argument("--col-block-mb", type=int, default=None,
                     help="None: auto; 0: off (paper chunks); MiB of X per column block")
     ap.add_argument("--e2e-steps", type=int, default=10)
+    ap.add_argument("--pipe-depth", type=int, default=2, help="e2e: agcn_pipe buffer slots")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="CPU-oracle sample budget")
     ap.add_argument("--ref-seconds", type=float, default=120.0,
                     help="--impl reference: total CPU budget over warm-up + timed steps")
@@ -644,7 +645,7 @@ def main():
             # the serving path: agcn_pipe_* overlaps job k's copy-in with job k-1's copy-out;
             # every job still copies its CSR + X in and its Y out (host wall clock, K jobs)
             Y_h2 = torch.empty((n, F), dtype=torch.float32).pin_memory()
-            with A.Pipeline(depth=2, max_block_warps=args.mbw, max_warp_nzs=args.mwn) as pipe:
+            with A.Pipeline(depth=args.pipe_depth, max_block_warps=args.mbw, max_warp_nzs=args.mwn) as pipe:
                 for Yo in (Y_h, Y_h2):                                        # warm-up (buffers)
                     pipe.submit(rp_h, ci_h, va_h, X_h, layers, out=Yo)
                 pipe.wait()
