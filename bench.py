@@ -40,13 +40,16 @@ def parse():
     ap.add_argument("--F", type=int, default=None)
     ap.add_argument("--layers", type=int, default=None)
     ap.add_argument("--partition", choices=["block", "warp"], default="block")
-    ap.add_argument("--kernel", choices=["auto", "general", "looped", "wide", "pipe"], default="auto")
+    ap.add_argument("--kernel", choices=["auto", "general", "looped", "wide"], default="auto")
     ap.add_argument("--mbw", type=int, default=12, help="Alg. 1 max_block_warps (P:318; paper: 12; "
                     "0 with --mwn 0: agcn_auto_partition's per-graph choice)")
     ap.add_argument("--mwn", type=int, default=32, help="Alg. 1 max_warp_nzs (P:318; SPEC default 32)")
-    ap.add_argument("--l2-hint", type=int, default=None, help="None: auto; 0: never; 1: always")
-    ap.add_argument("--col-block-mb", type=int, default=None,
-                    help="None: auto; 0: off (paper chunks); MiB of X per column block")
+    ap.add_argument("--l2-hint", default=None,
+                    choices=["auto", "none", "keep_all", "hot_window", "hot_hints"],
+                    help="agcn_l2_hint_t (default auto: hot_window for plans with hot rows)")
+    ap.add_argument("--hot-rows", type=int, default=None, help="agcn_opts_t.hot_rows (None: auto)")
+    ap.add_argument("--hot-mb", type=int, default=None, help="agcn_spmm_opts_t.hot_mb (None: device max)")
+    ap.add_argument("--chunk-shape", type=int, default=0, help="agcn_spmm_opts_t.chunk_shape (0: auto)")
     ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--pipe-depth", type=int, default=2, help="e2e: agcn_pipe buffer slots")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="CPU-oracle sample budget")
@@ -380,7 +383,8 @@ def main():
     X0 = torch.zeros((lay.padded_rows, F), dtype=torch.float32, device=dev)
     lay.pad(torch.from_numpy(X_host).to(dev), X0)
     bufs = [torch.empty_like(X0) for _ in range(min(layers, 2))]
-    plan_kw = dict(n_cols=n, max_block_warps=args.mbw, max_warp_nzs=args.mwn, partition=args.partition)
+    plan_kw = dict(n_cols=n, max_block_warps=args.mbw, max_warp_nzs=args.mwn, partition=args.partition,
+                   hot_rows=args.hot_rows)
     if P > 1:
         plan_kw.update(col_bounds=bounds, col_slot_rows=S)
 
@@ -431,7 +435,7 @@ def main():
             s0, s1 = ev(), ev()
             s0.record(stream)
             plan.spmm(va_d, Xin, out=out_rows, kernel=args.kernel, l2_hint=args.l2_hint,
-                      col_block_mb=args.col_block_mb, **epi_kw(Xin))
+                      hot_mb=args.hot_mb, chunk_shape=args.chunk_shape, **epi_kw(Xin))
             s1.record(stream)
             if record:
                 rec["spmm"].append((s0, s1))
@@ -440,7 +444,8 @@ def main():
                 s0, s1 = ev(), ev()
                 s0.record(stream)
                 plan.spmm(va_d, Xin, out=out_rows, kernel=args.kernel, l2_hint=args.l2_hint,
-                          col_block_mb=args.col_block_mb, peer_out=peer_out, **epi_kw(Xin))
+                          hot_mb=args.hot_mb, chunk_shape=args.chunk_shape, peer_out=peer_out,
+                          **epi_kw(Xin))
                 s1.record(stream)
                 if record:
                     rec["spmm"].append((s0, s1))
@@ -533,7 +538,6 @@ def main():
                          "traffic_gbs": traffic / (spmm_max * 1e-3) / 1e9 if traffic else None,
                          "traffic_frac": traffic / (spmm_max * 1e-3) / 1e9 / peaks["hbm_gbs"] if traffic else None,
                          "kernel": "agcn_spmm (%s + k_ov_reduce)" % (
-                             "k_spmm_pipe" if args.kernel == "pipe" else
                              "k_spmm_wide" if args.kernel in ("auto", "wide") and F in (8, 16, 32, 64, 128, 256)
                              else "k_spmm_block"),
                          "bytes_per_launch": b_comp, "peak_source": peaks["source"],
@@ -552,7 +556,7 @@ def main():
                 plan_g = A.Plan(rp_local, ci_d, stream=S, **plan_kw)
                 Yg = torch.empty((n, F), dtype=torch.float32, device=dev)
                 run = lambda: plan_g.spmm(va_d, X0, out=Yg, stream=S, kernel=args.kernel,  # noqa: E731
-                                          l2_hint=args.l2_hint, col_block_mb=args.col_block_mb,
+                                          l2_hint=args.l2_hint, hot_mb=args.hot_mb, chunk_shape=args.chunk_shape,
                                           **epi_kw(X0))
                 for _ in range(3):
                     run()

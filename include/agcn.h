@@ -65,6 +65,16 @@ typedef struct {
     const int64_t* col_bounds;
     int32_t col_nparts;
     int64_t col_slot_rows;
+    /* Hot X rows (north_star: "an L2 access-policy window keeping hot X rows resident"): the
+       plan marks the hot_rows highest-degree vertices -- the tail of the degree order it has
+       just computed -- as hot, and agcn_spmm gathers their X rows into a compact
+       plan-owned buffer that an L2 persisting window (or evict_last hints) keeps resident.
+       Row degree stands in for column in-degree (correlation 0.997-0.9997 on the power-law
+       configs, profiles/r02_c5_roof.md).  Needs a square A (n_cols == n) without col_bounds.
+       -1 (default): auto -- min(n, 262144) when n >= 2^19 (X of 128+ MiB at F = 64), else 0;
+       0: off; > 0: that many rows (capped at the rows of degree >= 1).  Results do not depend
+       on it.  Costs the plan one lookup per nonzero (C5: +0.4 ms). */
+    int64_t hot_rows;
 } agcn_opts_t;
 
 typedef struct {
@@ -78,6 +88,7 @@ typedef struct {
     int64_t n_oversized_blocks; /* descriptors of those rows (chunks of <= deg_bound nnz) */
     int32_t max_block_warps, max_warp_nzs, partition, reserved;
     size_t device_bytes;        /* device memory owned by the plan */
+    int64_t hot_rows;           /* hot X rows (agcn_opts_t.hot_rows as resolved) */
 } agcn_plan_stats_t;
 
 typedef enum {
@@ -100,11 +111,12 @@ void agcn_default_opts(agcn_opts_t* opts);
  *   n, nnz: rows of A and rowptr[n] - rowptr[0]; 0 <= n, 0 <= nnz < 2^31.  nnz < 0 means
  *           "read it from rowptr" (one extra readback of rowptr[0] and rowptr[n]).
  * Degree order is ascending and stable (ties keep original row order); degree-0 rows come
- * first and get no descriptor.  Step (3) of P:295 is the O(n) row-pointer update: the plan
- * stores the degree-sorted row pointer and, per sorted row, where its entries start in the
- * caller's arrays; it does NOT copy colidx.  Ownership: rowptr may be freed after return;
- * colidx is BORROWED and must stay valid and unchanged until agcn_plan_destroy (like a
- * cuSPARSE CSR descriptor).  The AGCN_PARTITION_WARP plan copies colidx.  Synchronises the
+ * first and get no descriptor.  Step (3) of P:295 reorders the CSR: the plan stores the
+ * degree-sorted row pointer, per sorted row where its entries start in the caller's vals,
+ * and its own degree-sorted copy of colidx (so every block's column indices are contiguous;
+ * hot columns re-encoded, see hot_rows).  Ownership: the plan copies what it needs --
+ * rowptr and colidx may be freed or changed after return.  The
+ * AGCN_PARTITION_WARP plan copies colidx in the original order.  Synchronises the
  * plan stream once mid-way (bucket counts, validation flags); the last kernels run
  * asynchronously on opts.stream, and agcn_spmm on another stream waits for them (event).
  * Block plans of graphs with n <= 32768, nnz <= 2^20, deg_bound <= 512 and at most 1024
@@ -140,11 +152,23 @@ typedef enum {
     AGCN_KERNEL_LOOPED = 2,  /* ablation 2 of the paper (Fig. 4(a), Table II):
                                 no combined warp -- GENERAL with one warp of 32 scalar lanes per
                                 row that loops over the columns in strides of 32; any F */
-    AGCN_KERNEL_WIDE = 3,    /* F = 8 L <= 256 (any L), 32-B aligned X/Y, max_block_warps
+    AGCN_KERNEL_WIDE = 3     /* F = 8 L <= 256 (any L), 32-B aligned X/Y, max_block_warps
                                 <= 32: one 256-bit row slice per lane, shuffle-broadcast CSR */
-    AGCN_KERNEL_PIPE = 4     /* F in {32,64,128,256}, 32-B aligned X/Y, max_block_warps <= 32:
-                                as WIDE, X rows gathered through a cp.async shared-memory ring */
 } agcn_kernel_t;
+
+typedef enum {
+    AGCN_L2_AUTO = -1,
+    AGCN_L2_NONE = 0,       /* plain X-row loads */
+    AGCN_L2_KEEP_ALL = 1,   /* every X-row load L2::evict_last (X that fits in L2) */
+    AGCN_L2_HOT_WINDOW = 2, /* the hot buffer read under an L2 access-policy window (hitProp
+                               persisting) over it; raises the DEVICE-WIDE persisting-L2 limit
+                               (cudaLimitPersistingL2CacheSize) to the window size the first
+                               time, which shrinks L2 for all later normal accesses of the
+                               process (measured: other SpMMs 10-15 % slower).  The buffer's
+                               lines are discarded from L2 after the SpMM.  Plans without hot
+                               rows: NONE */
+    AGCN_L2_HOT_HINTS = 3   /* hot buffer loads L2::evict_last, cold loads evict_first */
+} agcn_l2_hint_t;
 
 typedef enum {
     AGCN_AGG_SUM = 0,  /* y_i = sum_j a_ij x_j (GCN aggregation) */
@@ -153,16 +177,13 @@ typedef enum {
 
 typedef struct {
     int32_t kernel;       /* agcn_kernel_t; default AGCN_KERNEL_AUTO */
-    int32_t l2_hint;      /* X-row L2 residency: -1 (default) evict_last hints when X fits in L2
-                             (<= 128 MiB), 0 never, 1 always */
-    int32_t col_block_mb; /* WIDE kernel, rows of degree > deg_bound: execute them as pieces cut
-                             at column blocks of this many MiB of X, block by block, so the X
-                             slice being gathered stays in L2 (results unchanged: fixed-order
-                             partial sums; applies to rows of degree >= 2048 when X is larger
-                             than one block).  -1 (default) and 0: off (the paper's deg_bound
-                             chunks; measured faster on B200); > 0: MiB per block.
-                             Builds a plan-owned schedule on first use per F (stream-ordered,
-                             no host synchronisation). */
+    int32_t l2_hint;      /* X-row L2 residency (agcn_l2_hint_t; results never depend on it).
+                             Plans with hot rows always read them from the compact buffer;
+                             AGCN_L2_AUTO (default): KEEP_ALL when X fits in L2 (<= 128 MiB) and
+                             the plan has no hot rows, else NONE (profiles/r02_c5_roof.md) */
+    int32_t hot_mb;       /* HOT_* modes: MiB of hot X rows kept resident (rows = hot_mb MiB /
+                             (4 F), at most the plan's hot_rows); 0 (default): the device's
+                             maximum persisting-L2 size */
     /* Epilogue, applied to every output row i (fused into the WIDE kernel's stores and the
        oversized-row reduction; a separate pass over Y for the other kernels):
          y_i = agg(i) + self_scale * self[i] + bias;  y_i = max(y_i, 0) if relu
@@ -180,7 +201,12 @@ typedef struct {
        caller orders the peers' reads (e.g. a barrier after the layer). */
     float* peer_out[8];
     int32_t npeer;        /* 0 (default) .. 8 */
-    int32_t pad_;
+    /* WIDE kernel, plans with more than 16384 oversized-row chunks: the chunks run in a kernel
+       of their own (k_spmm_chunks) before the other descriptors.  0 (default): auto (F >= 128:
+       U 4 rows in flight per lane at 4 CTAs/SM; else off); -1: off (one kernel for every
+       descriptor); 3, 4: U 4 at that many CTAs/SM; 6: U 2 at 6 CTAs/SM.  Results are bitwise
+       the same. */
+    int32_t chunk_shape;
     int64_t reserved[2];
 } agcn_spmm_opts_t;
 

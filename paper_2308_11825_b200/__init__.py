@@ -95,7 +95,7 @@ class Plan:
     def __init__(self, rowptr, colidx, n: int | None = None, nnz: int | None = None, *,
                  n_cols: int | None = None, max_block_warps: int = 12, max_warp_nzs: int = 32,
                  partition: str = "block", col_bounds=None, col_slot_rows: int | None = None,
-                 stream=None):
+                 hot_rows: int | None = None, stream=None):
         L = _lib.lib()
         rp = _dev_ptr(rowptr, "int32", "rowptr")
         ci = _dev_ptr(colidx, "int32", "colidx") if colidx.numel() else 0
@@ -110,6 +110,7 @@ class Plan:
         opts.partition = {"block": 0, "warp": 1}[partition]
         opts.n_cols = 0 if n_cols is None else int(n_cols)
         opts.stream = _stream_handle(stream)
+        opts.hot_rows = -1 if hot_rows is None else int(hot_rows)
         self._bounds_keep = None
         if col_bounds is not None:
             b = np.ascontiguousarray(col_bounds, dtype=np.int64)
@@ -121,7 +122,6 @@ class Plan:
         if not h:
             _raise_last()
         self._h = h
-        self._colidx = colidx  # the plan borrows colidx (read by every spmm): keep it alive
         self.partition = partition
         st = self.stats()
         self.n, self.n_cols, self.nnz = st["n"], st["n_cols"], st["nnz"]
@@ -149,15 +149,16 @@ class Plan:
                                          out.ctypes.data or None, out.nbytes))
         return out
 
-    def spmm(self, vals, X, out=None, stream=None, kernel: str = "auto", l2_hint: int | None = None,
-             col_block_mb: int | None = None, aggregation: str = "sum", self_x=None,
-             self_scale: float = 0.0, bias=None, relu: bool = False, peer_out=()):
+    def spmm(self, vals, X, out=None, stream=None, kernel: str = "auto", l2_hint=None,
+             hot_mb: int | None = None, aggregation: str = "sum", self_x=None,
+             self_scale: float = 0.0, bias=None, relu: bool = False, peer_out=(), chunk_shape: int = 0):
         """Y = A.X (asynchronous on `stream`, default the current torch stream).
 
-        kernel: "auto" | "general" | "wide" (agcn_kernel_t); l2_hint: None (auto: evict_last
-        hints on X rows when X fits in L2), 0 (never) or 1 (always).  col_block_mb: None (auto),
-        0 (off: the paper's deg_bound chunks for oversized rows) or the X slice per column block
-        in MiB (agcn_spmm_opts_t.col_block_mb).
+        kernel: "auto" | "general" | "looped" | "wide" (agcn_kernel_t).  l2_hint
+        (agcn_l2_hint_t): None / "auto", "none", "keep_all" (evict_last on every X row),
+        "hot_window" (the plan's hot rows in a compact buffer under a persisting L2 window),
+        "hot_hints" (same buffer, evict_last / evict_first hints).  hot_mb: MiB of hot rows
+        kept resident (None: the device's persisting-L2 maximum).
         Epilogue (agcn_spmm_opts_t): y_i = agg_i + self_scale * self_x[i] + bias, then ReLU if
         relu; aggregation "sum" (GCN) or "mean" (GraphSAGE-mean, / deg_i); GIN: self_x = X,
         self_scale = 1 + eps.
@@ -173,8 +174,8 @@ class Plan:
         v = _dev_ptr(vals, "float32", "vals") if vals.numel() else 0
         x = _dev_ptr(X, "float32", "X") if X.numel() else 0
         y = _dev_ptr(out, "float32", "out") if out.numel() else 0
-        opts = _spmm_opts(kernel, l2_hint, col_block_mb, aggregation, self_x, self_scale, bias, relu,
-                          shape=(self.n, F), peer_out=peer_out)
+        opts = _spmm_opts(kernel, l2_hint, hot_mb, aggregation, self_x, self_scale, bias, relu,
+                          shape=(self.n, F), peer_out=peer_out, chunk_shape=chunk_shape)
         _check(_lib.lib().agcn_spmm_ex(self.handle, v or None, x or None, int(F), y or None,
                                        _stream_handle(stream), opts))
         return out
@@ -197,14 +198,15 @@ class Plan:
         self.close()
 
 
-def _spmm_opts(kernel: str = "auto", l2_hint: int | None = None, col_block_mb: int | None = None,
+def _spmm_opts(kernel: str = "auto", l2_hint=None, hot_mb: int | None = None,
                aggregation: str = "sum", self_x=None, self_scale: float = 0.0, bias=None,
-               relu: bool = False, shape=None, peer_out=()):
+               relu: bool = False, shape=None, peer_out=(), chunk_shape: int = 0):
     o = _lib.SpmmOpts()
     _lib.lib().agcn_default_spmm_opts(ctypes.byref(o))
     o.kernel = _lib.KERNELS[kernel]
-    o.l2_hint = -1 if l2_hint is None else int(l2_hint)
-    o.col_block_mb = -1 if col_block_mb is None else int(col_block_mb)
+    o.l2_hint = _lib.L2_HINTS[l2_hint] if l2_hint is None or isinstance(l2_hint, str) else int(l2_hint)
+    o.hot_mb = 0 if hot_mb is None else int(hot_mb)
+    o.chunk_shape = int(chunk_shape)
     o.aggregation = {"sum": 0, "mean": 1}[aggregation]
     o.relu = int(bool(relu))
     o.self_scale = float(self_scale)
@@ -238,12 +240,12 @@ def agcn_spmm(plan: Plan, vals, X, F: int, Y, stream=None) -> None:
 
 
 def agcn_spmm_ex(plan: Plan, vals, X, F: int, Y, stream=None, kernel: str = "auto",
-                 l2_hint: int | None = None, col_block_mb: int | None = None) -> None:
+                 l2_hint=None, hot_mb: int | None = None) -> None:
     v = _dev_ptr(vals, "float32", "vals") if vals.numel() else 0
     x = _dev_ptr(X, "float32", "X") if X.numel() else 0
     y = _dev_ptr(Y, "float32", "Y") if Y.numel() else 0
     _check(_lib.lib().agcn_spmm_ex(plan.handle, v or None, x or None, int(F), y or None,
-                                   _stream_handle(stream), _spmm_opts(kernel, l2_hint, col_block_mb)))
+                                   _stream_handle(stream), _spmm_opts(kernel, l2_hint, hot_mb)))
 
 
 def transpose(rowptr, colidx, n_cols: int, stream=None):

@@ -19,17 +19,19 @@ class Opts(ctypes.Structure):
     _fields_ = [("max_block_warps", c_i32), ("max_warp_nzs", c_i32), ("partition", c_i32),
                 ("validate", c_i32), ("n_cols", c_i64), ("stream", c_vp),
                 ("col_bounds", ctypes.POINTER(c_i64)), ("col_nparts", c_i32),
-                ("col_slot_rows", c_i64)]
+                ("col_slot_rows", c_i64), ("hot_rows", c_i64)]
 
 
-KERNELS = {"auto": 0, "general": 1, "looped": 2, "wide": 3, "pipe": 4}
+KERNELS = {"auto": 0, "general": 1, "looped": 2, "wide": 3}
+L2_HINTS = {None: -1, "auto": -1, "none": 0, 0: 0, "keep_all": 1, 1: 1, "hot_window": 2, 2: 2,
+            "hot_hints": 3, 3: 3}
 
 
 class SpmmOpts(ctypes.Structure):
-    _fields_ = [("kernel", c_i32), ("l2_hint", c_i32), ("col_block_mb", c_i32),
+    _fields_ = [("kernel", c_i32), ("l2_hint", c_i32), ("hot_mb", c_i32),
                 ("aggregation", c_i32), ("self_scale", ctypes.c_float), ("relu", c_i32),
                 ("self", c_vp), ("bias", c_vp), ("peer_out", c_vp * 8), ("npeer", c_i32),
-                ("pad_", c_i32), ("reserved", c_i64 * 2)]
+                ("chunk_shape", c_i32), ("reserved", c_i64 * 2)]
 
 
 class Stats(ctypes.Structure):
@@ -38,7 +40,7 @@ class Stats(ctypes.Structure):
                 ("n_zero_rows", c_i64), ("n_oversized_rows", c_i64),
                 ("n_oversized_blocks", c_i64), ("max_block_warps", c_i32),
                 ("max_warp_nzs", c_i32), ("partition", c_i32), ("reserved", c_i32),
-                ("device_bytes", c_size)]
+                ("device_bytes", c_size), ("hot_rows", c_i64)]
 
 
 _lib = None

@@ -74,6 +74,7 @@ void agcn_default_opts(agcn_opts_t* o) {
     o->max_warp_nzs = 32;
     o->partition = AGCN_PARTITION_BLOCK;
     o->validate = 1;
+    o->hot_rows = -1;
 }
 
 agcn_plan_t agcn_plan_ex(const int32_t* rowptr, const int32_t* colidx, int64_t n, int64_t nnz,
@@ -104,8 +105,8 @@ void agcn_default_spmm_opts(agcn_spmm_opts_t* o) {
     if (!o) return;
     std::memset(o, 0, sizeof(*o));
     o->kernel = AGCN_KERNEL_AUTO;
-    o->l2_hint = -1;
-    o->col_block_mb = -1;
+    o->l2_hint = AGCN_L2_AUTO;
+    o->hot_mb = 0;
 }
 
 agcn_status_t agcn_spmm_ex(agcn_plan_t plan, const float* vals, const float* X, int32_t F, float* Y,
@@ -115,10 +116,13 @@ agcn_status_t agcn_spmm_ex(agcn_plan_t plan, const float* vals, const float* X, 
         AGCN_CHECK(F > 0, AGCN_ERR_INVALID_ARG, "F must be > 0");
         agcn_spmm_opts_t o;
         if (opts) o = *opts; else agcn_default_spmm_opts(&o);
-        AGCN_CHECK(o.kernel >= AGCN_KERNEL_AUTO && o.kernel <= AGCN_KERNEL_PIPE, AGCN_ERR_INVALID_ARG,
+        AGCN_CHECK(o.kernel >= AGCN_KERNEL_AUTO && o.kernel <= AGCN_KERNEL_WIDE, AGCN_ERR_INVALID_ARG,
                    "unknown kernel");
-        AGCN_CHECK(o.l2_hint >= -1 && o.l2_hint <= 1, AGCN_ERR_INVALID_ARG, "l2_hint must be -1, 0 or 1");
-        AGCN_CHECK(o.col_block_mb >= -1, AGCN_ERR_INVALID_ARG, "col_block_mb must be >= -1");
+        AGCN_CHECK(o.l2_hint >= AGCN_L2_AUTO && o.l2_hint <= AGCN_L2_HOT_HINTS, AGCN_ERR_INVALID_ARG,
+                   "l2_hint must be -1 .. 3 (agcn_l2_hint_t)");
+        AGCN_CHECK(o.hot_mb >= 0, AGCN_ERR_INVALID_ARG, "hot_mb must be >= 0");
+        AGCN_CHECK(o.chunk_shape == -1 || o.chunk_shape == 0 || o.chunk_shape == 3 || o.chunk_shape == 4 ||
+                       o.chunk_shape == 6, AGCN_ERR_INVALID_ARG, "chunk_shape must be -1, 0, 3, 4 or 6");
         AGCN_CHECK(o.aggregation == AGCN_AGG_SUM || o.aggregation == AGCN_AGG_MEAN, AGCN_ERR_INVALID_ARG,
                    "unknown aggregation");
         AGCN_CHECK(o.self_scale == 0.f || o.self != nullptr, AGCN_ERR_INVALID_ARG,
@@ -180,9 +184,8 @@ agcn_status_t agcn_plan_stats(agcn_plan_t plan, agcn_plan_stats_t* out) {
         out->max_warp_nzs = plan->mwn;
         out->partition = plan->partition;
         out->device_bytes = plan->device_bytes + plan->ov_partial_floats * sizeof(float) +
-                            plan->sched.partial_floats * sizeof(float) +
-                            (size_t)plan->sched.cap * sizeof(int4) +
-                            (plan->sched.slot_base ? sizeof(int32_t) * (size_t)(plan->n_ov + 1) : 0);
+                            plan->xhot_floats * sizeof(float);
+        out->hot_rows = plan->n_hot;
     });
 }
 
@@ -205,7 +208,7 @@ agcn_status_t agcn_plan_copy(agcn_plan_t plan, int32_t field, void* host_dst, si
         AGCN_CHECK(is_task ? !blk : blk, AGCN_ERR_INVALID_ARG, "field not present for this partition");
         AGCN_CHECK(bytes == want, AGCN_ERR_INVALID_ARG,
                    "bytes must equal the field size (" + std::to_string(want) + ")");
-        if (field == AGCN_FIELD_SORTED_COLIDX) {  // not stored: materialised on demand
+        if (field == AGCN_FIELD_SORTED_COLIDX) {  // hot encoding undone on the way
             plan_copy_sorted_colidx(plan, static_cast<int32_t*>(host_dst));
             return;
         }

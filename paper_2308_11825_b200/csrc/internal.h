@@ -174,20 +174,8 @@ struct PlanFlags {          // device-written, read back once (validation + size
     int64_t ov_chunks_heavy;  // the part of ov_chunks from rows of degree >= kColBlockMinDeg
 };
 
-// Column-blocked execution schedule of the oversized rows (sched.cu), per block width.
 constexpr int32_t kHeavyChunks = 16;     // oversized rows above this many chunks: CTA-wide merge
-constexpr int32_t kColBlockMinDeg = 2048;  // rows of at least this degree are cut at blocks
-constexpr int32_t kMaxPieces = 16;         // pieces per deg_bound chunk at most
-struct ColSched {
-    int shift = -1;              // column block = column >> shift (-1: not built)
-    int32_t nb = 0;              // column blocks
-    int32_t F = 0;               // F the partial buffer is sized for
-    int64_t cap = 0;             // capacity in pieces (upper bound of the piece count)
-    int4* seg = nullptr;         // [cap] pieces {-1 - slot, first entry, 0, length}, block-major
-    int32_t* slot_base = nullptr;  // [n_ov + 1] first slot of oversized row k; [n_ov] = #pieces
-    float* partial = nullptr;    // [cap][F] partial rows
-    size_t partial_floats = 0, partial_need = 0;
-};
+constexpr int32_t kColBlockMinDeg = 2048;  // (statistics only: chunks of rows at least this long)
 
 }  // namespace agcn
 
@@ -206,10 +194,15 @@ struct agcn_plan_s {
     int32_t* perm = nullptr;           // [n]   sorted position -> original row
     int32_t* sorted_rowptr = nullptr;  // [n+1] row pointer of the degree-sorted CSR (P:295 (3))
     int32_t* row_src_off = nullptr;    // [n]   rowptr[perm[k]] - rowptr[0]
-    const int32_t* colidx = nullptr;   // BORROWED caller colidx (indexed by rowptr values)
-    const int32_t* cols = nullptr;     // what the SpMM reads, indexed like vals (rowptr-relative):
-                                       // colidx + rp_base, or cols_copy when relabelled
-    int32_t* cols_copy = nullptr;      // [nnz] plan-owned relabelled colidx (padded layout only)
+    // plan-owned column indices (the plan copies colidx):
+    int32_t* scols = nullptr;          // BLOCK: [nnz] colidx of the degree-sorted CSR (P:295 (3));
+                                       // descriptor {d, loc, ..} reads scols[loc ..]; padded-layout
+                                       // relabel applied; hot column -> -1 - slot
+    int32_t* cols_copy = nullptr;      // WARP: [nnz] colidx in the original order (rowptr-relative)
+    int64_t n_hot = 0;                 // hot X rows (the n_hot highest-degree vertices, square A)
+    int32_t* hot_cols = nullptr;       // [n_hot] column of hot slot k (slots in column order)
+    float* xhot = nullptr;             // SpMM scratch: X rows of the hot slots [n_hot][F]
+    size_t xhot_floats = 0;
     agcn::ColMap cmap{};               // optional padded-layout column relabel
     int4* desc = nullptr;              // [nblocks]
     int32_t* ov_chunk_start = nullptr; // [n_ov + 1]
@@ -223,7 +216,6 @@ struct agcn_plan_s {
     float* ov_partial = nullptr;
     size_t ov_partial_floats = 0;
     int32_t* ov_cnt = nullptr;         // [n_ov] finished-chunk counters of the fused level 3 (zero at rest)
-    agcn::ColSched sched;              // column-blocked schedule of the oversized rows (WIDE)
 
     size_t device_bytes = 0;
     bool capturing = false;         // agcn_graph_create: SpMMs being captured (plan complete)
@@ -237,11 +229,13 @@ void spmm_launch(agcn_plan_s* p, const float* vals, const float* X, int32_t F, f
                  cudaStream_t s, const agcn_spmm_opts_t& o);
 // spmm_wide.cu: 256-bit-per-lane kernel for F = 8 L <= 256
 bool wide_supported(const agcn_plan_s* p, const float* X, const float* Y, int32_t F);
-void launch_wide(agcn_plan_s* p, const float* vals, const float* X, int32_t F, float* Y,
-                 bool l2_keep, bool blocked, bool fuse_ov, const Epi& epi, cudaStream_t s);
-// spmm_pipe.cu: cp.async shared-memory gather pipeline, F in {32,64,128,256}
-bool pipe_supported(const agcn_plan_s* p, const float* X, const float* Y, int32_t F);
-void launch_pipe(agcn_plan_s* p, const float* vals, const float* X, int32_t F, float* Y, cudaStream_t s);
+// l2: agcn_l2_hint_t resolved (NONE / KEEP_ALL / HOT_WINDOW / HOT_HINTS); Xh: the hot rows
+// (plans with n_hot > 0); win_bytes: the persisting window over Xh (HOT_WINDOW)
+void launch_wide(agcn_plan_s* p, const float* vals, const float* X, const float* Xh, int32_t F, float* Y,
+                 int l2, size_t win_bytes, bool fuse_ov, int chunk_shape, const Epi& epi, cudaStream_t s);
+// spmm.cu: set the device's persisting-L2 limit to at least `bytes` (once per device and size);
+// returns the window size usable (0 if the device refuses)
+size_t ensure_persisting_l2(size_t bytes);
 // plan.cu: stable LSD radix sort of (key, val) pairs (8-bit digits); result in ka/va
 void radix_sort_pairs(int32_t*& ka, int32_t*& va, int32_t*& kb, int32_t*& vb, int64_t m, int64_t max_key,
                       cudaStream_t s);
@@ -252,9 +246,5 @@ void gemm_xw_tf32(const float* X, int64_t M, int32_t K, const float* Wt, int32_t
 void transpose_csr(const int32_t* rowptr, const int32_t* colidx, int64_t n, int64_t n_cols, int64_t nnz,
                    int32_t* rowptr_t, int32_t* colidx_t, int32_t* src, cudaStream_t s);
 void gather_vals(const float* vals, const int32_t* src, int64_t nnz, float* out, cudaStream_t s);
-// sched.cu
-int col_sched_shift(const agcn_plan_s* p, int32_t F, double target_bytes);
-void build_col_sched(agcn_plan_s* p, int shift, int32_t F, cudaStream_t s);
-void free_col_sched(ColSched& cs, cudaStream_t s);
 int num_sms();
 }  // namespace agcn

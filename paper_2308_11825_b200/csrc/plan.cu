@@ -225,16 +225,98 @@ __global__ void k_validate_cols(const int32_t* __restrict__ rowptr, const int32_
     if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) flags->bad_colidx = 1;
 }
 
-// Introspection only (agcn_plan_copy(AGCN_FIELD_SORTED_COLIDX)): materialise the colidx of the
-// degree-sorted CSR, one warp per sorted row.  Not on the plan / SpMM path (the SpMM reads
-// the caller's colidx through row_src_off).
-__global__ void k_gather_sorted_cols(int64_t n, const int32_t* __restrict__ sorted_rowptr,
-                                     const int32_t* __restrict__ rso,
-                                     const int32_t* __restrict__ cols, int32_t* __restrict__ out) {
-    const int64_t k = (int64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
-    if (k >= n) return;
-    const int32_t dst = sorted_rowptr[k], d = sorted_rowptr[k + 1] - dst, src = rso[k];
-    for (int32_t j = threadIdx.x & 31; j < d; j += 32) out[dst + j] = cols[src + j];
+// (3) continued: the plan's own colidx of the degree-sorted CSR.  Every descriptor is a
+// contiguous run [loc, loc + rows * deg) of the sorted CSR (chunk: [loc, loc + info)), its rows
+// starting at row_src_off in the caller's colidx; one warp copies one descriptor, 4 entries per
+// lane in flight.  On the way: the padded-layout relabel (ColMap, multi-GPU) or the hot-column
+// encoding c -> -1 - slot, slot = rank of c among the hot columns, from one 8-byte entry
+// {bitmap word, exclusive popcount prefix} per 32 columns (n_cols / 4 bytes, L2-resident).
+// Out-of-range columns are copied unchanged (the plan is rejected by the validation flags
+// before use; with validation off the caller guarantees the range).
+__device__ __forceinline__ int32_t encode_col(int32_t c, int64_t n_cols, const ColMap& cm,
+                                              const uint2* __restrict__ hot) {
+    if (cm.nparts > 0) return map_col(c, cm);
+    if (hot && c >= 0 && (int64_t)c < n_cols) {
+        const uint2 w = __ldg(hot + (c >> 5));
+        const uint32_t bit = 1u << (c & 31);
+        if (w.x & bit) return -1 - (int32_t)(w.y + __popc(w.x & (bit - 1)));
+    }
+    return c;
+}
+
+__global__ void k_sorted_cols(const int4* __restrict__ desc, int64_t nblocks, int32_t db,
+                              const int32_t* __restrict__ srp, const int32_t* __restrict__ rso,
+                              const int32_t* __restrict__ cols, int64_t n_cols, ColMap cm,
+                              const uint2* __restrict__ hot, int32_t* __restrict__ out) {
+    const int lane = threadIdx.x & 31;
+    const int64_t W = (int64_t)gridDim.x * (blockDim.x / 32);
+    for (int64_t b = (int64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5); b < nblocks; b += W) {
+        const int4 m = __ldg(desc + b);
+        const bool ov = m.x > db;
+        const int32_t d = ov ? m.w : m.x;
+        const int32_t total = ov ? m.w : (m.w & 0xffff) * d;
+        const int32_t src0 = ov ? __ldg(rso + m.z) + (m.y - __ldg(srp + m.z)) : 0;
+        const float rd = __frcp_rn((float)d);  // e / d exactly (e < 2^15, see spmm_wide.cu)
+        for (int32_t e0 = 0; e0 < total; e0 += 128) {
+            int32_t c[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const int32_t e = e0 + k * 32 + lane;
+                c[k] = 0;
+                if (e < total) {
+                    int32_t src = src0 + e;
+                    if (!ov) {
+                        const int32_t i = __float2int_rz(__fmul_rn((float)e + 0.5f, rd));
+                        src = __ldg(rso + m.z + i) + (e - i * d);
+                    }
+                    c[k] = __ldcs(cols + src);
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const int32_t e = e0 + k * 32 + lane;
+                if (e < total) __stcs(out + (int64_t)m.y + e, encode_col(c[k], n_cols, cm, hot));
+            }
+        }
+    }
+}
+
+// hot vertices: the H highest-degree ones (sorted positions n - H .. n - 1) -> column bitmap
+// (hot[w].x), then per-word popcounts (hot[w].y) turned into exclusive prefixes by a scan
+__global__ void k_hot_bits(const int32_t* __restrict__ perm, int64_t n, int64_t H, uint2* __restrict__ hot) {
+    const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k < H) {
+        const int32_t c = perm[n - 1 - k];
+        atomicOr(&hot[c >> 5].x, 1u << (c & 31));
+    }
+}
+__global__ void k_popc_words(const uint2* __restrict__ hot, int64_t nw, int32_t* __restrict__ cnt) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < nw) cnt[i] = __popc(hot[i].x);
+}
+// hot[w].y = prefix[w]; hot_cols[slot] = column of hot slot `slot` (slots in column order)
+__global__ void k_hot_list(uint2* __restrict__ hot, const int32_t* __restrict__ pre, int64_t nw,
+                           int32_t* __restrict__ hot_cols) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= nw) return;
+    uint32_t w = hot[i].x;
+    int32_t k = pre[i];
+    hot[i].y = (uint32_t)k;
+    while (w) {
+        const int b = __ffs(w) - 1;
+        hot_cols[k++] = (int32_t)(i * 32 + b);
+        w &= w - 1;
+    }
+}
+
+// Introspection (agcn_plan_copy(AGCN_FIELD_SORTED_COLIDX)): the plan's sorted colidx with the
+// hot encoding undone.
+__global__ void k_decode_hot(const int32_t* __restrict__ sc, int64_t nnz, const int32_t* __restrict__ hot_cols,
+                             int32_t* __restrict__ out) {
+    for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < nnz; q += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t c = sc[q];
+        out[q] = c >= 0 ? c : hot_cols[-1 - c];
+    }
 }
 
 // ---------------------------------------------------------------- (5) Algorithm 2 emission
@@ -402,13 +484,9 @@ void validate_cols(const int32_t* rowptr, const int32_t* colidx, int64_t nnz, in
     post_launch();
 }
 
-// The column array the SpMM reads (indexed like vals, rowptr-relative): the caller's colidx,
-// or -- for a padded multi-GPU layout -- a plan-owned relabelled copy (one flat pass).
-void set_spmm_cols(agcn_plan_s* p, const int32_t* colidx, cudaStream_t s) {
-    if (p->cmap.nparts <= 0) {
-        p->cols = colidx + p->rp_base;
-        return;
-    }
+// WARP plan: the plan's copy of colidx in the original order (rowptr-relative), relabelled for
+// a padded multi-GPU layout (one flat pass).
+void copy_cols_original(agcn_plan_s* p, const int32_t* colidx, cudaStream_t s) {
     p->cols_copy = dalloc<int32_t>(p->nnz, s);
     p->device_bytes += sizeof(int32_t) * (size_t)p->nnz;
     if (p->nnz > 0) {
@@ -416,7 +494,43 @@ void set_spmm_cols(agcn_plan_s* p, const int32_t* colidx, cudaStream_t s) {
             colidx + p->rp_base, p->nnz, p->cols_copy, p->cmap);
         post_launch();
     }
-    p->cols = p->cols_copy;
+}
+
+// Hot rows of a plan (agcn_opts_t.hot_rows): square A without a padded layout only.
+int64_t hot_rows_for(const agcn_plan_s* p, int64_t req) {
+    if (p->n_cols != p->n || p->cmap.nparts > 0 || req == 0) return 0;
+    const int64_t live = p->n - p->n_zero;  // vertices of degree >= 1
+    int64_t H = req > 0 ? req : (p->n >= (1ll << 19) ? 262144 : 0);
+    return std::max<int64_t>(0, std::min(H, live));
+}
+
+// BLOCK plan, after the descriptors: the degree-sorted colidx (P:295 (3)) with the hot encoding.
+void build_sorted_cols(agcn_plan_s* p, const int32_t* colidx, const agcn_opts_t& o, cudaStream_t s) {
+    p->scols = dalloc<int32_t>(p->nnz, s);
+    p->device_bytes += sizeof(int32_t) * (size_t)p->nnz;
+    p->n_hot = hot_rows_for(p, o.hot_rows);
+    Scratch tmp(s);
+    uint2* hot = nullptr;
+    if (p->n_hot > 0) {
+        const int64_t nw = (p->n_cols + 31) / 32;
+        hot = tmp.alloc<uint2>(nw);
+        int32_t* pre = tmp.alloc<int32_t>(nw + 1);
+        p->hot_cols = dalloc<int32_t>(p->n_hot, s);
+        p->device_bytes += sizeof(int32_t) * (size_t)p->n_hot;
+        AGCN_CUDA(cudaMemsetAsync(hot, 0, sizeof(uint2) * nw, s));
+        k_hot_bits<<<blocks_for(p->n_hot, 256), 256, 0, s>>>(p->perm, p->n, p->n_hot, hot);
+        post_launch();
+        k_popc_words<<<blocks_for(nw, 256), 256, 0, s>>>(hot, nw, pre);
+        post_launch();
+        exclusive_scan_i32(pre, pre, nw, s);
+        k_hot_list<<<blocks_for(nw, 256), 256, 0, s>>>(hot, pre, nw, p->hot_cols);
+        post_launch();
+    }
+    if (p->nnz == 0 || p->nblocks == 0) return;
+    const unsigned g = (unsigned)std::min<int64_t>(blocks_for(p->nblocks, kWarps), 148 * 8);
+    k_sorted_cols<<<g, kThreads, 0, s>>>(p->desc, p->nblocks, p->deg_bound, p->sorted_rowptr, p->row_src_off,
+                                         colidx + p->rp_base, p->n_cols, p->cmap, hot, p->scols);
+    post_launch();
 }
 
 // A second stream per device for plan work that can overlap the main sequence (validation).
@@ -814,7 +928,7 @@ bool build_block_plan_small(agcn_plan_s* p, const int32_t* rowptr, const int32_t
     p->nb_small = h.nb_small;
     p->nblocks = h.nb_small + h.ov_chunks;
     p->device_bytes = sizeof(int32_t) * (size_t)(3 * n + 1 + ovc_cap) + sizeof(int4) * (size_t)desc_cap;
-    set_spmm_cols(p, colidx, s);
+    build_sorted_cols(p, colidx, o, s);
     return true;
 }
 
@@ -897,7 +1011,7 @@ void build_block_plan(agcn_plan_s* p, const int32_t* rowptr, const int32_t* coli
     p->nblocks = blk + hf.ov_chunks;
     AGCN_CHECK(p->nblocks < (1ll << 31), AGCN_ERR_OVERFLOW, "too many descriptors");
 
-    // plan-owned arrays (colidx is borrowed: the SpMM reads it through row_src_off)
+    // plan-owned arrays (the sorted colidx copy follows the descriptors)
     p->perm = dalloc<int32_t>(n, s);
     p->sorted_rowptr = dalloc<int32_t>(n + 1, s);
     p->row_src_off = dalloc<int32_t>(n, s);
@@ -932,7 +1046,7 @@ void build_block_plan(agcn_plan_s* p, const int32_t* rowptr, const int32_t* coli
 
     // (3) "updating the row pointer array to reflect the new row order", O(n):
     // sorted degrees -> sorted_rowptr (scan) and row_src_off (where each sorted row starts in
-    // the caller's colidx / vals).  Column indices are not copied.
+    // the caller's colidx / vals); the sorted colidx is copied after the descriptors.
     if (n > 0) {
         k_sorted_rows<<<blocks_for(n, 256), 256, 0, s>>>(p->perm, rowptr, n, p->sorted_rowptr,
                                                           p->row_src_off);
@@ -964,7 +1078,7 @@ void build_block_plan(agcn_plan_s* p, const int32_t* rowptr, const int32_t* coli
         AGCN_CUDA(cudaMemsetAsync(p->ov_chunk_start, 0, sizeof(int32_t), s));
     }
 
-    set_spmm_cols(p, colidx, s);
+    build_sorted_cols(p, colidx, o, s);
 }
 
 // ---------------------------------------------------------------- warp-partition plan
@@ -992,7 +1106,7 @@ void build_warp_plan(agcn_plan_s* p, const int32_t* rowptr, const int32_t* colid
     p->rp_base = hf.rowptr_first;
     p->tasks = dalloc<int4>(ntasks, s);
     p->device_bytes = sizeof(int32_t) * (size_t)(n + 1) + sizeof(int4) * (size_t)ntasks;
-    set_spmm_cols(p, colidx, s);
+    copy_cols_original(p, colidx, s);
     if (n > 0) {
         k_emit_tasks<<<blocks_for(n, 256), 256, 0, s>>>(p->rowptr_copy, n, p->mwn, tstart, p->tasks);
         post_launch();
@@ -1003,28 +1117,26 @@ void build_warp_plan(agcn_plan_s* p, const int32_t* rowptr, const int32_t* colid
 
 void free_plan_arrays(agcn_plan_s* p) {
     void* ptrs[] = {p->perm,  p->sorted_rowptr, p->row_src_off, p->desc,       p->ov_chunk_start,
-                    p->tasks, p->rowptr_copy,   p->cols_copy,   p->ov_partial, p->ov_cnt};
+                    p->tasks, p->rowptr_copy,   p->cols_copy,   p->ov_partial, p->ov_cnt,
+                    p->scols, p->xhot, p->hot_cols};
     // Stream-ordered release on the plan's stream, after the last SpMM that used the plan on
     // another stream (p->last_use); no host synchronisation.
     if (p->last_use) cudaStreamWaitEvent(p->stream, p->last_use, 0);
     for (void* q : ptrs)
         if (q) cudaFreeAsync(q, p->stream);
-    free_col_sched(p->sched, p->stream);
     if (p->ready) cudaEventDestroy(p->ready);
     if (p->last_use) cudaEventDestroy(p->last_use);
 }
 
-// Degree-sorted colidx for introspection (parity tests), gathered on demand.
+// Degree-sorted colidx for introspection (parity tests): the plan's copy, hot encoding undone.
 void plan_copy_sorted_colidx(agcn_plan_s* p, int32_t* host_dst) {
     if (p->nnz == 0) return;
     cudaStream_t s = p->stream;
     Scratch tmp(s);
     int32_t* d = tmp.alloc<int32_t>(p->nnz);
-    if (p->n > 0 && p->sorted_rowptr) {
-        k_gather_sorted_cols<<<blocks_for(p->n, kWarps), kThreads, 0, s>>>(
-            p->n, p->sorted_rowptr, p->row_src_off, p->cols, d);
-        post_launch();
-    }
+    k_decode_hot<<<(unsigned)std::min<int64_t>(blocks_for(p->nnz, 256), 148 * 16), 256, 0, s>>>(
+        p->scols, p->nnz, p->hot_cols, d);
+    post_launch();
     AGCN_CUDA(cudaMemcpyAsync(host_dst, d, sizeof(int32_t) * p->nnz, cudaMemcpyDeviceToHost, s));
     AGCN_CUDA(cudaStreamSynchronize(s));
 }
@@ -1108,7 +1220,6 @@ agcn_plan_s* build_plan(const int32_t* rowptr, const int32_t* colidx, int64_t n,
         p->partition = o.partition;
         p->x_rows = o.col_nparts > 0 ? (int64_t)o.col_nparts * o.col_slot_rows : n_cols;
         p->stream = s;
-        p->colidx = colidx;
         if (o.partition == AGCN_PARTITION_BLOCK)
         {
             if (!build_block_plan_small(p, rowptr, colidx, o, s)) build_block_plan(p, rowptr, colidx, o, s);

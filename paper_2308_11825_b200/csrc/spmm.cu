@@ -9,8 +9,9 @@
 //    lanes with float4 loads (L*T float4 = the paper's round_dim, lanes past F truncated,
 //    P:493); a warp holds G = 32/L such "combined warps" (sub-warps), which split the
 //    descriptor's contiguous nonzeros evenly (per-sub-warp nnz differ by at most 4).
-//  * The descriptor's colidx (contiguous in degree-sorted order) and vals (one contiguous
-//    run per row, via row_src_off) are staged in shared memory once per descriptor.
+//  * The descriptor's colidx (the plan's degree-sorted copy: contiguous from loc) and vals
+//    (one contiguous run per row of the caller's array, via row_src_off) are staged in shared
+//    memory once per descriptor.  Hot columns (-1 - slot) read the plan's compact hot rows.
 //  * Three-level accumulation made deterministic: (1) registers, (2) the
 //    partial rows of sub-warps that share a row are merged in fixed sub-warp order through
 //    shared memory (replaces atomicAdd_block), (3) rows with degree > deg_bound are split
@@ -29,10 +30,6 @@ namespace {
 constexpr int kWarpsPerCta = 8;
 constexpr double kL2KeepBytes = 128.0 * 1024 * 1024;  // X up to ~L2 size gets evict_last hints
 
-int env_int(const char* name, int dflt) {  // experiment switches
-    const char* v = getenv(name);
-    return v ? atoi(v) : dflt;
-}
 constexpr int kCtaThreads = kWarpsPerCta * 32;
 
 template <bool V4>
@@ -102,12 +99,13 @@ struct BlockArgs {
     int32_t db;             // deg_bound
     int32_t stage;          // shared-memory entries per warp (>= db + 8, multiple of 4)
     int32_t rso_stage;      // shared-memory row offsets per warp (>= max_block_warps)
-    const int32_t* cols;    // column indices, indexed like vals (rowptr-relative)
+    const int32_t* scols;   // the plan's degree-sorted colidx (hot columns -1 - slot)
     const int32_t* srp;     // sorted rowptr
     const int32_t* rso;     // row_src_off
     const int32_t* perm;    // sorted -> original row
     const float* vals;      // caller vals, already offset by rowptr[0]
     const float* X;
+    const float* Xh;        // hot rows [n_hot][FV] (plans with hot rows)
     float* Y;
     float* ovp;             // oversized partials [ov_chunks][FV]
     int64_t n_zero;         // sorted rows [0, n_zero) have degree 0
@@ -129,6 +127,7 @@ __global__ void __launch_bounds__(kCtaThreads, 4) k_spmm_block(const __grid_cons
     VT* s_part = reinterpret_cast<VT*>(smem + (size_t)kWarpsPerCta * (2 * a.stage + a.rso_stage) * 4) +
                  warp * (G * 2 * T * L);
     const VT* __restrict__ X = reinterpret_cast<const VT*>(a.X);
+    const VT* __restrict__ XH = reinterpret_cast<const VT*>(a.Xh);
     VT* __restrict__ Y = reinterpret_cast<VT*>(a.Y);
     VT* __restrict__ OVP = reinterpret_cast<VT*>(a.ovp);
     const int32_t FV = a.FV;
@@ -174,7 +173,7 @@ __global__ void __launch_bounds__(kCtaThreads, 4) k_spmm_block(const __grid_cons
                 const int32_t r = e / d;
                 off = s_rso[r] + (e - r * d);
             }
-            s_col[e] = ldcs_i(a.cols + off);
+            s_col[e] = ldcs_i(a.scols + (int64_t)loc + e);
             s_val[e] = ldcs_f(a.vals + off);
         }
         __syncwarp();
@@ -219,11 +218,12 @@ __global__ void __launch_bounds__(kCtaThreads, 4) k_spmm_block(const __grid_cons
 #pragma unroll
                 for (int u = 0; u < U; ++u) {
                     const bool ok = q + u < q1;
+                    const VT* xr = col[u] >= 0 ? X + (int64_t)col[u] * FV : XH + (int64_t)(-1 - col[u]) * FV;
 #pragma unroll
                     for (int t = 0; t < T; ++t) {
                         const int32_t c = cc + li + t * L;
                         if (ok && c < FV)
-                            xv[u][t] = ldx(X + (int64_t)col[u] * FV + c, keep, pol);
+                            xv[u][t] = ldx(xr + c, keep, pol);
                         else
                             vzero(xv[u][t]);
                     }
@@ -309,55 +309,7 @@ __global__ void k_epilogue(float* __restrict__ Y, int64_t k0, int64_t k1, int32_
     }
 }
 
-// Level-3 merge: oversized row k gets the sum of its chunk partials.  One CTA per row:
-// thread (g, c) sums chunks c0+g, c0+g+NG, ... of vector column c in order, then thread
-// (0, c) adds the NG group sums in group order -> fixed summation order (deterministic).
-constexpr int kReduceThreads = 128;
-template <bool V4>
-__global__ void __launch_bounds__(kReduceThreads) k_ov_reduce(
-    const float* __restrict__ ovp_f, const int32_t* __restrict__ chunk_start,
-    const int32_t* __restrict__ perm, int64_t ov_start, float* __restrict__ Y_f, int32_t FV,
-    const int32_t* __restrict__ srp, const Epi epi) {
-    using VT = typename VecT<V4>::T;
-    __shared__ VT part[kReduceThreads];
-    const VT* ovp = reinterpret_cast<const VT*>(ovp_f);
-    VT* Y = reinterpret_cast<VT*>(Y_f);
-    const int64_t k = blockIdx.x;
-    const int32_t c0 = chunk_start[k], c1 = chunk_start[k + 1];
-    const int64_t orow = perm[ov_start + k];
-    const int FVc = FV < kReduceThreads ? FV : kReduceThreads;   // columns per pass
-    const int NG = kReduceThreads / FVc;                         // chunk groups
-    const int g = threadIdx.x / FVc, cl = threadIdx.x % FVc;
-    for (int32_t cb = 0; cb < FV; cb += FVc) {
-        const int32_t c = cb + cl;
-        VT acc;
-        vzero(acc);
-        if (g < NG && c < FV) {
-            int32_t j = c0 + g;
-            for (; j + 3 * NG < c1; j += 4 * NG) {
-                VT x0 = ovp[(int64_t)j * FV + c], x1 = ovp[(int64_t)(j + NG) * FV + c];
-                VT x2 = ovp[(int64_t)(j + 2 * NG) * FV + c], x3 = ovp[(int64_t)(j + 3 * NG) * FV + c];
-                vadd(acc, x0);
-                vadd(acc, x1);
-                vadd(acc, x2);
-                vadd(acc, x3);
-            }
-            for (; j < c1; j += NG) vadd(acc, ovp[(int64_t)j * FV + c]);
-        }
-        part[threadIdx.x] = acc;
-        __syncthreads();
-        if (g == 0 && c < FV) {
-            VT sum = part[cl];
-            for (int gg = 1; gg < NG; ++gg) vadd(sum, part[gg * FVc + cl]);
-            if (epi.active()) sum = epi_v(sum, srp[ov_start + k + 1] - srp[ov_start + k], orow, c, epi);
-            sty(Y + orow * FV + c, sum);
-            if (epi.npeer) fanout_v(epi, orow * FV + c, sum);
-        }
-        __syncthreads();
-    }
-}
-
-// Same level-3 merge, sized to the chunk counts (C5: median 3 chunks per oversized row, the
+// Level-3 merge (deterministic), sized to the chunk counts (C5: median 3 chunks per oversized row, the
 // heaviest 633).  Oversized rows sit in ascending degree order, so the n_heavy rows with more
 // than kHeavyChunks chunks are the suffix: CTAs [0, n_heavy) take one of them each, heaviest
 // first, with all 256 threads; the other CTAs take 8 rows each, one warp per row.  Lane or
@@ -532,20 +484,43 @@ void launch_epilogue(float* Y, int64_t k0, int64_t k1, int32_t F, const int32_t*
     post_launch();
 }
 
-int g_num_sms = 0;
-std::once_flag g_sms_once;
+// After an SpMM that read the hot buffer under a persisting window: drop its lines from L2
+// (discard.global.L2: invalidate without write-back -- the buffer is re-gathered by every call),
+// so they do not keep occupying the persisting set-aside for whatever runs next.
+__global__ void k_l2_discard(const float* __restrict__ p, int64_t lines) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < lines; i += (int64_t)gridDim.x * blockDim.x)
+        asm volatile("discard.global.L2 [%0], 128;" ::"l"(p + i * 32) : "memory");
+}
+
+// Per-device launch facts (a process may drive several devices): SM count and, per kernel
+// instantiation and shared-memory size, the occupancy after the shared-memory opt-in.
+constexpr int kMaxDev = 64;
+int cur_device() {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    return dev >= 0 && dev < kMaxDev ? dev : 0;
+}
+
+template <class K>
+int occupancy(K kern, int threads, size_t smem, size_t optin) {
+    static std::mutex mu;
+    static int occ[kMaxDev] = {};
+    static size_t occ_smem[kMaxDev] = {};
+    const int dev = cur_device();
+    std::lock_guard<std::mutex> lock(mu);
+    if (occ[dev] <= 0 || occ_smem[dev] != smem) {
+        if (optin) AGCN_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)optin));
+        AGCN_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[dev], kern, threads, smem));
+        if (occ[dev] < 1) occ[dev] = 1;
+        occ_smem[dev] = smem;
+    }
+    return occ[dev];
+}
 
 template <int L, int T, bool V4, int U>
 void launch_block_u(const BlockArgs& a, cudaStream_t s, size_t smem) {
     auto kern = k_spmm_block<L, T, V4, U>;
-    static int occ = -1;        // per instantiation, for the last shared-memory size
-    static size_t occ_smem = 0;
-    if (occ < 0 || occ_smem != smem) {
-        AGCN_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-        AGCN_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kCtaThreads, smem));
-        if (occ < 1) occ = 1;
-        occ_smem = smem;
-    }
+    const int occ = occupancy(kern, kCtaThreads, smem, 200 * 1024);
     const int64_t work = std::max<int64_t>(a.nblocks, (a.n_zero + 31) / 32);
     const int64_t want = (work + kWarpsPerCta - 1) / kWarpsPerCta;
     const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)num_sms() * occ));
@@ -553,29 +528,41 @@ void launch_block_u(const BlockArgs& a, cudaStream_t s, size_t smem) {
     post_launch();
 }
 
-// X-row loads in flight per lane: 8 for one vector per lane (T == 1), else 4 (register budget).
+// X-row loads in flight per lane: 4 (register budget; U 8 at one vector per lane measured no
+// better, r01).
 template <int L, int T, bool V4>
 void launch_block(const BlockArgs& a, cudaStream_t s, size_t smem) {
-    static const int u_env = env_int("AGCN_SPMM_U", 4);
-    if (T == 1 && u_env == 8)
-        launch_block_u<L, T, V4, 8>(a, s, smem);
-    else
-        launch_block_u<L, T, V4, 4>(a, s, smem);
+    launch_block_u<L, T, V4, 4>(a, s, smem);
 }
 
 template <int L, int T, bool V4>
 void launch_warp(const WarpArgs& a, cudaStream_t s) {
     auto kern = k_spmm_warp<L, T, V4, 4>;
-    static int occ = -1;
-    if (occ < 0) {
-        AGCN_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kCtaThreads, 0));
-        if (occ < 1) occ = 1;
-    }
+    const int occ = occupancy(kern, kCtaThreads, 0, 0);
     constexpr int G = 32 / L;
     const int64_t want = (a.ntasks + kWarpsPerCta * G - 1) / (kWarpsPerCta * G);
     const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)num_sms() * occ));
     kern<<<(unsigned)grid, kCtaThreads, 0, s>>>(a);
     post_launch();
+}
+
+// Xh[k] = X[hot_cols[k]] for k < H: the hot rows (the H highest-degree vertices) in a compact
+// buffer, one warp per row (16-byte vectors when F % 4 == 0 and X is aligned)
+template <bool V4>
+__global__ void k_gather_hot(const float* __restrict__ X, const int32_t* __restrict__ hot_cols,
+                             int64_t H, int32_t F, float* __restrict__ Xh) {
+    const int lane = threadIdx.x & 31;
+    const int64_t W = (int64_t)gridDim.x * (blockDim.x / 32);
+    for (int64_t k = (int64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5); k < H; k += W) {
+        const int64_t r = __ldg(hot_cols + k);
+        if (V4) {
+            const float4* src = reinterpret_cast<const float4*>(X + r * F);
+            float4* dst = reinterpret_cast<float4*>(Xh + k * F);
+            for (int32_t c = lane; c < F / 4; c += 32) dst[c] = __ldg(src + c);
+        } else {
+            for (int32_t c = lane; c < F; c += 32) Xh[k * F + c] = __ldg(X + r * F + c);
+        }
+    }
 }
 
 #define AGCN_DISPATCH_LT(SHAPE, FN, ...)                                             \
@@ -623,13 +610,47 @@ inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 
 }  // namespace
 
 int num_sms() {
-    std::call_once(g_sms_once, [] {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
-        if (g_num_sms <= 0) g_num_sms = 148;
-    });
-    return g_num_sms;
+    static std::atomic<int> sms[kMaxDev] = {};
+    const int dev = cur_device();
+    int v = sms[dev].load(std::memory_order_relaxed);
+    if (v <= 0) {
+        if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0) v = 148;
+        sms[dev].store(v, std::memory_order_relaxed);
+    }
+    return v;
+}
+
+size_t ensure_persisting_l2(size_t bytes) {
+    static std::mutex mu;
+    static size_t set[kMaxDev] = {};
+    static int maxp[kMaxDev] = {}, maxw[kMaxDev] = {};
+    const int dev = cur_device();
+    std::lock_guard<std::mutex> lock(mu);
+    if (maxp[dev] == 0) {
+        if (cudaDeviceGetAttribute(&maxp[dev], cudaDevAttrMaxPersistingL2CacheSize, dev) != cudaSuccess) maxp[dev] = -1;
+        if (cudaDeviceGetAttribute(&maxw[dev], cudaDevAttrMaxAccessPolicyWindowSize, dev) != cudaSuccess) maxw[dev] = 0;
+        cudaGetLastError();
+    }
+    if (maxp[dev] <= 0 || maxw[dev] <= 0) return 0;
+    bytes = std::min<size_t>(bytes, std::min<size_t>((size_t)maxp[dev], (size_t)maxw[dev]));
+    if (set[dev] < bytes) {
+        if (cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, bytes) != cudaSuccess) {
+            cudaGetLastError();
+            return 0;
+        }
+        set[dev] = bytes;
+    }
+    return bytes;
+}
+
+// default hot budget: the device's maximum persisting-L2 size
+static size_t max_persisting_l2() {
+    int v = 0;
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMaxPersistingL2CacheSize, cur_device()) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return v > 0 ? (size_t)v : 0;
 }
 
 void spmm_launch(agcn_plan_s* p, const float* vals, const float* X, int32_t F, float* Y,
@@ -656,7 +677,7 @@ void spmm_launch(agcn_plan_s* p, const float* vals, const float* X, int32_t F, f
     if (p->partition == AGCN_PARTITION_WARP) {
         AGCN_CUDA(cudaMemsetAsync(Y, 0, sizeof(float) * (size_t)p->n * F, s));
         if (p->ntasks > 0) {
-            WarpArgs a{p->tasks, p->ntasks, p->rowptr_copy, p->cols, vals + p->rp_base, X, Y, FV};
+            WarpArgs a{p->tasks, p->ntasks, p->rowptr_copy, p->cols_copy, vals + p->rp_base, X, Y, FV};
             if (v4)
                 AGCN_DISPATCH_LT(sh, warp_v4, a, s);
             else
@@ -670,28 +691,52 @@ void spmm_launch(agcn_plan_s* p, const float* vals, const float* X, int32_t F, f
     int kernel = o.kernel;
     if (kernel == AGCN_KERNEL_AUTO) kernel = wide_ok ? AGCN_KERNEL_WIDE : AGCN_KERNEL_GENERAL;
     if (kernel == AGCN_KERNEL_LOOPED) kernel = AGCN_KERNEL_GENERAL;  // with the {32 lanes, scalar} shape
+    AGCN_CHECK(kernel == AGCN_KERNEL_WIDE || kernel == AGCN_KERNEL_GENERAL, AGCN_ERR_INVALID_ARG,
+               "unknown kernel");
     AGCN_CHECK(kernel != AGCN_KERNEL_WIDE || wide_ok, AGCN_ERR_UNSUPPORTED,
                "WIDE kernel needs F = 8 L <= 256, 32-byte aligned X/Y, max_block_warps <= 32");
-    AGCN_CHECK(kernel != AGCN_KERNEL_PIPE || pipe_supported(p, X, Y, F), AGCN_ERR_UNSUPPORTED,
-               "PIPE kernel needs F in {32,64,128,256}, 32-byte aligned X/Y, max_block_warps <= 32");
-    // column-blocked oversized rows (WIDE kernel, sched.cu): X slice per block ~ col_block_mb
-    bool blocked = false;
-    if (kernel == AGCN_KERNEL_WIDE && o.col_block_mb > 0) {
-        const double target = o.col_block_mb * 1048576.0;
-        const int shift = col_sched_shift(p, F, target);
-        if (shift >= 0) {
-            if (p->sched.shift != shift || p->sched.F < F || !p->sched.seg) build_col_sched(p, shift, F, s);
-            blocked = true;
-        }
-    }
     // oversized-row partial buffer of the paper's chunks (grows, stream-ordered)
-    const size_t need = blocked ? 0 : (size_t)p->ov_chunks * (size_t)F;
+    const size_t need = (size_t)p->ov_chunks * (size_t)F;
     if (need > p->ov_partial_floats) {
         if (p->ov_partial) AGCN_CUDA(cudaFreeAsync(p->ov_partial, s));
         p->ov_partial = nullptr;
         p->ov_partial_floats = 0;
         AGCN_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p->ov_partial), need * sizeof(float), s));
         p->ov_partial_floats = need;
+    }
+    // hot X rows (agcn_opts_t.hot_rows): gathered into the plan's compact buffer every call
+    // (X changes between calls), read by the kernels for columns encoded -1 - slot
+    if (p->n_hot > 0) {
+        const size_t hneed = (size_t)p->n_hot * (size_t)F;
+        if (hneed > p->xhot_floats) {
+            if (p->xhot) AGCN_CUDA(cudaFreeAsync(p->xhot, s));
+            p->xhot = nullptr;
+            p->xhot_floats = 0;
+            AGCN_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p->xhot), hneed * sizeof(float), s));
+            p->xhot_floats = hneed;
+        }
+        const unsigned g = (unsigned)std::min<int64_t>((p->n_hot + 7) / 8, (int64_t)num_sms() * 16);
+        if (v4)
+            k_gather_hot<true><<<g, 256, 0, s>>>(X, p->hot_cols, p->n_hot, F, p->xhot);
+        else
+            k_gather_hot<false><<<g, 256, 0, s>>>(X, p->hot_cols, p->n_hot, F, p->xhot);
+        post_launch();
+    }
+    // L2 residency of X (agcn_l2_hint_t)
+    const double x_bytes = 4.0 * (double)p->x_rows * F;
+    int l2 = o.l2_hint;
+    // auto: evict_last on all of X when it fits in L2; otherwise plain loads (the hot rows, if
+    // the plan has them, still come from the compact buffer).  The persisting window and the
+    // hot/cold hints measured no faster than the compact buffer alone on C5 (r02k), and the
+    // window changes a device-wide limit that slowed the next kernels by 10-15 % -- opt-in only.
+    if (l2 == AGCN_L2_AUTO) l2 = x_bytes <= kL2KeepBytes && p->n_hot == 0 ? AGCN_L2_KEEP_ALL : AGCN_L2_NONE;
+    AGCN_CHECK(l2 >= AGCN_L2_NONE && l2 <= AGCN_L2_HOT_HINTS, AGCN_ERR_INVALID_ARG, "unknown l2_hint");
+    if ((l2 == AGCN_L2_HOT_WINDOW || l2 == AGCN_L2_HOT_HINTS) && p->n_hot == 0) l2 = AGCN_L2_NONE;
+    size_t win = 0;
+    if (l2 == AGCN_L2_HOT_WINDOW) {
+        const size_t budget = o.hot_mb > 0 ? (size_t)o.hot_mb << 20 : max_persisting_l2();
+        win = ensure_persisting_l2(std::min(budget, sizeof(float) * p->xhot_floats));
+        if (win == 0) l2 = AGCN_L2_NONE;
     }
     BlockArgs a;
     a.desc = p->desc;
@@ -700,37 +745,39 @@ void spmm_launch(agcn_plan_s* p, const float* vals, const float* X, int32_t F, f
     a.db = p->deg_bound;
     a.stage = ((p->deg_bound + 3) & ~3) + 8;
     a.rso_stage = (p->mbw + 3) & ~3;
-    a.cols = p->cols;
+    a.scols = p->scols;
     a.srp = p->sorted_rowptr;
     a.rso = p->row_src_off;
     a.perm = p->perm;
     a.vals = vals + p->rp_base;
     a.X = X;
+    a.Xh = p->xhot;
     a.Y = Y;
     a.ovp = p->ov_partial;
     a.n_zero = p->n_zero;
     a.FV = FV;
     const size_t elt = v4 ? sizeof(float4) : sizeof(float);
     const size_t smem = (size_t)kWarpsPerCta * ((2 * a.stage + a.rso_stage) * 4 + 64 * sh.T * elt);
-    // L2 residency of X: evict_last hints when X fits in L2 (auto), or as requested
-    const double x_bytes = 4.0 * (double)p->x_rows * F;
-    const bool keep = o.l2_hint < 0 ? x_bytes <= kL2KeepBytes : o.l2_hint > 0;
-    a.keep = keep;
+    a.keep = l2 == AGCN_L2_KEEP_ALL;
     // level 3 of the oversized rows of <= kHeavyChunks chunks fused into the WIDE kernel when
     // there are few chunks (saves the reduction launch on small graphs: C2 -4..7 %, C3 -7 %;
     // with C5's 201K chunks the per-chunk fence + counter costs more than the launch: +3 %;
-    // profiles/r01bk_fused_level3.md).  AGCN_FUSE_OV: -1 auto (default), 0 never, 1 always.
-    static const int fuse_env = [] { const char* e = getenv("AGCN_FUSE_OV"); return e ? atoi(e) : -1; }();
-    const bool fuse = kernel == AGCN_KERNEL_WIDE && !blocked && p->n_ov > 0 && fuse_env != 0 &&
-                      (fuse_env > 0 || p->ov_chunks <= kFuseOvMaxChunks) && env_int("AGCN_OV_REDUCE", 1) != 0;
+    // profiles/r01bk_fused_level3.md)
+    const bool fuse = kernel == AGCN_KERNEL_WIDE && p->n_ov > 0 && p->ov_chunks <= kFuseOvMaxChunks;
     if (fuse && !p->ov_cnt) {
         p->ov_cnt = dalloc<int32_t>(p->n_ov, s);
         AGCN_CUDA(cudaMemsetAsync(p->ov_cnt, 0, sizeof(int32_t) * p->n_ov, s));
     }
-    if (kernel == AGCN_KERNEL_PIPE)
-        launch_pipe(p, vals, X, F, Y, s);
-    else if (kernel == AGCN_KERNEL_WIDE)
-        launch_wide(p, vals, X, F, Y, keep, blocked, fuse, epi, s);  // epilogue fused
+    if (kernel == AGCN_KERNEL_WIDE)
+    {
+        launch_wide(p, vals, X, p->xhot, F, Y, l2, win, fuse, o.chunk_shape, epi, s);  // epilogue fused
+        if (win > 0) {
+            const int64_t lines = (int64_t)((win + 127) / 128);
+            k_l2_discard<<<(unsigned)std::min<int64_t>((lines + 255) / 256, (int64_t)num_sms() * 8), 256, 0, s>>>(
+                p->xhot, lines);
+            post_launch();
+        }
+    }
     else if (v4)
         AGCN_DISPATCH_LT(sh, block_v4, a, s, smem);
     else
@@ -738,26 +785,18 @@ void spmm_launch(agcn_plan_s* p, const float* vals, const float* X, int32_t F, f
     if (kernel != AGCN_KERNEL_WIDE && epi.active())  // rows of degree <= deg_bound
         launch_epilogue(Y, 0, p->ov_start, F, p->perm, p->sorted_rowptr, epi, s);
     if (p->n_ov > 0 && !(fuse && p->n_ov_heavy == 0)) {  // level 3: fixed-order sums of partial rows
-        const unsigned grid = (unsigned)p->n_ov;
-        const float* part = blocked ? p->sched.partial : p->ov_partial;
-        const int32_t* slots = blocked ? p->sched.slot_base : p->ov_chunk_start;
-        static const int red = env_int("AGCN_OV_REDUCE", 1);  // 1: sized (default), 0: CTA per row
+        const float* part = p->ov_partial;
+        const int32_t* slots = p->ov_chunk_start;
         const int64_t nh = p->n_ov_heavy;
         // fused: only the heavy rows (CTAs [0, nh) of the kernel) are left
         const unsigned hgrid = fuse ? (unsigned)nh
                                     : (unsigned)(nh + (p->n_ov - nh + kReduceWarps - 1) / kReduceWarps);
-        if (red && v4)
+        if (v4)
             k_ov_reduce_h<true><<<hgrid, kReduceWarps * 32, 0, s>>>(part, slots, p->perm, p->ov_start, p->n_ov,
                                                                    nh, Y, FV, p->sorted_rowptr, epi);
-        else if (red)
+        else
             k_ov_reduce_h<false><<<hgrid, kReduceWarps * 32, 0, s>>>(part, slots, p->perm, p->ov_start,
                                                                     p->n_ov, nh, Y, FV, p->sorted_rowptr, epi);
-        else if (v4)
-            k_ov_reduce<true><<<grid, kReduceThreads, 0, s>>>(part, slots, p->perm, p->ov_start, Y, FV,
-                                                              p->sorted_rowptr, epi);
-        else
-            k_ov_reduce<false><<<grid, kReduceThreads, 0, s>>>(part, slots, p->perm, p->ov_start, Y, FV,
-                                                               p->sorted_rowptr, epi);
         post_launch();
     }
 }

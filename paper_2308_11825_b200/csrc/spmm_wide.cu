@@ -17,12 +17,17 @@
 //    (rows with degree > deg_bound) writes per-chunk partial rows summed by k_ov_reduce.
 //  * the row offsets / output rows of the descriptor (<= 32 rows) are fetched once per
 //    descriptor, one per lane, and shuffled to the combined warps.
-//  * colidx / vals are read straight from the caller's CSR through row_src_off (the plan
-//    never copies them), one batch of pairs ahead (prefetch); both are evict-first streams
-//    (ld.global.cs).  When X fits in L2 its rows are loaded with an evict_last hint.
+//  * column indices come from the plan's degree-sorted copy (a descriptor's entries are the
+//    contiguous run from loc), vals from the caller's array through row_src_off, one batch of
+//    pairs ahead (prefetch), both through the read-only path (ld.global.nc).
+//  * X residency in L2 (agcn_l2_hint_t, template XM): 0 plain loads; 1 evict_last on every X
+//    row (X fits in L2); 2 the plan's hot columns (-1 - slot) read the compact hot buffer Xh --
+//    under the launch's persisting access-policy window in HOT_WINDOW mode; 3 as 2 with hot
+//    loads evict_last and cold loads evict_first.
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 
 #include "internal.h"
 
@@ -55,15 +60,23 @@ __device__ __forceinline__ void ld8(f8& r, const float* p, int hint) {
                      : "l"(p));
 }
 
+// acc += v * x over 8 floats as four packed fp32x2 FMAs (FFMA2, sm_100): per element the same
+// fma.rn as a scalar FFMA (bitwise identical results), half the FMA instructions
 __device__ __forceinline__ void fma8(f8& acc, float v, const f8& x) {
-    acc.a.x = fmaf(v, x.a.x, acc.a.x);
-    acc.a.y = fmaf(v, x.a.y, acc.a.y);
-    acc.a.z = fmaf(v, x.a.z, acc.a.z);
-    acc.a.w = fmaf(v, x.a.w, acc.a.w);
-    acc.b.x = fmaf(v, x.b.x, acc.b.x);
-    acc.b.y = fmaf(v, x.b.y, acc.b.y);
-    acc.b.z = fmaf(v, x.b.z, acc.b.z);
-    acc.b.w = fmaf(v, x.b.w, acc.b.w);
+    asm("{\n\t.reg .b64 vv, a0, a1, a2, a3, x0, x1, x2, x3;\n\t"
+        "mov.b64 vv, {%8, %8};\n\t"
+        "mov.b64 a0, {%0, %1};\n\tmov.b64 a1, {%2, %3};\n\t"
+        "mov.b64 a2, {%4, %5};\n\tmov.b64 a3, {%6, %7};\n\t"
+        "mov.b64 x0, {%9, %10};\n\tmov.b64 x1, {%11, %12};\n\t"
+        "mov.b64 x2, {%13, %14};\n\tmov.b64 x3, {%15, %16};\n\t"
+        "fma.rn.f32x2 a0, vv, x0, a0;\n\tfma.rn.f32x2 a1, vv, x1, a1;\n\t"
+        "fma.rn.f32x2 a2, vv, x2, a2;\n\tfma.rn.f32x2 a3, vv, x3, a3;\n\t"
+        "mov.b64 {%0, %1}, a0;\n\tmov.b64 {%2, %3}, a1;\n\t"
+        "mov.b64 {%4, %5}, a2;\n\tmov.b64 {%6, %7}, a3;\n\t}"
+        : "+f"(acc.a.x), "+f"(acc.a.y), "+f"(acc.a.z), "+f"(acc.a.w), "+f"(acc.b.x), "+f"(acc.b.y),
+          "+f"(acc.b.z), "+f"(acc.b.w)
+        : "f"(v), "f"(x.a.x), "f"(x.a.y), "f"(x.a.z), "f"(x.a.w), "f"(x.b.x), "f"(x.b.y), "f"(x.b.z),
+          "f"(x.b.w));
 }
 
 __device__ __forceinline__ void st8(float* p, const f8& v) {
@@ -80,28 +93,35 @@ struct WideArgs {
     int64_t n_desc;       // descriptors executed from desc (nblocks, or nb_small with pieces)
     int64_t first_ov;     // descriptor index of the first oversized chunk
     int64_t n_zero;       // sorted rows [0, n_zero) have degree 0
-    const int32_t* cols;  // column indices, indexed like vals (rowptr-relative)
+    const int32_t* scols; // the plan's degree-sorted colidx (hot columns -1 - slot)
     const int32_t* srp;   // sorted rowptr
     const int32_t* rso;   // row_src_off
     const int32_t* perm;  // sorted -> original row
     const float* vals;    // caller vals, offset by rowptr[0]
     const float* X;
+    const float* Xh;      // hot rows [n_hot][F] (XM >= 2)
     float* Y;
     float* ovp;           // oversized partial rows [ov_chunks][F]
     int32_t db;           // deg_bound
-    const int4* pieces;   // column-blocked pieces of the oversized rows (sched.cu), or NULL
-    const int32_t* n_pieces;  // device: number of pieces
-    float* piece_partial; // [pieces][F] partial rows (slot-indexed)
-    int64_t piece_cap;    // upper bound of the piece count (grid sizing)
     Epi epi;              // output epilogue (EPI)
     int32_t L;            // lanes per X row (F / 8); used when the kernel's LT is 0
-    int32_t zero_last;    // write the degree-0 rows after the descriptors (A/B: AGCN_ZERO_LAST)
     int32_t fuse_ov;      // level 3 of rows of <= kHeavyChunks chunks done by the last warp
     const int32_t* ov_cs; // [n_ov + 1] first chunk of oversized row k
     int32_t* ov_cnt;      // [n_ov] chunks of row k finished (zero between launches)
     int64_t ov_start;     // sorted position of the first oversized row
-    int32_t lean;         // auto shape choice: U 2 at 4 CTAs/SM (see launch<L>)
 };
+
+// one X-row slice of 8 floats for column code c (XM: see the file comment)
+template <int XM>
+__device__ __forceinline__ void ldx8(f8& r, const WideArgs& a, int32_t c, int32_t F, int li) {
+    // (XM 0 / 1 keep the c < 0 test although it is never true there: the same code shape as the
+    // hot modes, which ptxas allocates without spills at 80 registers)
+    if (c < 0) {
+        ld8(r, a.Xh + ((int64_t)(-1 - c) * F + li * 8), XM == 3 ? 1 : 0);
+    } else {
+        ld8(r, a.X + ((int64_t)c * F + li * 8), XM == 1 ? 1 : (XM == 3 ? 2 : 0));
+    }
+}
 
 
 // a finished output row slice of 8 floats at column c of original row orow (degree deg)
@@ -154,9 +174,9 @@ __device__ __noinline__ void ov_finish(const WideArgs& a, int32_t row, int32_t d
 }
 
 // L lanes per X row (F = 8 L), U X rows in flight per lane, MINB resident CTAs per SM
-// (register budget), KEEP: X-row loads carry an L2 evict_last hint.
+// (register budget), XM: X residency mode (file comment).
 // LT = 0: L is a runtime value (a.L), for the F = 8 L with L not a power of two.
-template <int LT, int U, int MINB, bool KEEP, bool PIECES, bool EPI>
+template <int LT, int U, int MINB, int XM, bool EPI>
 __global__ void __launch_bounds__(kThreads, MINB) k_spmm_wide(const __grid_constant__ WideArgs a) {
     const int L = LT ? LT : a.L;
     const int G = 32 / L;                     // combined warps per warp; lanes >= G L idle
@@ -170,9 +190,9 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_wide(const __grid_const
     const int32_t gw = blockIdx.x * kWarps + (threadIdx.x >> 5);
     const int32_t W = gridDim.x * kWarps;
 
-    // degree-0 rows: Y row = 0 (reading Q16); 32 rows per warp step, one perm load per lane.
-    // Before the descriptors, or after them (a.zero_last: the stores then fill the tail left by
-    // the last, longest descriptors instead of preceding the gathers)
+    // degree-0 rows: Y row = 0 (reading Q16); 32 rows per warp step, one perm load per lane,
+    // after the descriptors (the stores fill the tail left by the last, longest descriptors;
+    // C5 -1 %, profiles/r01bj_zero_rows_last.md)
     auto zero_rows = [&]() {
         f8 z;
         z.a = z.b = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -185,32 +205,23 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_wide(const __grid_const
             }
         }
     };
-    if (!a.zero_last) zero_rows();
 
-    // execution list: the plan's descriptors [0, n_desc), then (when the column-blocked
-    // schedule replaces the oversized chunks) its pieces, block-major
     const int32_t n_desc = (int32_t)a.n_desc;
-    const int32_t n_exec = n_desc + (PIECES ? __ldg(a.n_pieces) : 0);
-    for (int32_t b = gw; b < n_exec; b += W) {
-        const bool piece = PIECES && b >= n_desc;
-        const int4 m = piece ? __ldg(a.pieces + (b - n_desc)) : __ldg(a.desc + b);
-        const bool ov = piece || m.x > a.db;
+    for (int32_t b = gw; b < n_desc; b += W) {
+        const int4 m = __ldg(a.desc + b);
+        const bool ov = m.x > a.db;
         const int32_t R = ov ? 1 : (m.w & 0xffff);      // rows of the descriptor (<= 32)
-        const int32_t d = ov ? m.w : m.x;               // nonzeros per row (chunk / piece size if ov)
-        const int32_t slot = PIECES ? -1 - m.x : 0;     // a piece's partial row
-        // per-row data, one row per lane: where the row's entries start in the caller's
-        // colidx / vals (P:295 step (3) row-pointer update), and its output row
+        const int32_t d = ov ? m.w : m.x;               // nonzeros per row (chunk size if ov)
+        const int32_t cd = m.y;                         // the descriptor's column indices: scols[cd ..]
+        // per-row data, one row per lane: where the row's entries start in the caller's vals
+        // (P:295 step (3) row-pointer update), and its output row
         int32_t rso_l = 0, dst_l = 0;
         if (lane < R) {
-            if (piece) {
-                rso_l = m.y;
-            } else {
-                rso_l = __ldg(a.rso + m.z + lane);
-                if (ov)
-                    rso_l += m.y - __ldg(a.srp + m.z);  // chunk offset inside the row
-                else
-                    dst_l = __ldg(a.perm + m.z + lane);
-            }
+            rso_l = __ldg(a.rso + m.z + lane);
+            if (ov)
+                rso_l += m.y - __ldg(a.srp + m.z);  // chunk offset inside the row
+            else
+                dst_l = __ldg(a.perm + m.z + lane);
         }
         int K = 1;                                       // combined warps per row
         while (2 * K * R <= G) K *= 2;
@@ -225,13 +236,18 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_wide(const __grid_const
             const int32_t Ts = act && s < R ? ((R - s + G - 1) / G) * d : 0;
             int32_t c, cn;
             float v, vn;
+            // t / d through a float reciprocal: exact here ((t + 0.5) / d is >= 0.5 / d away from an
+            // integer and t < 2^15, so the rounding error of the product, < (t + 0.5) / d * 2^-22,
+            // cannot cross it)
+            const float rd = __frcp_rn((float)d);
             auto pair = [&](int32_t t, int32_t& cc, float& vv) {  // entry t of this sub-warp
-                const int32_t ri = t / d;
-                const int32_t e = __shfl_sync(0xffffffffu, rso_l, min(s + ri * G, 31)) + (t - ri * d);
+                const int32_t ri = __float2int_rz(__fmul_rn((float)t + 0.5f, rd));
+                const int32_t j = t - ri * d, r = s + ri * G;     // row r of the descriptor
+                const int32_t e = __shfl_sync(0xffffffffu, rso_l, min(r, 31)) + j;
                 cc = 0;
                 vv = 0.f;
                 if (t < Ts) {
-                    cc = __ldg(a.cols + e);
+                    cc = __ldg(a.scols + (uint32_t)(cd + r * d + j));
                     vv = __ldg(a.vals + e);
                 }
             };
@@ -249,7 +265,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_wide(const __grid_const
                     for (int u = 0; u < U; ++u) {
                         const int32_t cu = __shfl_sync(0xffffffffu, c, FULL ? s * L + q + u : (s * L + q + u) & 31);
                         if (q + u < nb && (UDIV || q + u < L))
-                            ld8(x[u], a.X + ((int64_t)cu * F + li * 8), KEEP ? 1 : 0);
+                            ldx8<XM>(x[u], a, cu, F, li);
                         else
                             x[u].a = x[u].b = make_float4(0.f, 0.f, 0.f, 0.f);
                     }
@@ -264,8 +280,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_wide(const __grid_const
                                 if (!ov)
                                     store_row<EPI>(a.Y, o, li * 8, F, d, acc, a.epi);
                                 else
-                                    st8((piece ? a.piece_partial + (int64_t)slot * F
-                                               : a.ovp + (int64_t)(b - a.first_ov) * F) + li * 8, acc);
+                                    st8(a.ovp + (int64_t)(b - a.first_ov) * F + li * 8, acc);
                             }
                             acc.a = acc.b = make_float4(0.f, 0.f, 0.f, 0.f);
                             left = d;
@@ -276,7 +291,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_wide(const __grid_const
                 c = cn;
                 v = vn;
             }
-            if (ov && !piece && a.fuse_ov) ov_finish<EPI>(a, m.z, m.x, F, lane, s, li);
+            if (ov && a.fuse_ov) ov_finish<EPI>(a, m.z, m.x, F, lane, s, li);
             continue;
         }
         // ---- rows split over K combined warps (R <= G/2): contiguous parts, xor-tree merge
@@ -289,13 +304,14 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_wide(const __grid_const
             const int32_t r = r0 + g;
             const bool gact = (FULL || g < NG) && r < R;           // idle groups / lanes: no work
             const int32_t mylen = gact ? len_k : 0;
-            const int32_t e0 = __shfl_sync(0xffffffffu, rso_l, r & 31) + p0;  // first entry
+            const int32_t e0 = __shfl_sync(0xffffffffu, rso_l, r & 31) + p0;  // first entry (vals)
+            const int32_t c0 = cd + (r * d + p0);                                // first entry (cols)
             acc.a = acc.b = make_float4(0.f, 0.f, 0.f, 0.f);
             // (colidx, val) pairs, L per batch, one per lane; the next batch is prefetched
             int32_t c = 0;
             float v = 0.f;
             if (li < mylen) {
-                c = __ldg(a.cols + e0 + li);
+                c = __ldg(a.scols + (uint32_t)(c0 + li));
                 v = __ldg(a.vals + e0 + li);
             }
             for (int32_t base = 0; base < part; base += L) {     // warp-uniform trip count
@@ -303,7 +319,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_wide(const __grid_const
                 int32_t cn = 0;
                 float vn = 0.f;
                 if (jn < mylen) {
-                    cn = __ldg(a.cols + e0 + jn);
+                    cn = __ldg(a.scols + (uint32_t)(c0 + jn));
                     vn = __ldg(a.vals + e0 + jn);
                 }
                 const int32_t nb = mylen - base;                 // valid pairs in this batch (may be <= 0)
@@ -316,7 +332,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_wide(const __grid_const
                     for (int u = 0; u < U; ++u) {
                         const int32_t cu = __shfl_sync(0xffffffffu, c, FULL ? s * L + q + u : (s * L + q + u) & 31);
                         if (q + u < nb && (UDIV || q + u < L))
-                            ld8(x[u], a.X + ((int64_t)cu * F + li * 8), KEEP ? 1 : 0);
+                            ldx8<XM>(x[u], a, cu, F, li);
                         else
                             x[u].a = x[u].b = make_float4(0.f, 0.f, 0.f, 0.f);
                     }
@@ -360,66 +376,183 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_wide(const __grid_const
                 if (!ov)
                     store_row<EPI>(a.Y, rd, li * 8, F, d, acc, a.epi);
                 else
-                    st8((piece ? a.piece_partial + (int64_t)slot * F
-                               : a.ovp + (int64_t)(b - a.first_ov) * F) + li * 8, acc);
+                    st8(a.ovp + (int64_t)(b - a.first_ov) * F + li * 8, acc);
             }
         }
-        if (ov && !piece && a.fuse_ov) ov_finish<EPI>(a, m.z, m.x, F, lane, s, li);
+        if (ov && a.fuse_ov) ov_finish<EPI>(a, m.z, m.x, F, lane, s, li);
     }
-    if (a.zero_last) zero_rows();
+    zero_rows();
 }
 
-template <int L, int U, int MINB, bool KEEP, bool PIECES, bool EPI>
-void launch_t(const WideArgs& a, cudaStream_t s) {
-    auto kern = k_spmm_wide<L, U, MINB, KEEP, PIECES, EPI>;
-    static int occ = -1;
-    if (occ < 0) {
+// The oversized-row chunks {deg, loc, row, nnz <= deg_bound} on their own: all G
+// combined warps of a warp split one chunk into contiguous parts (the main kernel's R = 1 case,
+// same split and the same xor-tree merge, so bitwise the same partial rows) with nothing else
+// live -- no row boundaries, no epilogue, no output-row bookkeeping -- so the register budget
+// goes to occupancy: U rows in flight per lane at MINB CTAs of 8 warps per SM.  Level 3 (the
+// chunk partials summed in order) stays with k_ov_reduce_h.
+template <int L, int U, int MINB, int XM>
+__global__ void __launch_bounds__(kThreads, MINB) k_spmm_chunks(const __grid_constant__ WideArgs a) {
+    constexpr int G = 32 / L;
+    constexpr int F = 8 * L;
+    const int lane = threadIdx.x & 31;
+    const int s = lane / L, li = lane % L;
+    const int32_t gw = blockIdx.x * kWarps + (threadIdx.x >> 5);
+    const int32_t W = gridDim.x * kWarps;
+    const int32_t nch = (int32_t)(a.n_desc - a.first_ov);
+    for (int32_t i = gw; i < nch; i += W) {
+        const int4 m = __ldg(a.desc + a.first_ov + i);
+        const int32_t len = m.w;
+        const int32_t vb = __ldg(a.rso + m.z) + (m.y - __ldg(a.srp + m.z));  // chunk start in vals
+        const int32_t part = (len + G - 1) / G;
+        const int32_t p0 = s * part;
+        const int32_t mylen = max(0, min(len - p0, part));
+        const uint32_t cb = (uint32_t)(m.y + p0);
+        const int32_t vbb = vb + p0;
+        f8 acc;
+        acc.a = acc.b = make_float4(0.f, 0.f, 0.f, 0.f);
+        int32_t c = 0;
+        float v = 0.f;
+        if (li < mylen) {
+            c = __ldg(a.scols + cb + li);
+            v = __ldg(a.vals + vbb + li);
+        }
+        for (int32_t base = 0; base < part; base += L) {  // warp-uniform trip count
+            const int32_t jn = base + L + li;
+            int32_t cn = 0;
+            float vn = 0.f;
+            if (jn < mylen) {
+                cn = __ldg(a.scols + cb + jn);
+                vn = __ldg(a.vals + vbb + jn);
+            }
+            const int32_t nb = mylen - base;
+            const int32_t nbu = min(L, part - base);
+#pragma unroll 1
+            for (int q = 0; q < L; q += U) {
+                if (q >= nbu) break;
+                f8 x[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int32_t cu = __shfl_sync(0xffffffffu, c, s * L + q + u);
+                    if (q + u < nb)
+                        ldx8<XM>(x[u], a, cu, F, li);
+                    else
+                        x[u].a = x[u].b = make_float4(0.f, 0.f, 0.f, 0.f);
+                }
+#pragma unroll
+                for (int u = 0; u < U; ++u) fma8(acc, __shfl_sync(0xffffffffu, v, s * L + q + u), x[u]);
+            }
+            c = cn;
+            v = vn;
+        }
+#pragma unroll
+        for (int o = L; o < 32; o <<= 1) {
+            acc.a.x = shfl_xor_add(acc.a.x, o);
+            acc.a.y = shfl_xor_add(acc.a.y, o);
+            acc.a.z = shfl_xor_add(acc.a.z, o);
+            acc.a.w = shfl_xor_add(acc.a.w, o);
+            acc.b.x = shfl_xor_add(acc.b.x, o);
+            acc.b.y = shfl_xor_add(acc.b.y, o);
+            acc.b.z = shfl_xor_add(acc.b.z, o);
+            acc.b.w = shfl_xor_add(acc.b.w, o);
+        }
+        if (s == 0) st8(a.ovp + (int64_t)i * F + li * 8, acc);
+    }
+}
+
+// launch `kern` on a persistent grid (SMs x occupancy, capped by the work) with the hot
+// buffer under a persisting L2 access-policy window when win > 0 (launch attribute)
+template <class K>
+void launch_grid(K kern, int& occ, int64_t work_warps, const WideArgs& a, size_t win, cudaStream_t s) {
+    if (occ <= 0) {
         AGCN_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kThreads, 0));
         if (occ < 1) occ = 1;
     }
-    const int G = 32 / (L ? L : a.L);
-    const int64_t work = std::max<int64_t>(a.n_desc + (a.pieces ? a.piece_cap : 0), (a.n_zero + G - 1) / G);
-    const int64_t want = (work + kWarps - 1) / kWarps;
+    const int64_t want = (work_warps + kWarps - 1) / kWarps;
     const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)num_sms() * occ));
-    kern<<<(unsigned)grid, kThreads, 0, s>>>(a);
+    if (win == 0) {
+        kern<<<(unsigned)grid, kThreads, 0, s>>>(a);
+    } else {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3((unsigned)grid);
+        cfg.blockDim = dim3(kThreads);
+        cfg.stream = s;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeAccessPolicyWindow;
+        at[0].val.accessPolicyWindow.base_ptr = const_cast<float*>(a.Xh);
+        at[0].val.accessPolicyWindow.num_bytes = win;
+        at[0].val.accessPolicyWindow.hitRatio = 1.0f;
+        at[0].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+        at[0].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        AGCN_CUDA(cudaLaunchKernelEx(&cfg, kern, a));
+    }
     post_launch();
 }
 
-int env_int(const char* name, int dflt) {  // experiment switch
-    const char* v = getenv(name);
-    return v ? atoi(v) : dflt;
+int dev_index() {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    return dev >= 0 && dev < 64 ? dev : 0;
 }
 
-template <int L, int U, int MINB, bool EPI>
-void launch_e(const WideArgs& a, bool keep, cudaStream_t s) {
-    if (a.pieces)
-        keep ? launch_t<L, U, MINB, true, true, EPI>(a, s) : launch_t<L, U, MINB, false, true, EPI>(a, s);
-    else
-        keep ? launch_t<L, U, MINB, true, false, EPI>(a, s) : launch_t<L, U, MINB, false, false, EPI>(a, s);
+template <int L, int U, int MINB, int XM, bool EPI>
+void launch_t(const WideArgs& a, size_t win, cudaStream_t s) {
+    static int occ[64] = {};  // per device; a benign race (every thread computes the same value)
+    const int G = 32 / (L ? L : a.L);
+    launch_grid(k_spmm_wide<L, U, MINB, XM, EPI>, occ[dev_index()], std::max<int64_t>(a.n_desc, (a.n_zero + G - 1) / G),
+                a, win, s);
 }
 
-template <int L, int U, int MINB>
-void launch_k(const WideArgs& a, bool keep, cudaStream_t s) {
-    if (a.epi.active())
-        launch_e<L, U, MINB, true>(a, keep, s);
-    else
-        launch_e<L, U, MINB, false>(a, keep, s);
+template <int L, int U, int MINB, int XM>
+void launch_c(const WideArgs& a, size_t win, cudaStream_t s) {
+    static int occ[64] = {};
+    launch_grid(k_spmm_chunks<L, U, MINB, XM>, occ[dev_index()], a.n_desc - a.first_ov, a, win, s);
 }
 
-template <int L>
-void launch(const WideArgs& a, bool keep, cudaStream_t s) {
-    // register budget vs rows in flight (AGCN_WIDE_VARIANT, A/B only; profiles/r01k_wide_ab.md,
-    // r01bc_kernel_shapes.md; the measured-and-dropped shapes -- U 4 at 4 CTAs/SM with spills,
-    // U 2 at 5 CTAs/SM, U 8 at 2 CTAs/SM -- are no longer instantiated):
-    //   0: U 4 at 3 CTAs/SM (80 regs)   4: U 2 at 4 CTAs/SM (64 regs)
-    //  -1 (default): 4 for mid-size graphs at F <= 64 (a.lean: C3 F32/F64 -5..9 %), else 0
-    static const int venv = env_int("AGCN_WIDE_VARIANT", -1);
-    const int variant = venv >= 0 ? venv : (a.lean ? 4 : 0);
+// the chunk kernel's shapes (agcn_spmm_opts_t.chunk_shape)
+template <int L, int XM>
+void launch_chunks(const WideArgs& a, int shape, size_t win, cudaStream_t s) {
     constexpr int U4 = L >= 4 ? 4 : L, U2 = L >= 2 ? 2 : L;
-    if (variant == 4)
-        launch_k<L, U2, 4>(a, keep, s);
+    if (shape == 3)
+        launch_c<L, U4, 3, XM>(a, win, s);
+    else if (shape == 6)
+        launch_c<L, U2, 6, XM>(a, win, s);
     else
-        launch_k<L, U4, 3>(a, keep, s);
+        launch_c<L, U4, 4, XM>(a, win, s);
+}
+
+template <int L, int U, int MINB, int XM>
+void launch_e(const WideArgs& a, size_t win, cudaStream_t s) {
+    if (a.epi.active())
+        launch_t<L, U, MINB, XM, true>(a, win, s);
+    else
+        launch_t<L, U, MINB, XM, false>(a, win, s);
+}
+
+// register budget vs rows in flight (profiles/r01k_wide_ab.md, r01bc_kernel_shapes.md,
+// r01bl_auto_shape.md): U 4 at 3 CTAs/SM (80 registers) by default; U 2 at 4 CTAs/SM (64
+// registers) for mid-size graphs at F <= 64 (lean: C3 F32/F64 -5..9 %).  Hot-row plans (large
+// graphs) always take the default shape.
+template <int L>
+void launch(const WideArgs& a, int xm, bool lean, size_t win, int chunks, cudaStream_t s) {
+    constexpr int U4 = L >= 4 ? 4 : (L ? L : 4), U2 = L >= 2 ? 2 : (L ? L : 2);
+    if (L && chunks) {  // the oversized chunks first, then the rest (n_desc = nb_small)
+        switch (xm) {
+            case 0: launch_chunks<L ? L : 1, 0>(a, chunks, 0, s); break;
+            case 1: launch_chunks<L ? L : 1, 1>(a, chunks, 0, s); break;
+            case 2: launch_chunks<L ? L : 1, 2>(a, chunks, win, s); break;
+            default: launch_chunks<L ? L : 1, 3>(a, chunks, win, s); break;
+        }
+    }
+    WideArgs b = a;
+    if (L && chunks) b.n_desc = a.first_ov;
+    switch (xm) {
+        case 0: lean ? launch_e<L, U2, 4, 0>(b, 0, s) : launch_e<L, U4, 3, 0>(b, 0, s); break;
+        case 1: lean ? launch_e<L, U2, 4, 1>(b, 0, s) : launch_e<L, U4, 3, 1>(b, 0, s); break;
+        case 2: launch_e<L, U4, 3, 2>(b, win, s); break;
+        default: launch_e<L, U4, 3, 3>(b, win, s); break;
+    }
 }
 
 }  // namespace
@@ -430,38 +563,36 @@ bool wide_supported(const agcn_plan_s* p, const float* X, const float* Y, int32_
     return shape && al && p->mbw <= 32;
 }
 
-void launch_wide(agcn_plan_s* p, const float* vals, const float* X, int32_t F, float* Y,
-                 bool l2_keep, bool blocked, bool fuse_ov, const Epi& epi, cudaStream_t s) {
-    const ColSched& cs = p->sched;
-    WideArgs a{p->desc, blocked ? p->nb_small : p->nblocks, p->nb_small, p->n_zero, p->cols,
-               p->sorted_rowptr, p->row_src_off, p->perm, vals + p->rp_base, X, Y, p->ov_partial,
-               p->deg_bound, blocked ? cs.seg : nullptr, blocked ? cs.slot_base + p->n_ov : nullptr,
-               blocked ? cs.partial : nullptr, blocked ? cs.cap : 0, epi};
-    AGCN_CHECK(a.n_desc + a.piece_cap < (1ll << 31), AGCN_ERR_OVERFLOW, "too many descriptors");
+void launch_wide(agcn_plan_s* p, const float* vals, const float* X, const float* Xh, int32_t F, float* Y,
+                 int l2, size_t win, bool fuse_ov, int chunk_shape, const Epi& epi, cudaStream_t s) {
+    WideArgs a{p->desc, p->nblocks, p->nb_small, p->n_zero, p->scols, p->sorted_rowptr, p->row_src_off,
+               p->perm, vals + p->rp_base, X, Xh, Y, p->ov_partial, p->deg_bound, epi};
+    AGCN_CHECK(a.n_desc < (1ll << 31), AGCN_ERR_OVERFLOW, "too many descriptors");
     a.L = F / 8;
-    static const int zero_last = env_int("AGCN_ZERO_LAST", 1);  // C5 -1 %, C3/C4 even (profiles r01bj)
-    a.zero_last = zero_last;
-    a.fuse_ov = fuse_ov && !blocked && p->n_ov > 0 && p->ov_cnt != nullptr;
+    a.fuse_ov = fuse_ov && p->n_ov > 0 && p->ov_cnt != nullptr;
     a.ov_cs = p->ov_chunk_start;
     a.ov_cnt = p->ov_cnt;
     a.ov_start = p->ov_start;
-    {   // nnz per resident warp of the default shape: mid-size graphs (C3: 328) are latency-
-        // bound with few descriptors per warp, where 32 warps/SM at U 2 win (profiles r01bl)
-        const double share = (double)p->nnz / ((double)num_sms() * 24.0);
-        a.lean = F <= 64 && share >= 100.0 && share <= 4000.0;
-    }
+    // X residency mode: plans with hot rows always decode hot columns (2, or 3 with hints)
+    const int xm = p->n_hot > 0 ? (l2 == AGCN_L2_HOT_HINTS ? 3 : 2) : (l2 == AGCN_L2_KEEP_ALL ? 1 : 0);
+    if (xm < 2) win = 0;
+    // nnz per resident warp of the default shape: mid-size graphs (C3: 328) are latency-
+    // bound with few descriptors per warp, where 32 warps/SM at U 2 win (profiles r01bl)
+    const double share = (double)p->nnz / ((double)num_sms() * 24.0);
+    const bool lean = F <= 64 && share >= 100.0 && share <= 4000.0;
+    // the chunk kernel: plans whose oversized chunks are not merged in-kernel (level 3 by
+    // k_ov_reduce_h), power-of-two L
+    // auto: F >= 128 (C4 -13 %; C5 at F = 64 measured neutral to +2 %, profiles/r02_c5_roof.md)
+    const int chunks = (!a.fuse_ov && p->ov_chunks > 0 && chunk_shape >= 0 && (chunk_shape || F >= 128))
+                           ? (chunk_shape ? chunk_shape : 4) : 0;
     switch (F) {
-        case 8: launch<1>(a, l2_keep, s); break;
-        case 16: launch<2>(a, l2_keep, s); break;
-        case 32: launch<4>(a, l2_keep, s); break;
-        case 64: launch<8>(a, l2_keep, s); break;
-        case 128: launch<16>(a, l2_keep, s); break;
-        case 256: launch<32>(a, l2_keep, s); break;
-        default: {  // F = 8 L, L not a power of two: one kernel with L at run time
-            static const int minb = env_int("AGCN_WIDE_RT_MINB", 3);
-            minb == 2 ? launch_k<0, 4, 2>(a, l2_keep, s) : launch_k<0, 4, 3>(a, l2_keep, s);
-            break;
-        }
+        case 8: launch<1>(a, xm, lean, win, chunks, s); break;
+        case 16: launch<2>(a, xm, lean, win, chunks, s); break;
+        case 32: launch<4>(a, xm, lean, win, chunks, s); break;
+        case 64: launch<8>(a, xm, lean, win, chunks, s); break;
+        case 128: launch<16>(a, xm, lean, win, chunks, s); break;
+        case 256: launch<32>(a, xm, lean, win, chunks, s); break;
+        default: launch<0>(a, xm, false, win, 0, s); break;  // F = 8 L, L not a power of two (run-time L)
     }
 }
 

@@ -209,8 +209,7 @@ def test_spmm_c2_F(F):
 
 KERNEL_F = [("general", F) for F in (3, 4, 16, 64, 128, 100)] + \
     [("looped", F) for F in (1, 16, 33, 64, 100, 128)] + \
-    [("wide", F) for F in (8, 16, 24, 32, 40, 64, 96, 128, 200, 248, 256)] + \
-    [("pipe", F) for F in (32, 64, 128, 256)]
+    [("wide", F) for F in (8, 16, 24, 32, 40, 64, 96, 128, 200, 248, 256)]
 
 
 @pytest.mark.parametrize("kernel,F", KERNEL_F)
@@ -229,34 +228,77 @@ def test_spmm_every_kernel(kernel, F):
         check_spmm(p, rowptr, colidx, vals, X, kernel=kernel)
 
 
-@pytest.mark.parametrize("F", [8, 64, 96, 128, 256])
-def test_column_blocked_oversized_rows(F):
-    """Oversized rows executed as column-blocked pieces (agcn_spmm_opts_t.col_block_mb) give
-    the oracle's result; unsorted rows (plain chunks) and sorted rows mixed; deterministic."""
-    rng = np.random.default_rng(F)
-    n_cols = 100000
-    degs = np.array([0, 3, 385, 900, 5000, 17, 384, 2000, 769, 12000, 1, 0, 400, 2100, 30000])
-    rowptr, colidx = _rows_csr(degs, n_cols, 3)
-    colidx = colidx.copy()
-    for r in range(degs.size):  # canonical CSR: sorted columns per row (duplicates kept)
-        colidx[rowptr[r]:rowptr[r + 1]].sort()
-    for r in (2, 7):  # two light rows with unsorted columns
-        a, b = rowptr[r], rowptr[r + 1]
-        colidx[a:b] = rng.permutation(colidx[a:b])
-    a = rowptr[9] + 1000  # a heavy row unsorted in a window straddling two chunks
-    colidx[a:a + 500] = rng.permutation(colidx[a:a + 500])
-    a = rowptr[14] + 384 * 7  # a chunk of a heavy row starting below the previous entry
-    colidx[a:a + 384] = np.sort(rng.integers(0, 50, 384))
+def _hub_graph(n, seed, F):
+    """Square power-law CSR with hubs (rows of degree > deg_bound), X and vals."""
+    rng = np.random.default_rng(seed)
+    degs = np.minimum(rng.zipf(1.4, size=n) - 1, 3 * n).astype(np.int64)
+    degs[rng.random(n) < 0.3] = 0
+    degs[rng.integers(0, n, 3)] = [2000, 900, 385]
+    rowptr = np.zeros(n + 1, dtype=np.int32)
+    rowptr[1:] = np.cumsum(degs)
+    w = 1.0 / np.arange(1, n + 1) ** 0.8
+    w = w[rng.permutation(n)]
+    colidx = rng.choice(n, size=int(rowptr[-1]), p=w / w.sum()).astype(np.int32)
     vals = rng.uniform(-1, 1, colidx.size).astype(np.float32)
-    X = rng.uniform(-1, 1, (n_cols, F)).astype(np.float32)
-    p = make_plan(rowptr, colidx, n_cols=n_cols)
-    Ys = []
-    for mb in (1, 2, 0):  # 1 MiB and 2 MiB blocks, then off
-        Y = p.spmm(cu(vals), cu(X), kernel="wide", col_block_mb=mb).cpu().numpy()
-        check_spmm(p, rowptr, colidx, vals, X, Y)
-        Ys.append(Y)
-    Y2 = p.spmm(cu(vals), cu(X), kernel="wide", col_block_mb=1).cpu().numpy()
-    assert np.array_equal(Ys[0], Y2)          # bitwise reproducible
+    X = rng.uniform(-1, 1, (n, F)).astype(np.float32)
+    return rowptr, colidx, vals, X
+
+
+@pytest.mark.parametrize("F", [8, 40, 64, 128, 256, 100, 3])
+def test_hot_rows_every_mode(F):
+    """Hot X rows (agcn_opts_t.hot_rows): the plan re-encodes the columns of its hot vertices
+    (tail of the degree order) and agcn_spmm reads them from a compact gathered buffer.  Every
+    hot count x L2 mode x kernel gives the oracle's result, bitwise equal to the plan without
+    hot rows (the summation order does not change); the sorted colidx copy decodes exactly."""
+    rowptr, colidx, vals, X = _hub_graph(3000, F, F)
+    o = oracle.plan(rowptr, colidx, 12, 32)
+    ref = make_plan(rowptr, colidx, hot_rows=0)
+    assert ref.stats()["hot_rows"] == 0
+    Y0 = check_spmm(ref, rowptr, colidx, vals, X)
+    kernels = ["auto", "general"] + (["wide"] if F % 8 == 0 else [])
+    for H in (1, 17, 500, 10 ** 9):
+        p = make_plan(rowptr, colidx, hot_rows=H)
+        live = int((np.diff(rowptr) > 0).sum())
+        assert p.stats()["hot_rows"] == min(H, live)
+        assert np.array_equal(p.copy("sorted_colidx"), o["sorted_colidx"])
+        assert np.array_equal(p.copy("blocks"), o["blocks"])
+        for kernel in kernels:
+            for l2 in ("auto", "none", "keep_all", "hot_window", "hot_hints"):
+                for hot_mb in (None, 1):
+                    Y = p.spmm(cu(vals), cu(X), kernel=kernel, l2_hint=l2, hot_mb=hot_mb).cpu().numpy()
+                    if kernel == "general":
+                        check_spmm(p, rowptr, colidx, vals, X, Y)
+                    else:
+                        assert np.array_equal(Y, Y0), (H, kernel, l2, hot_mb)
+
+
+def test_hot_rows_auto_rule():
+    """hot_rows = -1: on for square graphs with n >= 2^19, off otherwise and for padded layouts."""
+    rowptr = np.zeros(2 ** 19 + 1, dtype=np.int32)
+    rowptr[1:] = np.arange(1, 2 ** 19 + 1)
+    colidx = (np.arange(2 ** 19, dtype=np.int64) * 7919 % 2 ** 19).astype(np.int32)
+    p = make_plan(rowptr, colidx)
+    assert p.stats()["hot_rows"] == 262144
+    p2 = make_plan(rowptr, colidx, n_cols=2 ** 19 + 5)
+    assert p2.stats()["hot_rows"] == 0
+    vals = np.ones(colidx.size, np.float32)
+    X = np.random.default_rng(0).uniform(-1, 1, (2 ** 19, 8)).astype(np.float32)
+    Y = p.spmm(cu(vals), cu(X)).cpu().numpy()
+    assert np.array_equal(Y, X[colidx])
+
+
+def test_plan_copies_colidx():
+    """the caller may free or change rowptr / colidx after agcn_plan returns."""
+    w = gen.make_config("c2", vals_kind="uniform")
+    X = w.X(64)
+    for part in ("block", "warp"):
+        rp, ci = cu(w.rowptr), cu(w.colidx)
+        p = A.Plan(rp, ci, partition=part)
+        ci.fill_(-7)
+        rp.fill_(0)
+        del rp, ci
+        torch.cuda.empty_cache()
+        check_spmm(p, w.rowptr, w.colidx, w.vals, X)
 
 
 def test_spmm_kernel_unsupported_is_reported():
@@ -266,7 +308,7 @@ def test_spmm_kernel_unsupported_is_reported():
         p.spmm(cu(w.vals), cu(w.X(100)), kernel="wide")
     assert e.value.status == "AGCN_ERR_UNSUPPORTED"
     with pytest.raises(A.AgcnError):
-        p.spmm(cu(w.vals), cu(w.X(64)), kernel="wide", l2_hint=2)
+        p.spmm(cu(w.vals), cu(w.X(64)), kernel="wide", l2_hint=7)
 
 
 def test_wide_kernel_nonfinite_x_rows_not_referenced():
@@ -277,7 +319,7 @@ def test_wide_kernel_nonfinite_x_rows_not_referenced():
     X = np.ones((7, 64), dtype=np.float32)
     X[0] = np.inf
     X[6] = np.nan
-    for kernel in ("auto", "general", "looped", "wide", "pipe"):
+    for kernel in ("auto", "general", "looped", "wide"):
         p = make_plan(rowptr, colidx, n_cols=7)
         Y = p.spmm(cu(vals), cu(X), kernel=kernel).cpu().numpy()
         assert np.isfinite(Y).all(), kernel
@@ -453,7 +495,7 @@ EPI_CASES = [
 
 
 @pytest.mark.parametrize("kernel,F", [("auto", 64), ("wide", 128), ("wide", 40), ("general", 100), ("general", 64),
-                                      ("looped", 16), ("pipe", 64)])
+                                      ("looped", 16)])
 @pytest.mark.parametrize("case", range(len(EPI_CASES)))
 def test_spmm_epilogue(kernel, F, case):
     """GCN / GraphSAGE-mean / GIN aggregation with bias and ReLU vs the oracle, through
