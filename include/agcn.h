@@ -75,6 +75,10 @@ typedef struct {
        0: off; > 0: that many rows (capped at the rows of degree >= 1).  Results do not depend
        on it.  Costs the plan one lookup per nonzero (C5: +0.4 ms). */
     int64_t hot_rows;
+    int32_t small_plan;        /* 1 (default): graphs within the one-CTA limits (see agcn_plan_ex)
+                                  take the one-CTA plan; 0: always the general plan (same
+                                  metadata; for tests and measurements) */
+    int32_t reserved0;
 } agcn_opts_t;
 
 typedef struct {
@@ -299,8 +303,11 @@ agcn_status_t agcn_propagate_host(const int32_t* rowptr_host, const int32_t* col
  *   vals and writes the ybufs at these addresses (write new features into X in place).
  *   layers > 1 needs a square A.  NULL on failure.
  * agcn_graph_launch: asynchronous on `stream` (any stream; launches on one graph must be
- *   stream-ordered, as agcn_spmm calls on one plan).
- * agcn_graph_destroy: frees the graph.  The plan must outlive the graph and its launches.
+ *   stream-ordered, as agcn_spmm calls on one plan).  agcn_plan_destroy is ordered after the
+ *   latest launch.
+ * agcn_graph_destroy: frees the graph.  The plan must outlive the graph.  While a graph of a
+ *   plan exists, an agcn_spmm on that plan that would grow its scratch (a larger F than any
+ *   captured one) returns AGCN_ERR_UNSUPPORTED instead of moving memory under the graph.
  */
 typedef struct agcn_graph_s* agcn_graph_t;
 agcn_graph_t  agcn_graph_create(agcn_plan_t plan, const float* vals, const float* X, int32_t F, int32_t layers,

@@ -95,7 +95,7 @@ def spmm_check(rowptr, colidx, vals, X, Y, rows=None, rel=REL_TOL, abs_tol=ABS_T
     """Streaming tolerance check of a candidate fp32 Y against the fp64 definition.
 
     rows=None: Y is the full n x F output.  Otherwise Y[t] is output row rows[t].
-    Returns dict(max_ratio, worst=(row, col), nfail); pass iff nfail == 0 (ratio <= 1).
+    Returns dict(max_ratio, worst=(row, col), nfail, rows checked); pass iff nfail == 0 (ratio <= 1).
     """
     rowptr = _c(rowptr, np.int32); colidx = _c(colidx, np.int32)
     vals = _c(vals, np.float32); X = _c(X, np.float32); Y = _c(Y, np.float32)
@@ -114,7 +114,8 @@ def spmm_check(rowptr, colidx, vals, X, Y, rows=None, rel=REL_TOL, abs_tol=ABS_T
         nf = _load().orc_spmm_check(n, _p(rowptr, I32P), _p(colidx, I32P), _p(vals, F32P),
                                     _p(X, F32P), F, _p(Y, F32P), None, 0, rel, abs_tol,
                                     ctypes.byref(mr), _p(worst, I64P), nthreads)
-    return {"max_ratio": mr.value, "worst": (int(worst[0]), int(worst[1])), "nfail": int(nf)}
+    return {"max_ratio": mr.value, "worst": (int(worst[0]), int(worst[1])), "nfail": int(nf),
+            "rows": int(n if rows is None else rows.size)}
 
 
 def spmm_epilogue(rowptr, colidx, vals, X, aggregation="sum", self_x=None, self_scale=0.0,

@@ -95,7 +95,7 @@ class Plan:
     def __init__(self, rowptr, colidx, n: int | None = None, nnz: int | None = None, *,
                  n_cols: int | None = None, max_block_warps: int = 12, max_warp_nzs: int = 32,
                  partition: str = "block", col_bounds=None, col_slot_rows: int | None = None,
-                 hot_rows: int | None = None, stream=None):
+                 hot_rows: int | None = None, small_plan: bool = True, stream=None):
         L = _lib.lib()
         rp = _dev_ptr(rowptr, "int32", "rowptr")
         ci = _dev_ptr(colidx, "int32", "colidx") if colidx.numel() else 0
@@ -111,6 +111,7 @@ class Plan:
         opts.n_cols = 0 if n_cols is None else int(n_cols)
         opts.stream = _stream_handle(stream)
         opts.hot_rows = -1 if hot_rows is None else int(hot_rows)
+        opts.small_plan = int(bool(small_plan))
         self._bounds_keep = None
         if col_bounds is not None:
             b = np.ascontiguousarray(col_bounds, dtype=np.int64)

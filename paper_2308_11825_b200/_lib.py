@@ -19,7 +19,8 @@ class Opts(ctypes.Structure):
     _fields_ = [("max_block_warps", c_i32), ("max_warp_nzs", c_i32), ("partition", c_i32),
                 ("validate", c_i32), ("n_cols", c_i64), ("stream", c_vp),
                 ("col_bounds", ctypes.POINTER(c_i64)), ("col_nparts", c_i32),
-                ("col_slot_rows", c_i64), ("hot_rows", c_i64)]
+                ("col_slot_rows", c_i64), ("hot_rows", c_i64), ("small_plan", c_i32),
+                ("reserved0", c_i32)]
 
 
 KERNELS = {"auto": 0, "general": 1, "looped": 2, "wide": 3}

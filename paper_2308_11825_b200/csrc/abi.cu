@@ -75,6 +75,7 @@ void agcn_default_opts(agcn_opts_t* o) {
     o->partition = AGCN_PARTITION_BLOCK;
     o->validate = 1;
     o->hot_rows = -1;
+    o->small_plan = 1;
 }
 
 agcn_plan_t agcn_plan_ex(const int32_t* rowptr, const int32_t* colidx, int64_t n, int64_t nnz,

@@ -12,6 +12,7 @@ struct agcn_graph_s {
     cudaGraph_t graph = nullptr;
     cudaGraphExec_t exec = nullptr;
     int device = 0;
+    agcn_plan_s* plan = nullptr;  // counted in plan->n_graphs while the graph lives
 };
 
 extern "C" {
@@ -56,6 +57,8 @@ agcn_graph_t agcn_graph_create(agcn_plan_t plan, const float* vals, const float*
         }
         AGCN_CUDA(cudaStreamEndCapture(g->s, &g->graph));
         AGCN_CUDA(cudaGraphInstantiate(&g->exec, g->graph, 0));
+        g->plan = plan;
+        plan->n_graphs.fetch_add(1);
     });
     if (st != AGCN_OK && g) {
         if (g->exec) cudaGraphExecDestroy(g->exec);
@@ -70,14 +73,22 @@ agcn_graph_t agcn_graph_create(agcn_plan_t plan, const float* vals, const float*
 agcn_status_t agcn_graph_launch(agcn_graph_t g, agcn_stream_t stream) {
     return agcn::guarded([&] {
         AGCN_CHECK(g && g->exec, AGCN_ERR_INVALID_ARG, "NULL graph");
-        AGCN_CUDA(cudaGraphLaunch(g->exec, (cudaStream_t)stream));
+        cudaStream_t s = (cudaStream_t)stream;
+        agcn_plan_s* p = g->plan;
+        AGCN_CUDA(cudaGraphLaunch(g->exec, s));
         agcn::count_launch();
+        // order agcn_plan_destroy (stream-ordered on the plan's stream) after this replay
+        if (s != p->stream) {
+            if (!p->last_use) AGCN_CUDA(cudaEventCreateWithFlags(&p->last_use, cudaEventDisableTiming));
+            AGCN_CUDA(cudaEventRecord(p->last_use, s));
+        }
     });
 }
 
 agcn_status_t agcn_graph_destroy(agcn_graph_t g) {
     return agcn::guarded([&] {
         if (!g) return;
+        if (g->plan) g->plan->n_graphs.fetch_sub(1);
         if (g->exec) cudaGraphExecDestroy(g->exec);
         if (g->graph) cudaGraphDestroy(g->graph);
         if (g->s) cudaStreamDestroy(g->s);

@@ -219,6 +219,7 @@ struct agcn_plan_s {
 
     size_t device_bytes = 0;
     bool capturing = false;         // agcn_graph_create: SpMMs being captured (plan complete)
+    std::atomic<int> n_graphs{0};   // live agcn_graph_t holding this plan's scratch pointers
     cudaStream_t stream = nullptr;  // stream the plan was built on
     cudaEvent_t ready = nullptr;    // recorded on `stream` when the plan is complete
     cudaEvent_t last_use = nullptr; // recorded after an SpMM issued on a stream != `stream`

@@ -295,7 +295,14 @@ agcn_status_t agcn_pipe_wait(agcn_pipe_t pipe) {
     return agcn::guarded([&] {
         AGCN_CHECK(pipe, AGCN_ERR_INVALID_ARG, "NULL pipe");
         agcn::DeviceScope dev(pipe->device);
-        drain(pipe);
+        // every job's copies finish before this returns, also when one job failed (the caller
+        // may read or free the other jobs' Y buffers right after an error)
+        try {
+            drain(pipe);
+        } catch (...) {
+            try { sync_all(pipe); } catch (...) {}
+            throw;
+        }
         sync_all(pipe);
     });
 }

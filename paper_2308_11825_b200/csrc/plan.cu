@@ -713,6 +713,18 @@ k_plan_small(const int32_t* __restrict__ rowptr, const int32_t* __restrict__ col
     if (ovc) atomicAdd(&s_ovc, (unsigned long long)ovc);
     if (ovh) atomicAdd(&s_ovh, (unsigned long long)ovh);
     __syncthreads();
+    // an invalid rowptr (decreasing, or rowptr[n] - rowptr[0] != nnz) would size the descriptor
+    // array wrongly (it has room for n + nnz / db + kSmallOv + 1 entries): report before any
+    // global write (the host turns the flags into AGCN_ERR_BAD_CSR)
+    if (s_bad || (int64_t)rowptr[n] - base != nnz) {
+        if (tid == 0) {
+            out->fallback = 0;
+            out->bad_rowptr = s_bad;
+            out->rowptr_first = base;
+            out->rowptr_last = rowptr[n];
+        }
+        return;
+    }
     // (2b) bucket totals, bucket starts, (bin, warp) offsets in item order
     for (int b = tid; b < nbins; b += kSmallThreads) {
         int32_t t = 0;
@@ -869,8 +881,7 @@ k_plan_small(const int32_t* __restrict__ rowptr, const int32_t* __restrict__ col
 // than kSmallOv oversized rows; errors (bad CSR) are thrown as in the general path.
 bool build_block_plan_small(agcn_plan_s* p, const int32_t* rowptr, const int32_t* colidx,
                             const agcn_opts_t& o, cudaStream_t s) {
-    const char* env = getenv("AGCN_SMALL_PLAN");  // read per plan (tests switch it)
-    if (env && atoi(env) == 0) return false;
+    if (!o.small_plan) return false;
     const int64_t n = p->n, nnz = p->nnz;
     const int32_t db = p->deg_bound;
     if (n <= 0 || n > kSmallRows || nnz > kSmallNnz || db > kSmallDb) return false;

@@ -697,6 +697,12 @@ void spmm_launch(agcn_plan_s* p, const float* vals, const float* X, int32_t F, f
                "WIDE kernel needs F = 8 L <= 256, 32-byte aligned X/Y, max_block_warps <= 32");
     // oversized-row partial buffer of the paper's chunks (grows, stream-ordered)
     const size_t need = (size_t)p->ov_chunks * (size_t)F;
+    // scratch captured by a graph (agcn_graph_create) must not move under it
+    AGCN_CHECK(p->n_graphs.load() == 0 || (need <= p->ov_partial_floats &&
+                                           (size_t)p->n_hot * (size_t)F <= p->xhot_floats),
+               AGCN_ERR_UNSUPPORTED,
+               "a CUDA graph of this plan holds its scratch: a larger F needs agcn_graph_destroy first "
+               "(or create the graph with the largest F)");
     if (need > p->ov_partial_floats) {
         if (p->ov_partial) AGCN_CUDA(cudaFreeAsync(p->ov_partial, s));
         p->ov_partial = nullptr;

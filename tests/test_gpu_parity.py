@@ -33,8 +33,8 @@ def make_plan(rowptr, colidx, **kw):
     return A.Plan(cu(rowptr.astype(np.int32)), cu(colidx.astype(np.int32)), **kw)
 
 
-def check_plan_vs_oracle(rowptr, colidx, mbw=12, mwn=32, n_cols=None):
-    p = make_plan(rowptr, colidx, max_block_warps=mbw, max_warp_nzs=mwn, n_cols=n_cols)
+def check_plan_vs_oracle(rowptr, colidx, mbw=12, mwn=32, n_cols=None, **kw):
+    p = make_plan(rowptr, colidx, max_block_warps=mbw, max_warp_nzs=mwn, n_cols=n_cols, **kw)
     o = oracle.plan(rowptr, colidx, mbw, mwn)
     assert np.array_equal(p.copy("perm"), o["perm"])
     assert np.array_equal(p.copy("sorted_rowptr"), o["sorted_rowptr"])
@@ -86,7 +86,7 @@ def test_metadata_bit_exact_random(seed):
 
 
 def _plan_fields(p):
-    return {f: p.copy(f) for f in ("perm", "sorted_rowptr", "row_src_off", "blocks")}, p.stats()
+    return {f: p.copy(f) for f in ("perm", "sorted_rowptr", "row_src_off", "blocks", "sorted_colidx")}, p.stats()
 
 
 @pytest.mark.parametrize("seed", range(24))
@@ -105,16 +105,12 @@ def test_small_plan_equals_general_plan(seed):
         rowptr, colidx = gen.random_csr(n, nc, seed, max_deg=int(rng.choice([4, 60, 700])),
                                         dup=bool(seed % 2))
     got = {}
-    for small in ("1", "0"):
-        os.environ["AGCN_SMALL_PLAN"] = small
-        try:
-            p = check_plan_vs_oracle(rowptr, colidx, mbw, mwn, n_cols=nc)
-        finally:
-            os.environ.pop("AGCN_SMALL_PLAN", None)
+    for small in (True, False):
+        p = check_plan_vs_oracle(rowptr, colidx, mbw, mwn, n_cols=nc, small_plan=small)
         got[small] = _plan_fields(p)
-    for f in got["1"][0]:
-        assert np.array_equal(got["1"][0][f], got["0"][0][f]), f
-    s1, s0 = got["1"][1], got["0"][1]
+    for f in got[True][0]:
+        assert np.array_equal(got[True][0][f], got[False][0][f]), f
+    s1, s0 = got[True][1], got[False][1]
     for k in ("nblocks", "n_zero_rows", "n_oversized_rows", "n_oversized_blocks", "max_deg", "deg_bound"):
         assert s1[k] == s0[k], k
 
@@ -386,24 +382,31 @@ def _sample_rows(rowptr, k, seed):
 
 
 @pytest.mark.parametrize("name", ["c4", "c5"])
-def test_full_size_sampled(name):
+def test_full_size_every_row(name):
+    """BASELINE configs C4 and C5 at full size: metadata bit-exact, and EVERY output row of every
+    layer within the north_star tolerance of the fp64 oracle (streaming check),
+    through the default path (C5: hot rows on); the plan without hot rows gives bitwise the same Y."""
     w = gen.make_config(name)
     rp, ci, va = cu(w.rowptr), cu(w.colidx), cu(w.vals)
     p = A.Plan(rp, ci)
     o = oracle.plan(w.rowptr, w.colidx)                 # integer metadata bit-exact at full size
     for field in ("perm", "sorted_rowptr", "row_src_off", "blocks", "sorted_colidx"):
         assert np.array_equal(p.copy(field), o[field]), field
+    del o
     X = w.X()
     Xd = cu(X)
-    rows = _sample_rows(w.rowptr, 3000, 1)
     Y = p.spmm(va, Xd)
-    r = oracle.spmm_check(w.rowptr, w.colidx, w.vals, X, Y[cu(rows)].cpu().numpy(), rows=rows)
-    assert r["nfail"] == 0, r
+    Yh = Y.cpu().numpy()
+    r = oracle.spmm_check(w.rowptr, w.colidx, w.vals, X, Yh)
+    assert r["nfail"] == 0 and r["rows"] == w.n, r
+    if p.stats()["hot_rows"] > 0:
+        p0 = A.Plan(rp, ci, hot_rows=0)
+        assert torch.equal(p0.spmm(va, Xd), Y)
+        p0.close()
     if w.layers > 1:                                   # layer 2 on the GPU's own layer-1 output
-        Y1 = Y.cpu().numpy()
-        Y2 = p.spmm(va, Y)
-        r = oracle.spmm_check(w.rowptr, w.colidx, w.vals, Y1, Y2[cu(rows)].cpu().numpy(), rows=rows)
-        assert r["nfail"] == 0, r
+        Y2 = p.spmm(va, Y).cpu().numpy()
+        r = oracle.spmm_check(w.rowptr, w.colidx, w.vals, Yh, Y2)
+        assert r["nfail"] == 0 and r["rows"] == w.n, r
     # properties at full size: all-ones X gives row sums of vals
     ones = torch.ones((w.n, 4), device=DEV)
     Ys = p.spmm(va, ones).cpu().numpy()
@@ -467,6 +470,15 @@ def test_bad_csr_is_reported():
     with pytest.raises(A.AgcnError) as e:
         make_plan(rowptr, np.zeros(5, np.int32))
     assert e.value.status == "AGCN_ERR_BAD_CSR"
+    # a bogus huge degree (the one-CTA plan must not emit its oversized chunks
+    # before the check), decreasing or with the wrong total, on both plan paths
+    for rp, nnz in (([0, 1000000, 5], 5), ([0, 1000000], 5), ([0, 5, 1000000, 5], 5)):
+        for small in (True, False):
+            with pytest.raises(A.AgcnError) as e:
+                A.Plan(cu(np.array(rp, np.int32)), cu(np.zeros(8, np.int32)), len(rp) - 1, nnz,
+                       small_plan=small)
+            assert e.value.status == "AGCN_ERR_BAD_CSR", (rp, small)
+    torch.cuda.synchronize()  # the device is still healthy (no out-of-bounds write happened)
     with pytest.raises(A.AgcnError) as e:
         make_plan(np.array([0, 1, 2], np.int32), np.array([0, 7], np.int32), n_cols=3)
     assert e.value.status == "AGCN_ERR_BAD_CSR"
@@ -684,8 +696,19 @@ def test_pipeline_error_leaves_executor_usable():
                                        Yb.ctypes.data) == 2
     Y = pipe.submit(w.rowptr, w.colidx, w.vals, X, 1)
     pipe.wait()
+    ref = A.propagate_host(w.rowptr, w.colidx, w.vals, X, 1)
+    assert np.array_equal(Y, ref)
+    # a good job and a bad job in one batch: the failing wait still returns only after the good
+    # job's Y is written
+    w3 = gen.make_config("c3")
+    X3 = w3.X(64)
+    Yg = pipe.submit(w3.rowptr, w3.colidx, w3.vals, X3, 2)
+    pipe.submit(w.rowptr, bad, w.vals, X, 1)
+    with pytest.raises(A.AgcnError) as e:
+        pipe.wait()
+    assert e.value.status == "AGCN_ERR_BAD_CSR"
+    assert np.array_equal(Yg, A.propagate_host(w3.rowptr, w3.colidx, w3.vals, X3, 2))
     pipe.close()
-    assert np.array_equal(Y, A.propagate_host(w.rowptr, w.colidx, w.vals, X, 1))
 
 
 @pytest.mark.parametrize("name,F,layers", [("c1", 16, 2), ("c2", 64, 3), ("c3", 40, 1)])
@@ -714,4 +737,28 @@ def test_graphed_propagation(name, F, layers):
     assert torch.equal(Y, ref)
     if layers == 1:
         assert oracle.spmm_check(w.rowptr, w.colidx, w.vals, X2.cpu().numpy(), Y.cpu().numpy())["nfail"] == 0
+    g.close()
+
+
+def test_graph_scratch_guard():
+    """While a captured graph holds a plan's scratch, an SpMM that would grow it is refused
+    (ADVICE r01); smaller F works; after the graph is destroyed the plan grows normally."""
+    w = gen.make_config("c3")  # has oversized rows: level-3 scratch
+    rp, ci, va = cu(w.rowptr), cu(w.colidx), cu(w.vals)
+    X16 = cu(w.X(16))
+    g = A.GraphedPropagation(rp, ci, va, X16, 2)
+    p = g.plan
+    X64 = cu(w.X(64))
+    with pytest.raises(A.AgcnError) as e:
+        p.spmm(va, X64)
+    assert e.value.status == "AGCN_ERR_UNSUPPORTED"
+    Y8 = p.spmm(va, cu(w.X(8))).cpu().numpy()
+    check_spmm(p, w.rowptr, w.colidx, w.vals, w.X(8), Y8)
+    s = torch.cuda.Stream()
+    g.replay(stream=s)           # launch on another stream: the plan's destroy is ordered after it
+    _lib_destroy = A._lib.lib().agcn_graph_destroy(g._h)
+    assert _lib_destroy == 0
+    g._h = None
+    Y64 = p.spmm(va, X64).cpu().numpy()
+    check_spmm(p, w.rowptr, w.colidx, w.vals, w.X(64), Y64)
     g.close()
