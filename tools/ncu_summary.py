@@ -18,6 +18,10 @@ METRICS = {
     "dram_read_pct": ("dram__bytes_read.sum.pct_of_peak_sustained_elapsed", None),
     "dram_write_pct": ("dram__bytes_write.sum.pct_of_peak_sustained_elapsed", None),
     "l2_hit_pct": ("lts__t_sector_hit_rate.pct", None),
+    "l2_read_hit_pct": ("lts__t_sector_op_read_hit_rate.pct", None),
+    "l1_ld_sectors": ("l1tex__t_sectors_pipe_lsu_mem_global_op_ld.sum", None),
+    "l1_ld_requests": ("l1tex__t_requests_pipe_lsu_mem_global_op_ld.sum", None),
+    "l1_ld_wavefronts": ("l1tex__t_output_wavefronts_pipe_lsu_mem_global_op_ld.sum", None),
     "l1_hit_pct": ("l1tex__t_sector_hit_rate.pct", None),
     "lts_throughput_pct": ("lts__throughput.avg.pct_of_peak_sustained_elapsed", None),
     "l1_throughput_pct": ("l1tex__throughput.avg.pct_of_peak_sustained_elapsed", None),
@@ -55,6 +59,8 @@ def summarise(rep):
                 u = units[hdr.index(m)]
                 v *= conv.get(u, 1.0)
             e[k] = round(v, 4)
+        if e.get("l1_ld_requests"):
+            e["l1_sectors_per_request"] = round(e["l1_ld_sectors"] / e["l1_ld_requests"], 3)
         if "dram_read_GB" in e and "dram_write_GB" in e:
             e["dram_traffic_GB"] = round(e["dram_read_GB"] + e["dram_write_GB"], 4)
         res.append(e)
@@ -67,9 +73,9 @@ def main():
     for r in reps:
         allr += summarise(r)
     json.dump(allr, open(prefix + ".json", "w"), indent=1)
-    keys = ["report", "duration_us", "dram_traffic_GB", "dram_read_pct", "l2_hit_pct", "l1_hit_pct",
-            "lts_throughput_pct", "warps_active_pct", "registers", "cycles_per_issue",
-            "stall_long_scoreboard"]
+    keys = ["report", "kernel", "duration_us", "dram_traffic_GB", "dram_read_pct", "l2_hit_pct",
+            "l2_read_hit_pct", "l1_hit_pct", "l1_sectors_per_request", "lts_throughput_pct",
+            "warps_active_pct", "registers", "cycles_per_issue", "stall_long_scoreboard"]
     with open(prefix + ".md", "w") as f:
         f.write("| " + " | ".join(keys) + " |\n|" + "---|" * len(keys) + "\n")
         for e in allr:
