@@ -357,6 +357,22 @@ agcn_status_t agcn_gather_vals(const float* vals, const int32_t* src, int64_t nn
 agcn_status_t agcn_gemm_xw(const float* X, int64_t M, int32_t K, const float* Wt, int32_t N, float* Y,
                            const float* bias, int32_t relu, agcn_stream_t stream);
 
+/*
+ * agcn_gemm_xw with a precision choice (the X.W of the GCN layer):
+ *   AGCN_GEMM_FP32: fp32 accuracy, |y - y_ref| <= ~2^-19 sum_k |x_k w_k| + fp32 accumulation --
+ *     "3xTF32" on the tcgen05 tensor cores: both operands split in shared memory into a TF32
+ *     high part (low 13 mantissa bits cleared) and the exact remainder, x w accumulated as
+ *     x_hi w_hi + x_lo w_hi + x_hi w_lo (three kind::tf32 MMAs per K step of 8) when
+ *     N in {16, 32, 64, 128, 256} and the split W^T fits in shared memory (K * N <= 128 * 128
+ *     class); otherwise a CUDA-core fp32 FFMA kernel.  K in [4, 256], K % 4 == 0;
+ *     N in [4, 256], N % 4 == 0.
+ *   AGCN_GEMM_TF32: as agcn_gemm_xw.
+ * Same pointer / alignment rules as agcn_gemm_xw; asynchronous on `stream`.
+ */
+typedef enum { AGCN_GEMM_FP32 = 0, AGCN_GEMM_TF32 = 1 } agcn_gemm_precision_t;
+agcn_status_t agcn_gemm_xw_ex(const float* X, int64_t M, int32_t K, const float* Wt, int32_t N, float* Y,
+                              const float* bias, int32_t relu, int32_t precision, agcn_stream_t stream);
+
 /* Device buffers that other processes can map (CUDA IPC): the fused all-gather's peer X
    buffers.  agcn_device_alloc: cudaMalloc'd (exportable) bytes; agcn_ipc_export writes a
    64-byte handle of ptr (a pointer returned by agcn_device_alloc); agcn_ipc_open maps a

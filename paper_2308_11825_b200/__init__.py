@@ -282,9 +282,11 @@ def gather_vals(vals, src, out=None, stream=None):
     return out
 
 
-def gemm_xw(X, Wt, bias=None, relu: bool = False, out=None, stream=None):
-    """agcn_gemm_xw: Y = X . W (+ bias, ReLU) on the tcgen05 tensor cores (TF32).
+def gemm_xw(X, Wt, bias=None, relu: bool = False, out=None, stream=None, precision: str = "tf32"):
+    """agcn_gemm_xw_ex: Y = X . W (+ bias, ReLU) on the tcgen05 tensor cores.
 
+    precision "tf32" (TF32 operands) or "fp32" (3xTF32 split operands, fp32 accuracy; CUDA-core
+    FFMA for shapes whose split W does not fit in shared memory).
     X: [M, K] float32 CUDA; Wt: W transposed, [N, K] float32 CUDA (contiguous)."""
     torch = _torch()
     M, K = X.shape
@@ -294,9 +296,10 @@ def gemm_xw(X, Wt, bias=None, relu: bool = False, out=None, stream=None):
     if out is None:
         out = torch.empty((M, N), dtype=torch.float32, device=X.device)
     b = _dev_ptr(bias, "float32", "bias") if bias is not None else None
-    _check(_lib.lib().agcn_gemm_xw(_dev_ptr(X, "float32", "X"), int(M), int(K), _dev_ptr(Wt, "float32", "Wt"),
-                                   int(N), _dev_ptr(out, "float32", "out"), b, int(bool(relu)),
-                                   _stream_handle(stream)))
+    prec = {"fp32": 0, "tf32": 1}[precision]
+    _check(_lib.lib().agcn_gemm_xw_ex(_dev_ptr(X, "float32", "X"), int(M), int(K), _dev_ptr(Wt, "float32", "Wt"),
+                                      int(N), _dev_ptr(out, "float32", "out"), b, int(bool(relu)), prec,
+                                      _stream_handle(stream)))
     return out
 
 

@@ -102,6 +102,8 @@ def lib():
     L.agcn_gather_vals.restype = c_i32
     L.agcn_gemm_xw.argtypes = [c_vp, c_i64, c_i32, c_vp, c_i32, c_vp, c_vp, c_i32, c_vp]
     L.agcn_gemm_xw.restype = c_i32
+    L.agcn_gemm_xw_ex.argtypes = [c_vp, c_i64, c_i32, c_vp, c_i32, c_vp, c_vp, c_i32, c_i32, c_vp]
+    L.agcn_gemm_xw_ex.restype = c_i32
     L.agcn_device_alloc.argtypes = [c_size, ctypes.POINTER(c_vp)]
     L.agcn_device_alloc.restype = c_i32
     L.agcn_device_free.argtypes = [c_vp]
@@ -129,5 +131,5 @@ EXPORTS = ["agcn_default_opts", "agcn_plan", "agcn_plan_ex", "agcn_spmm", "agcn_
            "agcn_plan_stats", "agcn_plan_copy", "agcn_auto_partition", "agcn_shard_bounds", "agcn_propagate_host",
            "agcn_pipe_create", "agcn_pipe_submit", "agcn_pipe_wait", "agcn_pipe_destroy",
            "agcn_graph_create", "agcn_graph_launch", "agcn_graph_destroy",
-           "agcn_transpose", "agcn_gather_vals", "agcn_gemm_xw", "agcn_device_alloc", "agcn_device_free", "agcn_ipc_export",
+           "agcn_transpose", "agcn_gather_vals", "agcn_gemm_xw", "agcn_gemm_xw_ex", "agcn_device_alloc", "agcn_device_free", "agcn_ipc_export",
            "agcn_ipc_open", "agcn_ipc_close", "agcn_last_status", "agcn_last_error", "agcn_launch_count", "agcn_version"]

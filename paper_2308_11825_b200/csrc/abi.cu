@@ -310,6 +310,17 @@ agcn_status_t agcn_gemm_xw(const float* X, int64_t M, int32_t K, const float* Wt
     return guarded([&] { gemm_xw_tf32(X, M, K, Wt, N, Y, bias, relu, (cudaStream_t)stream); });
 }
 
+agcn_status_t agcn_gemm_xw_ex(const float* X, int64_t M, int32_t K, const float* Wt, int32_t N, float* Y,
+                              const float* bias, int32_t relu, int32_t precision, agcn_stream_t stream) {
+    return guarded([&] {
+        AGCN_CHECK(precision == AGCN_GEMM_FP32 || precision == AGCN_GEMM_TF32, AGCN_ERR_INVALID_ARG, "unknown precision");
+        if (precision == AGCN_GEMM_TF32)
+            gemm_xw_tf32(X, M, K, Wt, N, Y, bias, relu, (cudaStream_t)stream);
+        else
+            gemm_xw_fp32(X, M, K, Wt, N, Y, bias, relu, (cudaStream_t)stream);
+    });
+}
+
 agcn_status_t agcn_device_alloc(size_t bytes, void** ptr) {
     return guarded([&] {
         AGCN_CHECK(ptr != nullptr, AGCN_ERR_INVALID_ARG, "ptr is NULL");

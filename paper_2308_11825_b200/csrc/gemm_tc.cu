@@ -406,6 +406,245 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_gemm_tf32_ws(const __grid_con
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(2 * kAcc));
 }
 
+// ---------------------------------------------------------------- fp32-accurate: 3xTF32
+// X W in fp32 accuracy on the TF32 tensor cores by splitting both operands (the "3xTF32"
+// scheme): x = x_hi + x_lo with x_hi = x with its low 13 mantissa bits cleared (a TF32 value,
+// read exactly by kind::tf32 whether the hardware truncates or rounds) and x_lo = x - x_hi
+// (exact in fp32, |x_lo| < 2^-10 |x|); likewise w.  Then
+//     x w = x_hi w_hi + x_lo w_hi + x_hi w_lo + x_lo w_lo,
+// the last term (< 2^-20 |x w|) dropped, x_lo / w_lo themselves read as TF32 (relative error
+// 2^-10 of a term already 2^-10 small): |y - y_ref| <~ 2^-19 sum_k |x_k w_k| + fp32 accumulation,
+// inside the layer tolerance 1e-5 sum|x w|.  Three tcgen05.mma per K step of 8, all into the
+// same TMEM accumulator, in a fixed order (deterministic).
+//
+// Warp roles (persistent CTA per SM): warp 0 TMA producer (X k-stages of 128 rows x 32 columns
+// into an NSK-slot ring; W^T once), warp 1 MMA issuer, warps 2-5 epilogue (TMEM -> bias/ReLU ->
+// staged coalesced stores, two accumulators), warps 6-9 split each landed X stage in place
+// (hi) plus into a lo ring slot of the same (swizzled) layout, then fence.proxy.async so the
+// tensor core sees the generic-proxy writes.  W^T is split once per CTA the same way.
+constexpr int kX3Threads = 320;
+
+__device__ __forceinline__ void split_tf32(float x, float& hi, float& lo) {
+    hi = __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
+    lo = x - hi;
+}
+
+template <int N, int NSK, int CWT>
+__global__ void __launch_bounds__(kX3Threads, 1) k_gemm_3xtf32(const __grid_constant__ CUtensorMap tmX,
+                                                              const __grid_constant__ CUtensorMap tmW,
+                                                              float* __restrict__ Y, int64_t M, int32_t KT,
+                                                              const float* __restrict__ bias, int32_t relu) {
+    constexpr uint32_t kAcc = N <= 32 ? 32 : N <= 64 ? 64 : N <= 128 ? 128 : 256;
+    constexpr int kStage = kBM * kBK * 4;                      // one X k-stage (16 KB)
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    float* sX = reinterpret_cast<float*>(smem);                                  // [NSK][128][32] (hi in place)
+    float* sXl = reinterpret_cast<float*>(smem + NSK * kStage);                  // [NSK][128][32] lo
+    float* sW = reinterpret_cast<float*>(smem + 2 * NSK * kStage);               // [KT][N][32] hi in place
+    float* sWl = sW + (size_t)KT * N * kBK;                                      // [KT][N][32] lo
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sWl + (size_t)KT * N * kBK);
+    uint64_t* full = bars;                 // [NSK] X stage landed (TMA)
+    uint64_t* split = bars + NSK;          // [NSK] X stage split (4 converter warps)
+    uint64_t* empty = bars + 2 * NSK;      // [NSK] X stage consumed (MMA commit)
+    uint64_t* acc_full = bars + 3 * NSK;   // [2]
+    uint64_t* acc_empty = bars + 3 * NSK + 2;  // [2] (4 epilogue warps)
+    uint64_t* barW = bars + 3 * NSK + 4;   // W^T landed
+    uint64_t* wsplit = bars + 3 * NSK + 5; // W^T split (4 converter warps)
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * NSK + 6);
+    constexpr int CW = N < CWT ? N : CWT, SP = CW + 4;
+    float* staging = reinterpret_cast<float*>(reinterpret_cast<unsigned char*>(bars) + 256);  // after <= 19 barriers
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < NSK; ++i) {
+            mbar_init(full + i, 1);
+            mbar_init(split + i, 4);
+            mbar_init(empty + i, 1);
+        }
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(acc_full + i, 1);
+            mbar_init(acc_empty + i, 4);
+        }
+        mbar_init(barW, 1);
+        mbar_init(wsplit, 4);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "n"(2 * kAcc));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tmem = *tmem_slot;
+    const int64_t ntiles = (M + kBM - 1) / kBM;
+
+    if (warp == 0) {
+        if (lane == 0) {  // ---- TMA producer: W^T once, then every (tile, k-stage) in order
+            mbar_expect_tx(barW, (uint32_t)(KT * N * kBK * 4));
+            for (int k = 0; k < KT; ++k) tma_load_2d(sW + (size_t)k * N * kBK, &tmW, barW, k * kBK, 0);
+            int st = 0;
+            uint32_t ph = 0;
+            for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x)
+                for (int k = 0; k < KT; ++k) {
+                    mbar_wait(empty + st, ph ^ 1);
+                    mbar_expect_tx(full + st, (uint32_t)kStage);
+                    tma_load_2d(sX + (size_t)st * kBM * kBK, &tmX, full + st, k * kBK, (int)(t * kBM));
+                    if (++st == NSK) { st = 0; ph ^= 1; }
+                }
+        }
+    } else if (warp >= 6) {  // ---- converters: split W^T once, then every X stage
+        const int ct = threadIdx.x - 6 * 32;   // 0..127
+        mbar_wait(barW, 0);
+        for (int64_t i = ct; i < (int64_t)KT * N * kBK; i += 128) {
+            float h, l;
+            split_tf32(sW[i], h, l);
+            sW[i] = h;
+            sWl[i] = l;
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) mbar_arrive(wsplit);
+        int st = 0;
+        uint32_t ph = 0;
+        for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x)
+            for (int k = 0; k < KT; ++k) {
+                mbar_wait(full + st, ph);
+                float4* x4 = reinterpret_cast<float4*>(sX + (size_t)st * kBM * kBK);
+                float4* l4 = reinterpret_cast<float4*>(sXl + (size_t)st * kBM * kBK);
+#pragma unroll 4
+                for (int i = ct; i < kBM * kBK / 4; i += 128) {
+                    float4 v = x4[i], h, l;
+                    split_tf32(v.x, h.x, l.x);
+                    split_tf32(v.y, h.y, l.y);
+                    split_tf32(v.z, h.z, l.z);
+                    split_tf32(v.w, h.w, l.w);
+                    x4[i] = h;
+                    l4[i] = l;
+                }
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                __syncwarp();
+                if (lane == 0) mbar_arrive(split + st);
+                if (++st == NSK) { st = 0; ph ^= 1; }
+            }
+    } else if (warp == 1) {
+        if (lane == 0) {  // ---- MMA issuer: x_hi w_hi + x_lo w_hi + x_hi w_lo per K step
+            mbar_wait(wsplit, 0);
+            const uint32_t idesc = idesc_tf32<N>();
+            int st = 0;
+            uint32_t ph = 0, aph[2] = {0, 0};
+            int acc = 0;
+            for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+                mbar_wait(acc_empty + acc, aph[acc] ^ 1);
+                for (int k = 0; k < KT; ++k) {
+                    mbar_wait(split + st, ph);
+                    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                    const uint32_t xh = smem_u32(sX + (size_t)st * kBM * kBK), xl = smem_u32(sXl + (size_t)st * kBM * kBK);
+                    const uint32_t wh = smem_u32(sW + (size_t)k * N * kBK), wl = smem_u32(sWl + (size_t)k * N * kBK);
+#pragma unroll
+                    for (int kk = 0; kk < kBK / 8; ++kk) {
+                        const uint32_t d = tmem + acc * kAcc;
+                        umma_tf32(d, umma_desc_sw128(xh + kk * 32), umma_desc_sw128(wh + kk * 32), idesc, (k | kk) != 0);
+                        umma_tf32(d, umma_desc_sw128(xl + kk * 32), umma_desc_sw128(wh + kk * 32), idesc, 1);
+                        umma_tf32(d, umma_desc_sw128(xh + kk * 32), umma_desc_sw128(wl + kk * 32), idesc, 1);
+                    }
+                    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                                     smem_u32(empty + st))
+                                 : "memory");
+                    if (++st == NSK) { st = 0; ph ^= 1; }
+                }
+                asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                                 smem_u32(acc_full + acc))
+                             : "memory");
+                aph[acc] ^= 1;
+                acc ^= 1;
+            }
+        }
+    } else {  // ---- epilogue: warps 2..5 -> TMEM lane quadrant warp % 4
+        const int quad = warp & 3;
+        uint32_t aph[2] = {0, 0};
+        int acc = 0;
+        for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+            mbar_wait(acc_full + acc, aph[acc]);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            const int64_t row0 = t * kBM + quad * 32;
+            float* stg = staging + quad * 32 * SP;
+#pragma unroll 1
+            for (int cb = 0; cb < N; cb += CW) {
+#pragma unroll 1
+                for (int c0 = 0; c0 < CW; c0 += 16) {
+                    float v[16];
+                    tmem_ld16(tmem + acc * kAcc + ((uint32_t)(quad * 32) << 16) + (uint32_t)(cb + c0), v);
+#pragma unroll
+                    for (int i = 0; i < 16; i += 4) {
+                        float4 o = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+                        if (bias) {
+                            o.x += __ldg(bias + cb + c0 + i);
+                            o.y += __ldg(bias + cb + c0 + i + 1);
+                            o.z += __ldg(bias + cb + c0 + i + 2);
+                            o.w += __ldg(bias + cb + c0 + i + 3);
+                        }
+                        if (relu) {
+                            o.x = fmaxf(o.x, 0.f); o.y = fmaxf(o.y, 0.f); o.z = fmaxf(o.z, 0.f); o.w = fmaxf(o.w, 0.f);
+                        }
+                        *reinterpret_cast<float4*>(stg + lane * SP + c0 + i) = o;
+                    }
+                }
+                __syncwarp();
+                constexpr int nv = CW / 4;
+#pragma unroll 4
+                for (int e = lane; e < 32 * nv; e += 32) {
+                    const int r = e / nv, c = e - r * nv;
+                    if (row0 + r < M)
+                        __stcs(reinterpret_cast<float4*>(Y + (row0 + r) * N + cb) + c,
+                               *reinterpret_cast<const float4*>(stg + r * SP + 4 * c));
+                }
+                __syncwarp();
+            }
+            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) mbar_arrive(acc_empty + acc);
+            aph[acc] ^= 1;
+            acc ^= 1;
+        }
+    }
+    __syncthreads();
+    if (warp == 1)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(2 * kAcc));
+}
+
+// ---------------------------------------------------------------- fp32 on the CUDA cores
+// The fallback for shapes whose split W^T does not fit in shared memory next to the X ring
+// (K * N > 128 * 128): a plain fp32 FFMA kernel, one thread per (row, 4 consecutive columns),
+// K-loop in order with fmaf (the arithmetic of a textbook fp32 GEMM, deterministic).  W^T rows
+// are read through the read-only cache; X rows are reused from L1 by the N / 4 threads of a row.
+__global__ void k_gemm_fp32_cc(const float* __restrict__ X, int64_t M, int32_t K, const float* __restrict__ Wt,
+                               int32_t N, float* __restrict__ Y, const float* __restrict__ bias, int32_t relu) {
+    const int32_t nq = N / 4;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < M * nq; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t row = i / nq;
+        const int32_t c = (int32_t)(i - row * nq) * 4;
+        const float* x = X + row * K;
+        float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+        for (int32_t k = 0; k < K; ++k) {
+            const float xv = __ldg(x + k);
+            a0 = fmaf(xv, __ldg(Wt + (int64_t)c * K + k), a0);
+            a1 = fmaf(xv, __ldg(Wt + (int64_t)(c + 1) * K + k), a1);
+            a2 = fmaf(xv, __ldg(Wt + (int64_t)(c + 2) * K + k), a2);
+            a3 = fmaf(xv, __ldg(Wt + (int64_t)(c + 3) * K + k), a3);
+        }
+        float4 o = make_float4(a0, a1, a2, a3);
+        if (bias) {
+            o.x += __ldg(bias + c); o.y += __ldg(bias + c + 1); o.z += __ldg(bias + c + 2); o.w += __ldg(bias + c + 3);
+        }
+        if (relu) {
+            o.x = fmaxf(o.x, 0.f); o.y = fmaxf(o.y, 0.f); o.z = fmaxf(o.z, 0.f); o.w = fmaxf(o.w, 0.f);
+        }
+        __stcs(reinterpret_cast<float4*>(Y + row * N + c), o);
+    }
+}
+
 // ---------------------------------------------------------------- host: tensor maps
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
@@ -455,18 +694,12 @@ bool try_launch_ws(const CUtensorMap& mx, const CUtensorMap& mw, float* Y, int64
     return true;
 }
 
-int gemm_variant() {  // A/B switch: 0 pipelined (default when it fits), 1 one tile per CTA
-    static const int v = [] { const char* e = getenv("AGCN_GEMM_VARIANT"); return e ? atoi(e) : 0; }();
-    return v;
-}
-
 template <int N>
 void launch_gemm(const CUtensorMap& mx, const CUtensorMap& mw, float* Y, int64_t M, int32_t KT, const float* bias,
                  int32_t relu, cudaStream_t s) {
-    if (gemm_variant() == 0 && (try_launch_ws<N, 4>(mx, mw, Y, M, KT, bias, relu, s) ||
-                                try_launch_ws<N, 3>(mx, mw, Y, M, KT, bias, relu, s) ||
-                                try_launch_ws<N, 2>(mx, mw, Y, M, KT, bias, relu, s) ||
-                                try_launch_ws<N, 1, 32>(mx, mw, Y, M, KT, bias, relu, s)))
+    // pipelined warp-specialized kernel when it fits, else one tile per CTA
+    if (try_launch_ws<N, 4>(mx, mw, Y, M, KT, bias, relu, s) || try_launch_ws<N, 3>(mx, mw, Y, M, KT, bias, relu, s) ||
+        try_launch_ws<N, 2>(mx, mw, Y, M, KT, bias, relu, s) || try_launch_ws<N, 1, 32>(mx, mw, Y, M, KT, bias, relu, s))
         return;
     const size_t smem = 1024 + (size_t)KT * (kBM + N) * kBK * 4 + 64;
     AGCN_CHECK(smem <= 227 * 1024, AGCN_ERR_UNSUPPORTED, "F_in x F_out too large for the tcgen05 GEMM");
@@ -482,7 +715,60 @@ void launch_gemm(const CUtensorMap& mx, const CUtensorMap& mw, float* Y, int64_t
     post_launch();
 }
 
+template <int N, int NSK, int CWT>
+bool try_launch_3x(const CUtensorMap& mx, const CUtensorMap& mw, float* Y, int64_t M, int32_t KT, const float* bias,
+                   int32_t relu, cudaStream_t s) {
+    constexpr int CW = N < CWT ? N : CWT;
+    const size_t smem = 1024 + (size_t)2 * NSK * kBM * kBK * 4 + (size_t)2 * KT * N * kBK * 4 + 256 +
+                        (size_t)4 * 32 * (CW + 4) * 4;
+    if (smem > 227 * 1024) return false;
+    auto kern = k_gemm_3xtf32<N, NSK, CWT>;
+    AGCN_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    const int64_t ntiles = (M + kBM - 1) / kBM;
+    const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(ntiles, (int64_t)num_sms()));
+    kern<<<(unsigned)grid, kX3Threads, smem, s>>>(mx, mw, Y, M, KT, bias, relu);
+    post_launch();
+    return true;
+}
+
+template <int N>
+bool launch_3x(const CUtensorMap& mx, const CUtensorMap& mw, float* Y, int64_t M, int32_t KT, const float* bias,
+               int32_t relu, cudaStream_t s) {
+    return try_launch_3x<N, 4, 64>(mx, mw, Y, M, KT, bias, relu, s) ||
+           try_launch_3x<N, 3, 32>(mx, mw, Y, M, KT, bias, relu, s) ||
+           try_launch_3x<N, 2, 32>(mx, mw, Y, M, KT, bias, relu, s);
+}
+
 }  // namespace
+
+void gemm_xw_fp32(const float* X, int64_t M, int32_t K, const float* Wt, int32_t N, float* Y, const float* bias,
+                  int32_t relu, cudaStream_t s) {
+    AGCN_CHECK(M >= 0 && K >= 1 && K <= 256 && (K % 4) == 0, AGCN_ERR_UNSUPPORTED, "K must be in [4, 256], K % 4 == 0");
+    AGCN_CHECK(N >= 4 && N <= 256 && N % 4 == 0, AGCN_ERR_UNSUPPORTED, "N must be in [4, 256], N % 4 == 0");
+    AGCN_CHECK(X && Wt && Y, AGCN_ERR_INVALID_ARG, "NULL pointer");
+    AGCN_CHECK(((reinterpret_cast<uintptr_t>(X) | reinterpret_cast<uintptr_t>(Wt) | reinterpret_cast<uintptr_t>(Y)) & 15u) == 0,
+               AGCN_ERR_INVALID_ARG, "X, W^T and Y must be 16-byte aligned");
+    if (M == 0) return;
+    const int32_t KT = (K + kBK - 1) / kBK;
+    bool done = false;
+    if (N == 16 || N == 32 || N == 64 || N == 128 || N == 256) {
+        const CUtensorMap mx = make_map(X, M, K, kBM);
+        const CUtensorMap mw = make_map(Wt, N, K, (uint32_t)N);
+        switch (N) {
+            case 16: done = launch_3x<16>(mx, mw, Y, M, KT, bias, relu, s); break;
+            case 32: done = launch_3x<32>(mx, mw, Y, M, KT, bias, relu, s); break;
+            case 64: done = launch_3x<64>(mx, mw, Y, M, KT, bias, relu, s); break;
+            case 128: done = launch_3x<128>(mx, mw, Y, M, KT, bias, relu, s); break;
+            default: done = launch_3x<256>(mx, mw, Y, M, KT, bias, relu, s); break;
+        }
+    }
+    if (!done) {
+        const int64_t work = M * (N / 4);
+        const unsigned grid = (unsigned)std::min<int64_t>((work + 255) / 256, (int64_t)num_sms() * 16);
+        k_gemm_fp32_cc<<<grid, 256, 0, s>>>(X, M, K, Wt, N, Y, bias, relu);
+        post_launch();
+    }
+}
 
 void gemm_xw_tf32(const float* X, int64_t M, int32_t K, const float* Wt, int32_t N, float* Y, const float* bias,
                   int32_t relu, cudaStream_t s) {

@@ -243,6 +243,9 @@ void radix_sort_pairs(int32_t*& ka, int32_t*& va, int32_t*& kb, int32_t*& vb, in
 // gemm_tc.cu: Y = X W on tcgen05 (kind::tf32); Wt = W^T [N x K] row-major
 void gemm_xw_tf32(const float* X, int64_t M, int32_t K, const float* Wt, int32_t N, float* Y, const float* bias,
                   int32_t relu, cudaStream_t s);
+// fp32 accuracy: 3xTF32 split operands on tcgen05 (W^T split fits in shared memory), else CUDA-core FFMA
+void gemm_xw_fp32(const float* X, int64_t M, int32_t K, const float* Wt, int32_t N, float* Y, const float* bias,
+                  int32_t relu, cudaStream_t s);
 // transpose.cu
 void transpose_csr(const int32_t* rowptr, const int32_t* colidx, int64_t n, int64_t n_cols, int64_t nnz,
                    int32_t* rowptr_t, int32_t* colidx_t, int32_t* src, cudaStream_t s);

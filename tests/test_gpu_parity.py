@@ -580,8 +580,8 @@ def test_transpose_rectangular_shard_and_empty():
 
 # ---------------------------------------------------------------- GCN layer (8(f3))
 @pytest.mark.parametrize("fin,fout,prec", [(64, 16, "fp32"), (16, 64, "fp32"), (128, 128, "fp32"),
-                                           (32, 8, "fp32"), (64, 16, "tf32"), (16, 64, "tf32"),
-                                           (128, 128, "tf32")])
+                                           (32, 8, "fp32"), (256, 64, "fp32"), (64, 256, "fp32"),
+                                           (64, 16, "tf32"), (16, 64, "tf32"), (128, 128, "tf32")])
 def test_gcn_layer(fin, fout, prec):
     """fp32: the north-star tolerance (1e-5 relative); tf32 (tcgen05 X.W): 2^-9 relative."""
     from paper_2308_11825_b200.layer import GCNLayer
@@ -616,6 +616,32 @@ def test_gemm_xw_tcgen05_tf32(M, K, N, epi):
     err = np.abs(Y - ref)
     assert np.all(err <= 2.0 ** -9 * mag + 1e-6), float((err / (2.0 ** -9 * mag + 1e-6)).max())
     assert err.mean() > 1e-7 or M * N < 100            # it really is TF32 (not an fp32 fallback)
+
+
+@pytest.mark.parametrize("M,K,N", [(1, 4, 16), (127, 32, 16), (300, 64, 64), (1000, 100, 32),
+                                   (4097, 128, 128), (513, 256, 64), (257, 64, 256), (70000, 64, 64),
+                                   (100, 16, 8), (300, 256, 256), (33, 12, 20)])
+@pytest.mark.parametrize("epi", [False, True])
+def test_gemm_xw_fp32(M, K, N, epi):
+    """agcn_gemm_xw_ex(AGCN_GEMM_FP32): 3xTF32 on tcgen05 (or the CUDA-core kernel where the split
+    W does not fit) vs the fp64 product within the layer tolerance 1e-5 sum|x w| + 1e-7, and at
+    least 50x more accurate than the TF32 path on the same data (the split is really applied)."""
+    rng = np.random.default_rng(M + K + N + 7)
+    X = rng.uniform(-1, 1, (M, K)).astype(np.float32)
+    W = rng.uniform(-1, 1, (K, N)).astype(np.float32)
+    b = rng.uniform(-1, 1, N).astype(np.float32) if epi else None
+    Wt = cu(np.ascontiguousarray(W.T))
+    Y = A.gemm_xw(cu(X), Wt, bias=cu(b) if epi else None, relu=epi, precision="fp32").cpu().numpy()
+    ref = X.astype(np.float64) @ W.astype(np.float64)
+    mag = np.abs(X).astype(np.float64) @ np.abs(W).astype(np.float64)
+    if epi:
+        ref = np.maximum(ref + b, 0.0)
+        mag = mag + np.abs(b)
+    err = np.abs(Y - ref)
+    assert np.all(err <= 1e-5 * mag + 1e-7), float((err / (1e-5 * mag + 1e-7)).max())
+    if N in (16, 32, 64, 128, 256) and M * N >= 100 and K * N <= 128 * 128:   # tf32 and 3xTF32 both run
+        Yt = A.gemm_xw(cu(X), Wt, bias=cu(b) if epi else None, relu=epi, precision="tf32").cpu().numpy()
+        assert np.abs(Yt - ref).mean() > 50 * err.mean()
 
 
 def test_pipeline_matches_propagate_host():

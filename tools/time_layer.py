@@ -1,5 +1,6 @@
-"""Time one GCN layer (paper_2308_11825_b200.layer.GCNLayer: cuBLAS X.W + agcn SpMM with the
-fused bias/ReLU epilogue) on a config: python tools/time_layer.py c5 64 64"""
+"""Time one GCN layer (paper_2308_11825_b200.layer.GCNLayer: tcgen05 X.W + agcn SpMM with the
+fused bias/ReLU epilogue) on a config, and its X.W alone (libagcn at the layer's precision, and
+cuBLAS fp32 for comparison): python tools/time_layer.py c5 64 64 [fp32|tf32]"""
 import json
 import os
 import sys
@@ -37,9 +38,17 @@ torch.backends.cuda.matmul.allow_tf32 = False
 Wt = W.t().contiguous()
 e0.record()
 for _ in range(10):
-    T = A.gemm_xw(X, Wt) if prec == "tf32" else torch.mm(X, W)
+    T = A.gemm_xw(X, Wt, precision=prec)
 e1.record()
 torch.cuda.synchronize()
 gemm = e0.elapsed_time(e1) / 10
+e0.record()
+for _ in range(10):
+    T = torch.mm(X, W)
+e1.record()
+torch.cuda.synchronize()
+cub = e0.elapsed_time(e1) / 10
+gb = 4.0 * w.n * (fin + fout) / 1e9
 print(json.dumps({"config": name, "fin": fin, "fout": fout, "precision": prec, "order": layer.order, "layer_ms": ms,
-                  "gemm_XW_ms": gemm, "flops": 2 * w.nnz * min(fin, fout) + 2 * w.n * fin * fout}))
+                  "gemm_XW_ms": gemm, "gemm_XW_TBps": gb / gemm, "cublas_fp32_XW_ms": cub,
+                  "flops": 2 * w.nnz * min(fin, fout) + 2 * w.n * fin * fout}))
