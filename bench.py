@@ -70,6 +70,9 @@ def parse():
     ap.add_argument("--fused-allgather", action="store_true",
                     help="N>1: the SpMM epilogue stores rows into every rank's X (CUDA IPC / NVLink) "
                          "instead of an all-gather collective (SURVEY 8(f1))")
+    ap.add_argument("--overlap-chunks", type=int, default=1,
+                    help="K > 1: column-chunked propagation, the all-gather of chunk k overlapping the "
+                         "SpMM of chunk k+1 (SURVEY 8(f1)); 1: one SpMM + one all-gather per layer")
     ap.add_argument("--dist-backend", choices=["nccl", "gloo"], default="nccl",
                     help="gloo: test mode, every rank on cuda:0, all-gather staged through the host")
     ap.add_argument("--profile", action="store_true",
@@ -495,8 +498,9 @@ def main():
 
     import agcn_inputs as gen
     import paper_2308_11825_b200 as A
-    from paper_2308_11825_b200.dist import (PeerBuffers, ShardLayout, make_all_gather, propagate,
-                                            propagate_fused)
+    from paper_2308_11825_b200.dist import (PeerBuffers, ShardLayout, chunk_widths, join_columns,
+                                            make_all_gather, make_all_gather_async, propagate,
+                                            propagate_chunked, propagate_fused, split_columns)
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -553,6 +557,14 @@ def main():
 
     gather = make_all_gather(args.dist_backend) if P > 1 else None
     fused = args.fused_allgather and P > 1
+    K = max(1, args.overlap_chunks)
+    if K > 1 and fused:
+        raise SystemExit("--overlap-chunks and --fused-allgather are alternatives")
+    if K > 1:   # chunk-major layout: K contiguous [P*S, w_k] buffers per X / Y
+        widths = chunk_widths(F, K)
+        X0c = split_columns(X0, widths)
+        bufs_c = [[torch.empty_like(c) for _ in range(min(layers, 2))] for c in X0c]
+        gather_async = make_all_gather_async(args.dist_backend) if P > 1 else None
     peers = PeerBuffers(lay, F) if fused else None
 
     def fused_barrier():  # the peers' stores of this layer are complete everywhere
@@ -597,6 +609,8 @@ def main():
                 if record:
                     rec["spmm"].append((s0, s1))
             out = propagate_fused(lay, spmm_f, X0, peers, layers, fused_barrier)
+        elif K > 1:
+            out = join_columns(propagate_chunked(lay, spmm, X0c, bufs_c, layers, gather_async))
         else:
             out = propagate(lay, spmm, X0, bufs, layers, all_gather if P > 1 else None)
         return plan, out  # plans stay alive until after the timed region (closed below)
@@ -633,7 +647,7 @@ def main():
     spmm_ms = [a.elapsed_time(b) for a, b in rec["spmm"]]
     plan_ms = [a.elapsed_time(b) for a, b in rec["plan"]]
     ag_ms = [a.elapsed_time(b) for a, b in rec["ag"]]
-    spmm_avg = sum(spmm_ms) / max(1, len(spmm_ms))
+    spmm_avg = sum(spmm_ms) / max(1, len(spmm_ms)) * K      # per layer (K chunk SpMMs per layer)
     vec = torch.tensor([ms_local, spmm_avg, sum(plan_ms) / max(1, len(plan_ms)),
                         sum(ag_ms) / max(1, len(ag_ms)) if ag_ms else 0.0], device=dev)
     if P > 1:
@@ -667,7 +681,10 @@ def main():
                        "layers": layers, "partition": args.partition, "kernel": args.kernel,
                        "aggregation": args.aggregation, "gin_eps": args.gin_eps, "bias_relu": args.bias_relu,
                        "allgather": ("fused (SpMM epilogue peer stores)" if fused else
-                                     f"{args.dist_backend} all_gather_into_tensor") if P > 1 else None, "parallelism": f"row-shard{P}",
+                                     f"{args.dist_backend} all_gather_into_tensor" +
+                                     (f", {K} column chunks overlapped with the SpMM" if K > 1 else ""))
+                                    if P > 1 else None, "parallelism": f"row-shard{P}",
+                       "overlap_chunks": K,
                        "max_block_warps": st_plan["max_block_warps"], "max_warp_nzs": st_plan["max_warp_nzs"],
                        "partition_params": "auto (agcn_auto_partition)" if args.mbw == 0 and args.mwn == 0
                                            else "given",
@@ -711,9 +728,12 @@ def main():
             chk = []
             with A.Plan(rp_local, ci_d, **plan_kw) as pc:
                 Xin = X0
+                kw = dict(kernel=args.kernel, l2_hint=args.l2_hint, hot_mb=args.hot_mb, chunk_shape=args.chunk_shape)
                 for l in range(layers):
-                    Yl = pc.spmm(va_d, Xin, kernel=args.kernel, l2_hint=args.l2_hint, hot_mb=args.hot_mb,
-                                 chunk_shape=args.chunk_shape)
+                    if K > 1:   # the same column chunks as the timed run
+                        Yl = join_columns([pc.spmm(va_d, c, **kw) for c in split_columns(Xin, widths)])
+                    else:
+                        Yl = pc.spmm(va_d, Xin, **kw)
                     r = oracle.spmm_check(w.rowptr, w.colidx, w.vals, Xin.cpu().numpy(), Yl[rows_d].cpu().numpy(),
                                           rows=rows)
                     chk.append({"layer": l + 1, "rows": r["rows"], "nfail": r["nfail"], "max_ratio": r["max_ratio"]})

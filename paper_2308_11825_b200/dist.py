@@ -96,6 +96,94 @@ def propagate(layout: ShardLayout, spmm, X0, bufs, layers: int, all_gather=None)
     return cur
 
 
+def chunk_widths(F: int, K: int) -> list:
+    """Column chunks of the overlapped propagation: K widths summing to F, multiples of 8 where
+    possible (the WIDE kernel's 32-byte lanes), the earlier chunks never narrower."""
+    if K < 1 or K > F:
+        raise ValueError(f"need 1 <= K <= F, got K={K}, F={F}")
+    q = F // K
+    base = (q // 8) * 8 if q >= 8 else q
+    widths = [base] * K
+    rest = F - base * K
+    i = 0
+    while rest > 0:                        # hand out the remainder in steps of 8 (or 1)
+        step = 8 if rest >= 8 and base >= 8 else 1
+        widths[i % K] += step
+        rest -= step
+        i += 1
+    return widths
+
+
+def split_columns(X, widths):
+    """[rows, F] -> K contiguous [rows, w_k] column blocks (the chunk-major layout)."""
+    out, c = [], 0
+    for wk in widths:
+        out.append(X[:, c:c + wk].contiguous())
+        c += wk
+    return out
+
+
+def join_columns(chunks):
+    import torch
+    return torch.cat(chunks, 1)
+
+
+def propagate_chunked(layout: ShardLayout, spmm, X0_chunks, bufs_chunks, layers: int, all_gather_async=None):
+    """Column-chunked propagation with the all-gather of chunk k overlapping the SpMM of chunk
+    k + 1.  The SpMM is column-separable -- (A X)[:, c] = A X[:, c] -- so every
+    layer runs as K narrower SpMMs over contiguous chunk buffers ([P*S, w_k] each, the chunk-
+    major layout), and a chunk's all-gather only has to finish before the NEXT layer's SpMM of
+    the same chunk reads it:
+
+        layer l:  SpMM_0  SpMM_1  SpMM_2 ...            (compute stream)
+                        AG_0    AG_1    AG_2 ...        (communicator's stream, async)
+        layer l+1: wait(AG_0) SpMM_0, wait(AG_1) SpMM_1, ...
+
+    spmm(Xin_chunk, out_rows_chunk) as in ``propagate``; all_gather_async(full, slot) starts an
+    in-place all-gather and returns a handle with .wait() (device-side ordering of the current
+    stream after the collective, e.g. torch.distributed async work); None for one rank.
+    bufs_chunks: per chunk a list of >= 1 padded buffers (not X0's).  Returns the list of the
+    last layer's chunk buffers; every pending all-gather has been waited for."""
+    K = len(X0_chunks)
+    cur = list(X0_chunks)
+    pending = [None] * K
+    for layer in range(layers):
+        nxt = [bufs_chunks[k][layer % len(bufs_chunks[k])] for k in range(K)]
+        for k in range(K):
+            if pending[k] is not None:      # this chunk's input of the previous layer is complete
+                pending[k].wait()
+                pending[k] = None
+            spmm(cur[k], layout.own_rows(nxt[k]))
+            if all_gather_async is not None and layout.P > 1:
+                pending[k] = all_gather_async(nxt[k], layout.slot(nxt[k]))
+        cur = nxt
+    for k in range(K):
+        if pending[k] is not None:
+            pending[k].wait()
+    return cur
+
+
+def make_all_gather_async(backend: str):
+    """all_gather_async(full, slot) -> handle with .wait(): nccl: torch.distributed async work
+    (runs on the communicator's stream; .wait() orders the current stream after it, no host
+    block); gloo (test mode): the host-staged all-gather, done before returning."""
+    import torch.distributed as dist
+
+    if backend == "nccl":
+        return lambda full, slot: dist.all_gather_into_tensor(full, slot, async_op=True)
+    sync = make_all_gather("gloo")
+
+    class _Done:
+        def wait(self):
+            pass
+
+    def ag(full, slot):
+        sync(full, slot)
+        return _Done()
+
+    return ag
+
+
 def make_all_gather(backend: str):
     """In-place all-gather of the S-row slots of a padded [P*S, F] buffer.
 

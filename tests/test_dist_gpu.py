@@ -65,7 +65,7 @@ def _worker(rank, world, port, F, q, fused=False):
             plan.spmm(va_d, Xin, out=out_rows)
             layers_out.append(Xin)
 
-        if fused:   # the SpMM epilogue stores every row into all ranks' buffers (CUDA IPC)
+        if fused is True:   # the SpMM epilogue stores every row into all ranks' buffers (CUDA IPC)
             from paper_2308_11825_b200.dist import PeerBuffers, propagate_fused
             peers = PeerBuffers(lay, F)
 
@@ -78,6 +78,21 @@ def _worker(rank, world, port, F, q, fused=False):
                 dist.barrier()
 
             out = propagate_fused(lay, spmm_f, X0, peers, 2, barrier)
+        elif fused == "chunks":   # column chunks, all-gather of chunk k overlapping SpMM k+1
+            from paper_2308_11825_b200.dist import (chunk_widths, join_columns, make_all_gather_async,
+                                                    propagate_chunked, split_columns)
+            widths = chunk_widths(F, 3)
+            X0c = split_columns(X0, widths)
+            bufs_c = [[torch.empty_like(c) for _ in range(2)] for c in X0c]
+            seen = []
+
+            def spmm_c(Xin, out_rows):
+                plan.spmm(va_d, Xin, out=out_rows)
+                seen.append(Xin)
+
+            outc = propagate_chunked(lay, spmm_c, X0c, bufs_c, 2, make_all_gather_async("gloo"))
+            out = join_columns(outc)
+            layers_out = [join_columns(seen[:3]), join_columns(seen[3:6])]
         else:
             out = propagate(lay, spmm, X0, bufs, 2, make_all_gather("gloo"))
         torch.cuda.synchronize()
@@ -88,7 +103,7 @@ def _worker(rank, world, port, F, q, fused=False):
             r2 = oracle.spmm_check(w.rowptr, w.colidx, w.vals, Y1, Y2)
             q.put(("ok", r1["nfail"], r2["nfail"], r1["max_ratio"], r2["max_ratio"]))
         dist.barrier()
-        if fused:
+        if fused is True:
             peers.close()
         plan.close()
     except Exception as e:  # pragma: no cover
@@ -98,10 +113,13 @@ def _worker(rank, world, port, F, q, fused=False):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,F,fused", [(2, 64, False), (3, 16, False), (2, 64, True), (3, 128, True)])
+@pytest.mark.parametrize("world,F,fused", [(2, 64, False), (3, 16, False), (2, 64, True), (3, 128, True),
+                                           (2, 64, "chunks"), (3, 40, "chunks")])
 def test_sharded_propagation_on_gpu(world, F, fused):
     """fused=True: the fused all-gather -- peer stores from the SpMM epilogue
-    into IPC-mapped buffers of every rank instead of a collective."""
+    into IPC-mapped buffers of every rank instead of a collective.  fused="chunks": the
+    column-chunked propagation (3 chunks; the all-gather of chunk k overlaps the SpMM of chunk
+    k+1), every layer checked against the oracle."""
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
@@ -115,18 +133,19 @@ def test_sharded_propagation_on_gpu(world, F, fused):
     assert n1 == 0 and n2 == 0, (m1, m2)
 
 
-@pytest.mark.parametrize("fused", [False, True])
+@pytest.mark.parametrize("fused", [False, True, "chunks"])
 def test_bench_multi_rank_mode(fused):
     """bench.py under torchrun, 2 ranks (gloo test mode on one GPU): one JSON line from rank 0."""
     port = _free_port()
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
            "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.join(ROOT, "bench.py"),
            "--gpus", "2", "--steps", "2", "--warmup", "3", "--config", "c3", "--dist-backend", "gloo",
-           "--e2e-steps", "1"] + (["--fused-allgather"] if fused else [])
+           "--e2e-steps", "1"] + (["--fused-allgather"] if fused is True else []) + \
+          (["--overlap-chunks", "2"] if fused == "chunks" else [])
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT)
     assert r.returncode == 0, r.stderr[-3000:]
     lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
     assert len(lines) == 1, r.stdout[-2000:]
     d = json.loads(lines[0])
     assert d["n_gpus"] == 2 and d["value"] > 0 and d["gpu_launches"] > 0
-    assert d["allgather_ms"] > 0 and d["e2e"]["value"] > 0
+    assert (d["allgather_ms"] > 0 or fused == "chunks") and d["e2e"]["value"] > 0
