@@ -247,8 +247,10 @@ __device__ __forceinline__ int32_t encode_col(int32_t c, int64_t n_cols, const C
 __global__ void k_sorted_cols(const int4* __restrict__ desc, int64_t nblocks, int32_t db,
                               const int32_t* __restrict__ srp, const int32_t* __restrict__ rso,
                               const int32_t* __restrict__ cols, int64_t n_cols, ColMap cm,
-                              const uint2* __restrict__ hot, int32_t* __restrict__ out) {
+                              const uint2* __restrict__ hot, int32_t* __restrict__ out,
+                              PlanFlags* __restrict__ flags) {
     const int lane = threadIdx.x & 31;
+    int32_t bad = 0;  // colidx validation fused into the copy (flags != NULL)
     const int64_t W = (int64_t)gridDim.x * (blockDim.x / 32);
     for (int64_t b = (int64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5); b < nblocks; b += W) {
         const int4 m = __ldg(desc + b);
@@ -275,10 +277,14 @@ __global__ void k_sorted_cols(const int4* __restrict__ desc, int64_t nblocks, in
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
                 const int32_t e = e0 + k * 32 + lane;
-                if (e < total) __stcs(out + (int64_t)m.y + e, encode_col(c[k], n_cols, cm, hot));
+                if (e < total) {
+                    bad |= (c[k] < 0) | ((int64_t)c[k] >= n_cols);
+                    __stcs(out + (int64_t)m.y + e, encode_col(c[k], n_cols, cm, hot));
+                }
             }
         }
     }
+    if (flags && __any_sync(0xffffffffu, bad) && lane == 0) flags->bad_colidx = 1;
 }
 
 // hot vertices: the H highest-degree ones (sorted positions n - H .. n - 1) -> column bitmap
@@ -504,8 +510,10 @@ int64_t hot_rows_for(const agcn_plan_s* p, int64_t req) {
     return std::max<int64_t>(0, std::min(H, live));
 }
 
-// BLOCK plan, after the descriptors: the degree-sorted colidx (P:295 (3)) with the hot encoding.
-void build_sorted_cols(agcn_plan_s* p, const int32_t* colidx, const agcn_opts_t& o, cudaStream_t s) {
+// BLOCK plan, after the descriptors: the degree-sorted colidx (P:295 (3)) with the hot encoding;
+// d_flags != NULL: validate the column range on the way (read back by the caller).
+void build_sorted_cols(agcn_plan_s* p, const int32_t* colidx, const agcn_opts_t& o, cudaStream_t s,
+                       PlanFlags* d_flags = nullptr) {
     p->scols = dalloc<int32_t>(p->nnz, s);
     p->device_bytes += sizeof(int32_t) * (size_t)p->nnz;
     p->n_hot = hot_rows_for(p, o.hot_rows);
@@ -529,49 +537,9 @@ void build_sorted_cols(agcn_plan_s* p, const int32_t* colidx, const agcn_opts_t&
     if (p->nnz == 0 || p->nblocks == 0) return;
     const unsigned g = (unsigned)std::min<int64_t>(blocks_for(p->nblocks, kWarps), 148 * 8);
     k_sorted_cols<<<g, kThreads, 0, s>>>(p->desc, p->nblocks, p->deg_bound, p->sorted_rowptr, p->row_src_off,
-                                         colidx + p->rp_base, p->n_cols, p->cmap, hot, p->scols);
+                                         colidx + p->rp_base, p->n_cols, p->cmap, hot, p->scols, d_flags);
     post_launch();
 }
-
-// A second stream per device for plan work that can overlap the main sequence (validation).
-cudaStream_t aux_stream(int dev) {
-    static std::mutex mu;
-    static cudaStream_t streams[64] = {};
-    std::lock_guard<std::mutex> lock(mu);
-    if (dev < 0 || dev >= 64) return nullptr;
-    if (!streams[dev]) AGCN_CUDA(cudaStreamCreateWithFlags(&streams[dev], cudaStreamNonBlocking));
-    return streams[dev];
-}
-
-// Fork / join of one overlap region.  If the region is left early (an error), the main
-// stream still waits for the side work before anything declared earlier (scratch freed on
-// the main stream) is released.
-struct Overlap {
-    cudaStream_t main, side;
-    cudaEvent_t fork = nullptr, join = nullptr;
-    bool joined = false;
-    Overlap(cudaStream_t m, cudaStream_t sd) : main(m), side(sd) {
-        if (!side) return;
-        AGCN_CUDA(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
-        AGCN_CUDA(cudaEventCreateWithFlags(&join, cudaEventDisableTiming));
-        AGCN_CUDA(cudaEventRecord(fork, main));
-        AGCN_CUDA(cudaStreamWaitEvent(side, fork, 0));
-    }
-    void finish() {  // after the side work is enqueued: main waits for it
-        if (!side || joined) return;
-        AGCN_CUDA(cudaEventRecord(join, side));
-        AGCN_CUDA(cudaStreamWaitEvent(main, join, 0));
-        joined = true;
-    }
-    ~Overlap() {
-        if (side && !joined) {
-            cudaEventRecord(join, side);
-            cudaStreamWaitEvent(main, join, 0);
-        }
-        if (fork) cudaEventDestroy(fork);
-        if (join) cudaEventDestroy(join);
-    }
-};
 
 }  // namespace
 
@@ -956,17 +924,14 @@ void build_block_plan(agcn_plan_s* p, const int32_t* rowptr, const int32_t* coli
     int32_t* table = tmp.alloc<int32_t>((size_t)nbins * ntiles + 1);
     AGCN_CUDA(cudaMemsetAsync(d_flags, 0, sizeof(PlanFlags), s));
 
-    // colidx validation on a second stream, overlapping the histogram and scan below
-    Overlap ov(s, o.validate && nnz > 0 ? aux_stream(p->device) : nullptr);
-    if (o.validate) validate_cols(rowptr, colidx, nnz, p->n_cols, d_flags, ov.side ? ov.side : s);
-    // (1)+(2a) per-tile bucket histograms, bucket totals, max degree, rowptr validation
+    // (1)+(2a) per-tile bucket histograms, bucket totals, max degree, rowptr validation (the
+    // colidx range is validated inside the sorted-colidx copy at the end, read back once there)
     k_deg_hist<<<(unsigned)ntiles, kThreads, nbins * sizeof(int32_t), s>>>(rowptr, n, db, nbins, ntiles,
                                                                          table, d_flags);
     post_launch();
     exclusive_scan_i32(table, table, (int64_t)nbins * ntiles, s);
     k_bin_totals<<<(nbins + 255) / 256, 256, 0, s>>>(table, ntiles, nbins, n, bin_cnt);
     post_launch();
-    ov.finish();
 
     std::vector<int32_t> h_cnt(nbins);
     PlanFlags hf{};
@@ -983,7 +948,6 @@ void build_block_plan(agcn_plan_s* p, const int32_t* rowptr, const int32_t* coli
         read_flags(d_flags, &hf, s);
     }
     check_csr_flags(hf, nnz);
-    AGCN_CHECK(!hf.bad_colidx, AGCN_ERR_BAD_CSR, "colidx out of [0, n_cols)");
     p->rp_base = hf.rowptr_first;
 
     // host-side bucket bookkeeping (tiny: deg_bound + 2 entries)
@@ -1089,7 +1053,15 @@ void build_block_plan(agcn_plan_s* p, const int32_t* rowptr, const int32_t* coli
         AGCN_CUDA(cudaMemsetAsync(p->ov_chunk_start, 0, sizeof(int32_t), s));
     }
 
-    build_sorted_cols(p, colidx, o, s);
+    build_sorted_cols(p, colidx, o, s, o.validate ? d_flags : nullptr);
+    if (o.validate && nnz > 0) {  // the plan's second (and last) synchronisation: colidx range
+        int32_t* pin = static_cast<int32_t*>(pinned_staging(sizeof(int32_t)));
+        int32_t bad = 0;
+        AGCN_CUDA(cudaMemcpyAsync(pin ? pin : &bad, &d_flags->bad_colidx, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+        AGCN_CUDA(cudaStreamSynchronize(s));
+        if (pin) bad = *pin;
+        AGCN_CHECK(!bad, AGCN_ERR_BAD_CSR, "colidx out of [0, n_cols)");
+    }
 }
 
 // ---------------------------------------------------------------- warp-partition plan
