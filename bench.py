@@ -51,6 +51,7 @@ def parse():
     ap.add_argument("--hot-rows", type=int, default=None, help="agcn_opts_t.hot_rows (None: auto)")
     ap.add_argument("--hot-mb", type=int, default=None, help="agcn_spmm_opts_t.hot_mb (None: device max)")
     ap.add_argument("--chunk-shape", type=int, default=0, help="agcn_spmm_opts_t.chunk_shape (0: auto)")
+    ap.add_argument("--chunk-order", type=int, default=0, help="agcn_spmm_opts_t.chunk_order (0: bucketed, -1: off)")
     ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--pipe-depth", type=int, default=2, help="e2e: agcn_pipe buffer slots")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="CPU-oracle sample budget")
@@ -129,6 +130,7 @@ def live_traffic(args, timeout_s: float = 420.0):
            "--clock-control", "none", "-k", TRAFFIC_KERNELS, "--csv", "--log-file", logf,
            sys.executable, os.path.abspath(__file__), "--profile", "--config", args.config,
            "--steps", "1", "--warmup", "3", "--kernel", args.kernel, "--chunk-shape", str(args.chunk_shape),
+           "--chunk-order", str(args.chunk_order),
            "--mbw", str(args.mbw), "--mwn", str(args.mwn), "--partition", args.partition]
     for k in ("F", "layers", "hot_rows", "hot_mb", "l2_hint"):
         v = getattr(args, k)
@@ -594,7 +596,7 @@ def main():
             s0, s1 = ev(), ev()
             s0.record(stream)
             plan.spmm(va_d, Xin, out=out_rows, kernel=args.kernel, l2_hint=args.l2_hint,
-                      hot_mb=args.hot_mb, chunk_shape=args.chunk_shape, **epi_kw(Xin))
+                      hot_mb=args.hot_mb, chunk_shape=args.chunk_shape, chunk_order=args.chunk_order, **epi_kw(Xin))
             s1.record(stream)
             if record:
                 rec["spmm"].append((s0, s1))
@@ -603,7 +605,7 @@ def main():
                 s0, s1 = ev(), ev()
                 s0.record(stream)
                 plan.spmm(va_d, Xin, out=out_rows, kernel=args.kernel, l2_hint=args.l2_hint,
-                          hot_mb=args.hot_mb, chunk_shape=args.chunk_shape, peer_out=peer_out,
+                          hot_mb=args.hot_mb, chunk_shape=args.chunk_shape, chunk_order=args.chunk_order, peer_out=peer_out,
                           **epi_kw(Xin))
                 s1.record(stream)
                 if record:
@@ -728,7 +730,7 @@ def main():
             chk = []
             with A.Plan(rp_local, ci_d, **plan_kw) as pc:
                 Xin = X0
-                kw = dict(kernel=args.kernel, l2_hint=args.l2_hint, hot_mb=args.hot_mb, chunk_shape=args.chunk_shape)
+                kw = dict(kernel=args.kernel, l2_hint=args.l2_hint, hot_mb=args.hot_mb, chunk_shape=args.chunk_shape, chunk_order=args.chunk_order)
                 for l in range(layers):
                     if K > 1:   # the same column chunks as the timed run
                         Yl = join_columns([pc.spmm(va_d, c, **kw) for c in split_columns(Xin, widths)])

@@ -78,7 +78,8 @@ typedef struct {
     int32_t small_plan;        /* 1 (default): graphs within the one-CTA limits (see agcn_plan_ex)
                                   take the one-CTA plan; 0: always the general plan (same
                                   metadata; for tests and measurements) */
-    int32_t reserved0;
+    int32_t chunk_buckets;     /* oversized-chunk execution order (agcn_spmm_opts_t.chunk_order):
+                                  buckets of in-row position; 0 (default): 64 */
 } agcn_opts_t;
 
 typedef struct {
@@ -211,6 +212,11 @@ typedef struct {
        descriptor); 3, 4: U 4 at that many CTAs/SM; 6: U 2 at 6 CTAs/SM.  Results are bitwise
        the same. */
     int32_t chunk_shape;
+    /* Execution order of the oversized-row chunks (the descriptors keep Alg. 2's order):
+       0 (default): bucketed by the chunk's position in its row (concurrent warps gather from
+       the same part of X: L2 reuse across hub rows); -1: descriptor order.  Same results. */
+    int32_t chunk_order;
+    int32_t pad0_;
     int64_t reserved[2];
 } agcn_spmm_opts_t;
 
@@ -234,8 +240,8 @@ agcn_status_t agcn_plan_destroy(agcn_plan_t plan);
  * The Alg. 1 parameters agcn_plan_ex uses when opts.max_block_warps == opts.max_warp_nzs == 0:
  * a host-only rule in n, nnz and the SM count (sms <= 0: the current device's), measured on
  * B200 (profiles/r01at_auto_partition.md).  With share = nnz / (sms * 24):
- * share < 8 -> (12, 32); nnz >= 256 n -> (24, 32); share < 960 -> (4, 16), (8, 16) or (8, 32)
- * for share / 2.5 below 128, below 256, at least 256; else (12, 32).  Never fails for
+ * share < 8 -> (12, 32); share < 960 -> (4, 16), (8, 16) or (8, 32) for share / 2.5 below
+ * 128, below 256, at least 256; else (12, 32).  Never fails for
  * n, nnz >= 0 and non-NULL outputs (else AGCN_ERR_INVALID_ARG).
  */
 agcn_status_t agcn_auto_partition(int64_t n, int64_t nnz, int32_t sms, int32_t* max_block_warps,

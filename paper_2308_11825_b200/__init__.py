@@ -95,7 +95,7 @@ class Plan:
     def __init__(self, rowptr, colidx, n: int | None = None, nnz: int | None = None, *,
                  n_cols: int | None = None, max_block_warps: int = 12, max_warp_nzs: int = 32,
                  partition: str = "block", col_bounds=None, col_slot_rows: int | None = None,
-                 hot_rows: int | None = None, small_plan: bool = True, stream=None):
+                 hot_rows: int | None = None, small_plan: bool = True, chunk_buckets: int = 0, stream=None):
         L = _lib.lib()
         rp = _dev_ptr(rowptr, "int32", "rowptr")
         ci = _dev_ptr(colidx, "int32", "colidx") if colidx.numel() else 0
@@ -112,6 +112,7 @@ class Plan:
         opts.stream = _stream_handle(stream)
         opts.hot_rows = -1 if hot_rows is None else int(hot_rows)
         opts.small_plan = int(bool(small_plan))
+        opts.chunk_buckets = int(chunk_buckets)
         self._bounds_keep = None
         if col_bounds is not None:
             b = np.ascontiguousarray(col_bounds, dtype=np.int64)
@@ -152,7 +153,8 @@ class Plan:
 
     def spmm(self, vals, X, out=None, stream=None, kernel: str = "auto", l2_hint=None,
              hot_mb: int | None = None, aggregation: str = "sum", self_x=None,
-             self_scale: float = 0.0, bias=None, relu: bool = False, peer_out=(), chunk_shape: int = 0):
+             self_scale: float = 0.0, bias=None, relu: bool = False, peer_out=(), chunk_shape: int = 0,
+             chunk_order: int = 0):
         """Y = A.X (asynchronous on `stream`, default the current torch stream).
 
         kernel: "auto" | "general" | "looped" | "wide" (agcn_kernel_t).  l2_hint
@@ -176,7 +178,8 @@ class Plan:
         x = _dev_ptr(X, "float32", "X") if X.numel() else 0
         y = _dev_ptr(out, "float32", "out") if out.numel() else 0
         opts = _spmm_opts(kernel, l2_hint, hot_mb, aggregation, self_x, self_scale, bias, relu,
-                          shape=(self.n, F), peer_out=peer_out, chunk_shape=chunk_shape)
+                          shape=(self.n, F), peer_out=peer_out, chunk_shape=chunk_shape,
+                          chunk_order=chunk_order)
         _check(_lib.lib().agcn_spmm_ex(self.handle, v or None, x or None, int(F), y or None,
                                        _stream_handle(stream), opts))
         return out
@@ -201,13 +204,14 @@ class Plan:
 
 def _spmm_opts(kernel: str = "auto", l2_hint=None, hot_mb: int | None = None,
                aggregation: str = "sum", self_x=None, self_scale: float = 0.0, bias=None,
-               relu: bool = False, shape=None, peer_out=(), chunk_shape: int = 0):
+               relu: bool = False, shape=None, peer_out=(), chunk_shape: int = 0, chunk_order: int = 0):
     o = _lib.SpmmOpts()
     _lib.lib().agcn_default_spmm_opts(ctypes.byref(o))
     o.kernel = _lib.KERNELS[kernel]
     o.l2_hint = _lib.L2_HINTS[l2_hint] if l2_hint is None or isinstance(l2_hint, str) else int(l2_hint)
     o.hot_mb = 0 if hot_mb is None else int(hot_mb)
     o.chunk_shape = int(chunk_shape)
+    o.chunk_order = int(chunk_order)
     o.aggregation = {"sum": 0, "mean": 1}[aggregation]
     o.relu = int(bool(relu))
     o.self_scale = float(self_scale)

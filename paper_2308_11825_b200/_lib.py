@@ -20,7 +20,7 @@ class Opts(ctypes.Structure):
                 ("validate", c_i32), ("n_cols", c_i64), ("stream", c_vp),
                 ("col_bounds", ctypes.POINTER(c_i64)), ("col_nparts", c_i32),
                 ("col_slot_rows", c_i64), ("hot_rows", c_i64), ("small_plan", c_i32),
-                ("reserved0", c_i32)]
+                ("chunk_buckets", c_i32)]
 
 
 KERNELS = {"auto": 0, "general": 1, "looped": 2, "wide": 3}
@@ -32,7 +32,8 @@ class SpmmOpts(ctypes.Structure):
     _fields_ = [("kernel", c_i32), ("l2_hint", c_i32), ("hot_mb", c_i32),
                 ("aggregation", c_i32), ("self_scale", ctypes.c_float), ("relu", c_i32),
                 ("self", c_vp), ("bias", c_vp), ("peer_out", c_vp * 8), ("npeer", c_i32),
-                ("chunk_shape", c_i32), ("reserved", c_i64 * 2)]
+                ("chunk_shape", c_i32), ("chunk_order", c_i32), ("pad0_", c_i32),
+                ("reserved", c_i64 * 2)]
 
 
 class Stats(ctypes.Structure):

@@ -124,6 +124,7 @@ agcn_status_t agcn_spmm_ex(agcn_plan_t plan, const float* vals, const float* X, 
         AGCN_CHECK(o.hot_mb >= 0, AGCN_ERR_INVALID_ARG, "hot_mb must be >= 0");
         AGCN_CHECK(o.chunk_shape == -1 || o.chunk_shape == 0 || o.chunk_shape == 3 || o.chunk_shape == 4 ||
                        o.chunk_shape == 6, AGCN_ERR_INVALID_ARG, "chunk_shape must be -1, 0, 3, 4 or 6");
+        AGCN_CHECK(o.chunk_order == 0 || o.chunk_order == -1, AGCN_ERR_INVALID_ARG, "chunk_order must be 0 or -1");
         AGCN_CHECK(o.aggregation == AGCN_AGG_SUM || o.aggregation == AGCN_AGG_MEAN, AGCN_ERR_INVALID_ARG,
                    "unknown aggregation");
         AGCN_CHECK(o.self_scale == 0.f || o.self != nullptr, AGCN_ERR_INVALID_ARG,

@@ -206,6 +206,7 @@ struct agcn_plan_s {
     agcn::ColMap cmap{};               // optional padded-layout column relabel
     int4* desc = nullptr;              // [nblocks]
     int32_t* ov_chunk_start = nullptr; // [n_ov + 1]
+    int32_t* ov_order = nullptr;       // [ov_chunks] execution order of the oversized chunks
 
     // AGCN_PARTITION_WARP
     int64_t ntasks = 0;
@@ -233,7 +234,8 @@ bool wide_supported(const agcn_plan_s* p, const float* X, const float* Y, int32_
 // l2: agcn_l2_hint_t resolved (NONE / KEEP_ALL / HOT_WINDOW / HOT_HINTS); Xh: the hot rows
 // (plans with n_hot > 0); win_bytes: the persisting window over Xh (HOT_WINDOW)
 void launch_wide(agcn_plan_s* p, const float* vals, const float* X, const float* Xh, int32_t F, float* Y,
-                 int l2, size_t win_bytes, bool fuse_ov, int chunk_shape, const Epi& epi, cudaStream_t s);
+                 int l2, size_t win_bytes, bool fuse_ov, int chunk_shape, bool chunk_order, const Epi& epi,
+                 cudaStream_t s);
 // spmm.cu: set the device's persisting-L2 limit to at least `bytes` (once per device and size);
 // returns the window size usable (0 if the device refuses)
 size_t ensure_persisting_l2(size_t bytes);

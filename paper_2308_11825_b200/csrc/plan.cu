@@ -315,6 +315,23 @@ __global__ void k_hot_list(uint2* __restrict__ hot, const int32_t* __restrict__ 
     }
 }
 
+// Execution order of the oversized-row chunks (kernel-internal; the descriptors keep Alg. 2's
+// order): chunk j of a row of nc chunks covers the j-th run of the row's columns, which lie
+// around fraction (j + 0.5) / nc of the column range when the row's columns are sorted and
+// spread over it; executing the chunks bucketed by that fraction lets concurrently running
+// warps gather from the same part of X, so X rows are reused across hub rows in L2 (P:491,
+// "improving cache hit rate").  key = bucket in [0, kOvBuckets), stable sort by key.
+constexpr int kOvBuckets = 64;
+__global__ void k_ov_keys(const int4* __restrict__ desc, int64_t nb_small, int64_t nch, int32_t db, int32_t nbk,
+                          const int32_t* __restrict__ srp, int32_t* __restrict__ key, int32_t* __restrict__ idx) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= nch) return;
+    const int4 m = desc[nb_small + i];
+    const int32_t j = (m.y - srp[m.z]) / db, nc = (m.x + db - 1) / db;
+    key[i] = (int32_t)min((int64_t)nbk - 1, ((2 * (int64_t)j + 1) * nbk) / (2 * (int64_t)nc));
+    idx[i] = (int32_t)i;
+}
+
 // Introspection (agcn_plan_copy(AGCN_FIELD_SORTED_COLIDX)): the plan's sorted colidx with the
 // hot encoding undone.
 __global__ void k_decode_hot(const int32_t* __restrict__ sc, int64_t nnz, const int32_t* __restrict__ hot_cols,
@@ -508,6 +525,25 @@ int64_t hot_rows_for(const agcn_plan_s* p, int64_t req) {
     const int64_t live = p->n - p->n_zero;  // vertices of degree >= 1
     int64_t H = req > 0 ? req : (p->n >= (1ll << 19) ? 262144 : 0);
     return std::max<int64_t>(0, std::min(H, live));
+}
+
+// BLOCK plan, after the descriptors: the execution order of the oversized chunks (k_ov_keys).
+void build_ov_order(agcn_plan_s* p, int32_t buckets, cudaStream_t s) {
+    const int64_t m = p->ov_chunks;
+    const int32_t nbk = buckets > 0 ? buckets : kOvBuckets;
+    if (m <= 1) return;
+    Scratch tmp(s);
+    int32_t* ka = tmp.alloc<int32_t>(m);
+    int32_t* va = tmp.alloc<int32_t>(m);
+    int32_t* kb = tmp.alloc<int32_t>(m);
+    int32_t* vb = tmp.alloc<int32_t>(m);
+    k_ov_keys<<<blocks_for(m, 256), 256, 0, s>>>(p->desc, p->nb_small, m, p->deg_bound, nbk, p->sorted_rowptr,
+                                                  ka, va);
+    post_launch();
+    radix_sort_pairs(ka, va, kb, vb, m, nbk - 1, s);
+    p->ov_order = dalloc<int32_t>(m, s);
+    p->device_bytes += sizeof(int32_t) * (size_t)m;
+    AGCN_CUDA(cudaMemcpyAsync(p->ov_order, va, sizeof(int32_t) * m, cudaMemcpyDeviceToDevice, s));
 }
 
 // BLOCK plan, after the descriptors: the degree-sorted colidx (P:295 (3)) with the hot encoding;
@@ -908,6 +944,7 @@ bool build_block_plan_small(agcn_plan_s* p, const int32_t* rowptr, const int32_t
     p->nblocks = h.nb_small + h.ov_chunks;
     p->device_bytes = sizeof(int32_t) * (size_t)(3 * n + 1 + ovc_cap) + sizeof(int4) * (size_t)desc_cap;
     build_sorted_cols(p, colidx, o, s);
+    build_ov_order(p, o.chunk_buckets, s);
     return true;
 }
 
@@ -1054,6 +1091,7 @@ void build_block_plan(agcn_plan_s* p, const int32_t* rowptr, const int32_t* coli
     }
 
     build_sorted_cols(p, colidx, o, s, o.validate ? d_flags : nullptr);
+    build_ov_order(p, o.chunk_buckets, s);
     if (o.validate && nnz > 0) {  // the plan's second (and last) synchronisation: colidx range
         int32_t* pin = static_cast<int32_t*>(pinned_staging(sizeof(int32_t)));
         int32_t bad = 0;
@@ -1101,7 +1139,7 @@ void build_warp_plan(agcn_plan_s* p, const int32_t* rowptr, const int32_t* colid
 void free_plan_arrays(agcn_plan_s* p) {
     void* ptrs[] = {p->perm,  p->sorted_rowptr, p->row_src_off, p->desc,       p->ov_chunk_start,
                     p->tasks, p->rowptr_copy,   p->cols_copy,   p->ov_partial, p->ov_cnt,
-                    p->scols, p->xhot, p->hot_cols};
+                    p->scols, p->xhot, p->hot_cols, p->ov_order};
     // Stream-ordered release on the plan's stream, after the last SpMM that used the plan on
     // another stream (p->last_use); no host synchronisation.
     if (p->last_use) cudaStreamWaitEvent(p->stream, p->last_use, 0);
@@ -1142,11 +1180,13 @@ static void keep_pool_cached(int dev) {
 // profiles/r01at_auto_partition.md, in terms of share = nnz per resident warp of the default
 // SpMM kernel (SMs x 24):
 //   * share < 8 (tiny graphs, launch-bound):          (12, 32) -- the paper's values
-//   * mean degree >= 256 (dense hubs, Reddit-shaped):  (24, 32) -- deg_bound 768, rows stay whole
 //   * share < 960 (small graphs):  deg_bound = largest of 64/128/256 <= max(64, share / 2.5) --
 //     oversized-row chunks short against a warp's share, so the chunk tail (processed last,
 //     degree order ascending) does not set the critical path: (4,16) / (8,16) / (8,32)
 //   * otherwise:                                       (12, 32)
+// (Round 1 kept dense-hub graphs, mean degree >= 256, at (24, 32) to keep their rows whole;
+// with the oversized chunks executed in column-position order (round 2) (12, 32) is faster on
+// C4: 3.64 vs 3.78 ms, profiles/r02x_chunk_order.txt.)
 void auto_partition(int64_t n, int64_t nnz, int32_t sms, int32_t* mbw, int32_t* mwn) {
     if (sms <= 0) {
         int dev = 0;
@@ -1157,16 +1197,13 @@ void auto_partition(int64_t n, int64_t nnz, int32_t sms, int32_t* mbw, int32_t* 
     *mbw = 12;
     *mwn = 32;
     if (share < 8) return;
-    if (n > 0 && nnz >= 256 * n) {
-        *mbw = 24;
-        return;
-    }
     if (share < 960) {
         const double t = share / 2.5;
         if (t >= 256) { *mbw = 8; *mwn = 32; }
         else if (t >= 128) { *mbw = 8; *mwn = 16; }
         else { *mbw = 4; *mwn = 16; }
     }
+    (void)n;
 }
 
 agcn_plan_s* build_plan(const int32_t* rowptr, const int32_t* colidx, int64_t n, int64_t nnz,

@@ -776,7 +776,7 @@ void spmm_launch(agcn_plan_s* p, const float* vals, const float* X, int32_t F, f
     }
     if (kernel == AGCN_KERNEL_WIDE)
     {
-        launch_wide(p, vals, X, p->xhot, F, Y, l2, win, fuse, o.chunk_shape, epi, s);  // epilogue fused
+        launch_wide(p, vals, X, p->xhot, F, Y, l2, win, fuse, o.chunk_shape, o.chunk_order == 0, epi, s);  // epilogue fused
         if (win > 0) {
             const int64_t lines = (int64_t)((win + 127) / 128);
             k_l2_discard<<<(unsigned)std::min<int64_t>((lines + 255) / 256, (int64_t)num_sms() * 8), 256, 0, s>>>(

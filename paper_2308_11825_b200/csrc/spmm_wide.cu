@@ -102,6 +102,7 @@ struct WideArgs {
     const float* Xh;      // hot rows [n_hot][F] (XM >= 2)
     float* Y;
     float* ovp;           // oversized partial rows [ov_chunks][F]
+    const int32_t* ov_order;  // execution order of the oversized chunks, or NULL (descriptor order)
     int32_t db;           // deg_bound
     Epi epi;              // output epilogue (EPI)
     int32_t L;            // lanes per X row (F / 8); used when the kernel's LT is 0
@@ -207,7 +208,9 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_wide(const __grid_const
     };
 
     const int32_t n_desc = (int32_t)a.n_desc;
-    for (int32_t b = gw; b < n_desc; b += W) {
+    for (int32_t b0 = gw; b0 < n_desc; b0 += W) {
+        // the oversized chunks [first_ov, n_desc) run in the plan's execution order
+        const int32_t b = a.ov_order && b0 >= a.first_ov ? (int32_t)a.first_ov + __ldg(a.ov_order + (b0 - a.first_ov)) : b0;
         const int4 m = __ldg(a.desc + b);
         const bool ov = m.x > a.db;
         const int32_t R = ov ? 1 : (m.w & 0xffff);      // rows of the descriptor (<= 32)
@@ -399,7 +402,8 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_chunks(const __grid_con
     const int32_t gw = blockIdx.x * kWarps + (threadIdx.x >> 5);
     const int32_t W = gridDim.x * kWarps;
     const int32_t nch = (int32_t)(a.n_desc - a.first_ov);
-    for (int32_t i = gw; i < nch; i += W) {
+    for (int32_t i0 = gw; i0 < nch; i0 += W) {
+        const int32_t i = a.ov_order ? __ldg(a.ov_order + i0) : i0;   // the plan's execution order
         const int4 m = __ldg(a.desc + a.first_ov + i);
         const int32_t len = m.w;
         const int32_t vb = __ldg(a.rso + m.z) + (m.y - __ldg(a.srp + m.z));  // chunk start in vals
@@ -564,9 +568,11 @@ bool wide_supported(const agcn_plan_s* p, const float* X, const float* Y, int32_
 }
 
 void launch_wide(agcn_plan_s* p, const float* vals, const float* X, const float* Xh, int32_t F, float* Y,
-                 int l2, size_t win, bool fuse_ov, int chunk_shape, const Epi& epi, cudaStream_t s) {
+                 int l2, size_t win, bool fuse_ov, int chunk_shape, bool chunk_order, const Epi& epi,
+                 cudaStream_t s) {
     WideArgs a{p->desc, p->nblocks, p->nb_small, p->n_zero, p->scols, p->sorted_rowptr, p->row_src_off,
-               p->perm, vals + p->rp_base, X, Xh, Y, p->ov_partial, p->deg_bound, epi};
+               p->perm, vals + p->rp_base, X, Xh, Y, p->ov_partial, chunk_order ? p->ov_order : nullptr,
+               p->deg_bound, epi};
     AGCN_CHECK(a.n_desc < (1ll << 31), AGCN_ERR_OVERFLOW, "too many descriptors");
     a.L = F / 8;
     a.fuse_ov = fuse_ov && p->n_ov > 0 && p->ov_cnt != nullptr;

@@ -788,3 +788,23 @@ def test_graph_scratch_guard():
     Y64 = p.spmm(va, X64).cpu().numpy()
     check_spmm(p, w.rowptr, w.colidx, w.vals, w.X(64), Y64)
     g.close()
+
+
+@pytest.mark.parametrize("F", [8, 40, 64, 128, 256])
+def test_chunk_order_and_chunk_kernel(F):
+    """The oversized chunks in column-position order (agcn_spmm_opts_t.chunk_order, plan option
+    chunk_buckets) and in the separate chunk kernel (chunk_shape) give bitwise the result of
+    descriptor order in the main kernel, which passes the oracle."""
+    rowptr, colidx, vals, X = _hub_graph(4000, 100 + F, F)
+    ref = None
+    for mbw, mwn in ((2, 8), (12, 32)):
+        for buckets in (0, 3, 1000):
+            p = make_plan(rowptr, colidx, max_block_warps=mbw, max_warp_nzs=mwn, chunk_buckets=buckets, hot_rows=0)
+            Y0 = p.spmm(cu(vals), cu(X), kernel="wide", chunk_order=-1, chunk_shape=-1).cpu().numpy()
+            if ref is None:
+                check_spmm(p, rowptr, colidx, vals, X, Y0)
+            for order in (0, -1):
+                for shape in (-1, 0, 3, 4, 6):
+                    Y = p.spmm(cu(vals), cu(X), kernel="wide", chunk_order=order, chunk_shape=shape).cpu().numpy()
+                    assert np.array_equal(Y, Y0), (mbw, mwn, buckets, order, shape)
+            ref = Y0
