@@ -184,8 +184,9 @@ typedef struct {
     int32_t kernel;       /* agcn_kernel_t; default AGCN_KERNEL_AUTO */
     int32_t l2_hint;      /* X-row L2 residency (agcn_l2_hint_t; results never depend on it).
                              Plans with hot rows always read them from the compact buffer;
-                             AGCN_L2_AUTO (default): KEEP_ALL when X fits in L2 (<= 128 MiB) and
-                             the plan has no hot rows, else NONE (profiles/r02_c5_roof.md) */
+                             AGCN_L2_AUTO (default): HOT_HINTS for plans with hot rows, else
+                             KEEP_ALL when X fits in L2 (<= 128 MiB), else NONE
+                             (profiles/r02_c5_roof.md, r02z_l2_modes.txt) */
     int32_t hot_mb;       /* HOT_* modes: MiB of hot X rows kept resident (rows = hot_mb MiB /
                              (4 F), at most the plan's hot_rows); 0 (default): the device's
                              maximum persisting-L2 size */

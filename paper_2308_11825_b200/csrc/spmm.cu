@@ -731,11 +731,12 @@ void spmm_launch(agcn_plan_s* p, const float* vals, const float* X, int32_t F, f
     // L2 residency of X (agcn_l2_hint_t)
     const double x_bytes = 4.0 * (double)p->x_rows * F;
     int l2 = o.l2_hint;
-    // auto: evict_last on all of X when it fits in L2; otherwise plain loads (the hot rows, if
-    // the plan has them, still come from the compact buffer).  The persisting window and the
-    // hot/cold hints measured no faster than the compact buffer alone on C5 (r02k), and the
-    // window changes a device-wide limit that slowed the next kernels by 10-15 % -- opt-in only.
-    if (l2 == AGCN_L2_AUTO) l2 = x_bytes <= kL2KeepBytes && p->n_hot == 0 ? AGCN_L2_KEEP_ALL : AGCN_L2_NONE;
+    // auto: evict_last on all of X when it fits in L2; plans with hot rows: the compact hot
+    // buffer with evict_last hot / evict_first cold loads (C5 -1.8 % against plain loads, 3 x 3
+    // runs, profiles/r02z_l2_modes.txt); otherwise plain loads.  The persisting window measured
+    // slower in the bench flow (C5 3.57 vs 3.27 ms; it changes a device-wide limit) -- opt-in.
+    if (l2 == AGCN_L2_AUTO)
+        l2 = p->n_hot > 0 ? AGCN_L2_HOT_HINTS : (x_bytes <= kL2KeepBytes ? AGCN_L2_KEEP_ALL : AGCN_L2_NONE);
     AGCN_CHECK(l2 >= AGCN_L2_NONE && l2 <= AGCN_L2_HOT_HINTS, AGCN_ERR_INVALID_ARG, "unknown l2_hint");
     if ((l2 == AGCN_L2_HOT_WINDOW || l2 == AGCN_L2_HOT_HINTS) && p->n_hot == 0) l2 = AGCN_L2_NONE;
     size_t win = 0;
