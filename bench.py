@@ -42,9 +42,9 @@ def parse():
     ap.add_argument("--layers", type=int, default=None)
     ap.add_argument("--partition", choices=["block", "warp"], default="block")
     ap.add_argument("--kernel", choices=["auto", "general", "looped", "wide"], default="auto")
-    ap.add_argument("--mbw", type=int, default=12, help="Alg. 1 max_block_warps (P:318; paper: 12; "
-                    "0 with --mwn 0: agcn_auto_partition's per-graph choice)")
-    ap.add_argument("--mwn", type=int, default=32, help="Alg. 1 max_warp_nzs (P:318; SPEC default 32)")
+    ap.add_argument("--mbw", type=int, default=0, help="Alg. 1 max_block_warps (P:318; the paper's storage "
+                    "example: 12); 0 with --mwn 0 (default): agcn_auto_partition's per-graph choice")
+    ap.add_argument("--mwn", type=int, default=0, help="Alg. 1 max_warp_nzs (P:318; SPEC default 32)")
     ap.add_argument("--l2-hint", default=None,
                     choices=["auto", "none", "keep_all", "hot_window", "hot_hints"],
                     help="agcn_l2_hint_t (default auto: hot_window for plans with hot rows)")

@@ -1183,10 +1183,12 @@ static void keep_pool_cached(int dev) {
 //   * share < 960 (small graphs):  deg_bound = largest of 64/128/256 <= max(64, share / 2.5) --
 //     oversized-row chunks short against a warp's share, so the chunk tail (processed last,
 //     degree order ascending) does not set the critical path: (4,16) / (8,16) / (8,32)
-//   * otherwise:                                       (12, 32)
+//   * otherwise, mean degree < 64:                    (32, 16) -- many short rows: 32-row
+//     descriptors amortise the per-descriptor metadata chain (C5 3.27 vs 3.42 ms at (12, 32))
+//   * otherwise:                                       (12, 32)  (C4: best of the sweep)
 // (Round 1 kept dense-hub graphs, mean degree >= 256, at (24, 32) to keep their rows whole;
 // with the oversized chunks executed in column-position order (round 2) (12, 32) is faster on
-// C4: 3.64 vs 3.78 ms, profiles/r02x_chunk_order.txt.)
+// C4: 3.64 vs 3.78 ms, profiles/r02x_chunk_order.txt, r02ad_partition_sweep.txt.)
 void auto_partition(int64_t n, int64_t nnz, int32_t sms, int32_t* mbw, int32_t* mwn) {
     if (sms <= 0) {
         int dev = 0;
@@ -1202,8 +1204,12 @@ void auto_partition(int64_t n, int64_t nnz, int32_t sms, int32_t* mbw, int32_t* 
         if (t >= 256) { *mbw = 8; *mwn = 32; }
         else if (t >= 128) { *mbw = 8; *mwn = 16; }
         else { *mbw = 4; *mwn = 16; }
+        return;
     }
-    (void)n;
+    if (n > 0 && nnz < 64 * n) {
+        *mbw = 32;
+        *mwn = 16;
+    }
 }
 
 agcn_plan_s* build_plan(const int32_t* rowptr, const int32_t* colidx, int64_t n, int64_t nnz,

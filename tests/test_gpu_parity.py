@@ -388,8 +388,9 @@ def test_full_size_every_row(name):
     through the default path (C5: hot rows on); the plan without hot rows gives bitwise the same Y."""
     w = gen.make_config(name)
     rp, ci, va = cu(w.rowptr), cu(w.colidx), cu(w.vals)
-    p = A.Plan(rp, ci)
-    o = oracle.plan(w.rowptr, w.colidx)                 # integer metadata bit-exact at full size
+    p = A.Plan(rp, ci, max_block_warps=0, max_warp_nzs=0)   # the bench's (auto) Alg. 1 parameters
+    st = p.stats()
+    o = oracle.plan(w.rowptr, w.colidx, st["max_block_warps"], st["max_warp_nzs"])  # bit-exact at full size
     for field in ("perm", "sorted_rowptr", "row_src_off", "blocks", "sorted_colidx"):
         assert np.array_equal(p.copy(field), o[field]), field
     del o
@@ -400,7 +401,7 @@ def test_full_size_every_row(name):
     r = oracle.spmm_check(w.rowptr, w.colidx, w.vals, X, Yh)
     assert r["nfail"] == 0 and r["rows"] == w.n, r
     if p.stats()["hot_rows"] > 0:
-        p0 = A.Plan(rp, ci, hot_rows=0)
+        p0 = A.Plan(rp, ci, hot_rows=0, max_block_warps=0, max_warp_nzs=0)
         assert torch.equal(p0.spmm(va, Xd), Y)
         p0.close()
     if w.layers > 1:                                   # layer 2 on the GPU's own layer-1 output
