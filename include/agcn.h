@@ -71,7 +71,7 @@ typedef struct {
        plan-owned buffer that an L2 persisting window (or evict_last hints) keeps resident.
        Row degree stands in for column in-degree (correlation 0.997-0.9997 on the power-law
        configs, profiles/r02_c5_roof.md).  Needs a square A (n_cols == n) without col_bounds.
-       -1 (default): auto -- min(n, 262144) when n >= 2^19 (X of 128+ MiB at F = 64), else 0;
+       -1 (default): auto -- min(n, 524288) when n >= 2^19 (X of 128+ MiB at F = 64), else 0;
        0: off; > 0: that many rows (capped at the rows of degree >= 1).  Results do not depend
        on it.  Costs the plan one lookup per nonzero (C5: +0.4 ms). */
     int64_t hot_rows;

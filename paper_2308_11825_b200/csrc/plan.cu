@@ -523,7 +523,7 @@ void copy_cols_original(agcn_plan_s* p, const int32_t* colidx, cudaStream_t s) {
 int64_t hot_rows_for(const agcn_plan_s* p, int64_t req) {
     if (p->n_cols != p->n || p->cmap.nparts > 0 || req == 0) return 0;
     const int64_t live = p->n - p->n_zero;  // vertices of degree >= 1
-    int64_t H = req > 0 ? req : (p->n >= (1ll << 19) ? 262144 : 0);
+    int64_t H = req > 0 ? req : (p->n >= (1ll << 19) ? 524288 : 0);  // C5 sweep: profiles/r02af
     return std::max<int64_t>(0, std::min(H, live));
 }
 

@@ -274,7 +274,7 @@ def test_hot_rows_auto_rule():
     rowptr[1:] = np.arange(1, 2 ** 19 + 1)
     colidx = (np.arange(2 ** 19, dtype=np.int64) * 7919 % 2 ** 19).astype(np.int32)
     p = make_plan(rowptr, colidx)
-    assert p.stats()["hot_rows"] == 262144
+    assert p.stats()["hot_rows"] == 2 ** 19
     p2 = make_plan(rowptr, colidx, n_cols=2 ** 19 + 5)
     assert p2.stats()["hot_rows"] == 0
     vals = np.ones(colidx.size, np.float32)
