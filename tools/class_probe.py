@@ -38,6 +38,8 @@ def timed(fn, reps=10):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--hot-rows", type=int, default=None)
+    ap.add_argument("--mbw", type=int, default=12)
+    ap.add_argument("--mwn", type=int, default=32)
     args = ap.parse_args()
     dev = torch.device("cuda:0")
     w = agcn_inputs.make_config("c5")
@@ -46,7 +48,7 @@ def main():
     X = torch.from_numpy(w.X()).to(dev)
     Y = torch.empty_like(X)
     classes = [("all", 1, 1 << 30), ("zero rows only", 0, 0), ("deg 1-8", 1, 8), ("deg 9-32", 9, 32),
-               ("deg 33-128", 33, 128), ("deg 129-384", 129, 384), ("deg > 384", 385, 1 << 30)]
+               ("deg 33-128", 33, 128), ("deg 129-384", 129, 384), ("deg 385-512", 385, 512), ("deg > 512", 513, 1 << 30)]
     tot = deg.sum()
     for name, lo, hi in classes:
         keep = (deg >= lo) & (deg <= hi)
@@ -56,7 +58,7 @@ def main():
         ci = w.colidx[idx]
         va = w.vals[idx]
         p = agcn.Plan(torch.from_numpy(rp.astype(np.int32)).to(dev), torch.from_numpy(ci).to(dev),
-                      hot_rows=args.hot_rows)
+                      hot_rows=args.hot_rows, max_block_warps=args.mbw, max_warp_nzs=args.mwn)
         vd = torch.from_numpy(va).to(dev)
         t = timed(lambda: p.spmm(vd, X, out=Y))
         nz = int(keep.sum() if lo > 0 else 0)
