@@ -195,10 +195,9 @@ struct agcn_plan_s {
     int32_t* sorted_rowptr = nullptr;  // [n+1] row pointer of the degree-sorted CSR (P:295 (3))
     int32_t* row_src_off = nullptr;    // [n]   rowptr[perm[k]] - rowptr[0]
     // plan-owned column indices (the plan copies colidx):
-    int32_t* scols = nullptr;          // BLOCK: [nnz] colidx of the degree-sorted CSR (P:295 (3));
-                                       // descriptor {d, loc, ..} reads scols[loc ..]; padded-layout
-                                       // relabel applied; hot column -> -1 - slot
-    int32_t* cols_copy = nullptr;      // WARP: [nnz] colidx in the original order (rowptr-relative)
+    int32_t* cols_copy = nullptr;      // [nnz] colidx in the caller's order (rowptr-relative): the
+                                       // SpMM reads it at row_src_off like vals; padded-layout
+                                       // relabel applied; BLOCK plans: hot column -> -1 - slot
     int64_t n_hot = 0;                 // hot X rows (the n_hot highest-degree vertices, square A)
     int32_t* hot_cols = nullptr;       // [n_hot] column of hot slot k (slots in column order)
     float* xhot = nullptr;             // SpMM scratch: X rows of the hot slots [n_hot][F]

@@ -225,14 +225,14 @@ __global__ void k_validate_cols(const int32_t* __restrict__ rowptr, const int32_
     if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) flags->bad_colidx = 1;
 }
 
-// (3) continued: the plan's own colidx of the degree-sorted CSR.  Every descriptor is a
-// contiguous run [loc, loc + rows * deg) of the sorted CSR (chunk: [loc, loc + info)), its rows
-// starting at row_src_off in the caller's colidx; one warp copies one descriptor, 4 entries per
-// lane in flight.  On the way: the padded-layout relabel (ColMap, multi-GPU) or the hot-column
-// encoding c -> -1 - slot, slot = rank of c among the hot columns, from one 8-byte entry
-// {bitmap word, exclusive popcount prefix} per 32 columns (n_cols / 4 bytes, L2-resident).
-// Out-of-range columns are copied unchanged (the plan is rejected by the validation flags
-// before use; with validation off the caller guarantees the range).
+// The plan's copy of colidx (the caller may free its arrays after agcn_plan),
+// in the caller's order -- the SpMM reads a sorted row's column indices and vals at the same
+// offsets (row_src_off, P:295 step (3)) -- made in one flat, coalesced pass: 4 entries per
+// thread in flight.  On the way: the colidx range check (flags != NULL), the padded-layout
+// relabel (ColMap, multi-GPU) or the hot-column encoding c -> -1 - slot, slot = rank of c among
+// the hot columns, from one 8-byte entry {bitmap word, exclusive popcount prefix} per 32
+// columns (n_cols / 4 bytes, L2-resident).  Out-of-range columns are copied unchanged (the plan
+// is rejected by the flags before use; with validation off the caller guarantees the range).
 __device__ __forceinline__ int32_t encode_col(int32_t c, int64_t n_cols, const ColMap& cm,
                                               const uint2* __restrict__ hot) {
     if (cm.nparts > 0) return map_col(c, cm);
@@ -244,47 +244,24 @@ __device__ __forceinline__ int32_t encode_col(int32_t c, int64_t n_cols, const C
     return c;
 }
 
-__global__ void k_sorted_cols(const int4* __restrict__ desc, int64_t nblocks, int32_t db,
-                              const int32_t* __restrict__ srp, const int32_t* __restrict__ rso,
-                              const int32_t* __restrict__ cols, int64_t n_cols, ColMap cm,
-                              const uint2* __restrict__ hot, int32_t* __restrict__ out,
-                              PlanFlags* __restrict__ flags) {
-    const int lane = threadIdx.x & 31;
-    int32_t bad = 0;  // colidx validation fused into the copy (flags != NULL)
-    const int64_t W = (int64_t)gridDim.x * (blockDim.x / 32);
-    for (int64_t b = (int64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5); b < nblocks; b += W) {
-        const int4 m = __ldg(desc + b);
-        const bool ov = m.x > db;
-        const int32_t d = ov ? m.w : m.x;
-        const int32_t total = ov ? m.w : (m.w & 0xffff) * d;
-        const int32_t src0 = ov ? __ldg(rso + m.z) + (m.y - __ldg(srp + m.z)) : 0;
-        const float rd = __frcp_rn((float)d);  // e / d exactly (e < 2^15, see spmm_wide.cu)
-        for (int32_t e0 = 0; e0 < total; e0 += 128) {
-            int32_t c[4];
+__global__ void k_copy_cols_enc(const int32_t* __restrict__ cols, int64_t nnz, int64_t n_cols, ColMap cm,
+                                const uint2* __restrict__ hot, int32_t* __restrict__ out,
+                                PlanFlags* __restrict__ flags) {
+    int32_t bad = 0;
+    const int64_t T = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t q0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q0 < nnz; q0 += 4 * T) {
+        int32_t c[4];
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                const int32_t e = e0 + k * 32 + lane;
-                c[k] = 0;
-                if (e < total) {
-                    int32_t src = src0 + e;
-                    if (!ov) {
-                        const int32_t i = __float2int_rz(__fmul_rn((float)e + 0.5f, rd));
-                        src = __ldg(rso + m.z + i) + (e - i * d);
-                    }
-                    c[k] = __ldcs(cols + src);
-                }
-            }
+        for (int k = 0; k < 4; ++k) c[k] = q0 + k * T < nnz ? __ldcs(cols + q0 + k * T) : 0;
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                const int32_t e = e0 + k * 32 + lane;
-                if (e < total) {
-                    bad |= (c[k] < 0) | ((int64_t)c[k] >= n_cols);
-                    __stcs(out + (int64_t)m.y + e, encode_col(c[k], n_cols, cm, hot));
-                }
+        for (int k = 0; k < 4; ++k) {
+            if (q0 + k * T < nnz) {
+                bad |= (c[k] < 0) | ((int64_t)c[k] >= n_cols);
+                __stcs(out + q0 + k * T, encode_col(c[k], n_cols, cm, hot));
             }
         }
     }
-    if (flags && __any_sync(0xffffffffu, bad) && lane == 0) flags->bad_colidx = 1;
+    if (flags && __any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) flags->bad_colidx = 1;
 }
 
 // hot vertices: the H highest-degree ones (sorted positions n - H .. n - 1) -> column bitmap
@@ -332,13 +309,17 @@ __global__ void k_ov_keys(const int4* __restrict__ desc, int64_t nb_small, int64
     idx[i] = (int32_t)i;
 }
 
-// Introspection (agcn_plan_copy(AGCN_FIELD_SORTED_COLIDX)): the plan's sorted colidx with the
-// hot encoding undone.
-__global__ void k_decode_hot(const int32_t* __restrict__ sc, int64_t nnz, const int32_t* __restrict__ hot_cols,
-                             int32_t* __restrict__ out) {
-    for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < nnz; q += (int64_t)gridDim.x * blockDim.x) {
-        const int32_t c = sc[q];
-        out[q] = c >= 0 ? c : hot_cols[-1 - c];
+// Introspection (agcn_plan_copy(AGCN_FIELD_SORTED_COLIDX)): the colidx of the degree-sorted
+// CSR, gathered on demand from the plan's copy (one warp per sorted row), hot encoding undone.
+__global__ void k_gather_sorted_cols(int64_t n, const int32_t* __restrict__ sorted_rowptr,
+                                     const int32_t* __restrict__ rso, const int32_t* __restrict__ cols,
+                                     const int32_t* __restrict__ hot_cols, int32_t* __restrict__ out) {
+    const int64_t k = (int64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+    if (k >= n) return;
+    const int32_t dst = sorted_rowptr[k], d = sorted_rowptr[k + 1] - dst, src = rso[k];
+    for (int32_t j = threadIdx.x & 31; j < d; j += 32) {
+        const int32_t c = cols[src + j];
+        out[dst + j] = c >= 0 ? c : hot_cols[-1 - c];
     }
 }
 
@@ -546,11 +527,11 @@ void build_ov_order(agcn_plan_s* p, int32_t buckets, cudaStream_t s) {
     AGCN_CUDA(cudaMemcpyAsync(p->ov_order, va, sizeof(int32_t) * m, cudaMemcpyDeviceToDevice, s));
 }
 
-// BLOCK plan, after the descriptors: the degree-sorted colidx (P:295 (3)) with the hot encoding;
+// BLOCK plan, after the degree order: the plan's colidx copy with the hot encoding;
 // d_flags != NULL: validate the column range on the way (read back by the caller).
-void build_sorted_cols(agcn_plan_s* p, const int32_t* colidx, const agcn_opts_t& o, cudaStream_t s,
-                       PlanFlags* d_flags = nullptr) {
-    p->scols = dalloc<int32_t>(p->nnz, s);
+void build_cols(agcn_plan_s* p, const int32_t* colidx, const agcn_opts_t& o, cudaStream_t s,
+                PlanFlags* d_flags = nullptr) {
+    p->cols_copy = dalloc<int32_t>(p->nnz, s);
     p->device_bytes += sizeof(int32_t) * (size_t)p->nnz;
     p->n_hot = hot_rows_for(p, o.hot_rows);
     Scratch tmp(s);
@@ -570,10 +551,9 @@ void build_sorted_cols(agcn_plan_s* p, const int32_t* colidx, const agcn_opts_t&
         k_hot_list<<<blocks_for(nw, 256), 256, 0, s>>>(hot, pre, nw, p->hot_cols);
         post_launch();
     }
-    if (p->nnz == 0 || p->nblocks == 0) return;
-    const unsigned g = (unsigned)std::min<int64_t>(blocks_for(p->nblocks, kWarps), 148 * 8);
-    k_sorted_cols<<<g, kThreads, 0, s>>>(p->desc, p->nblocks, p->deg_bound, p->sorted_rowptr, p->row_src_off,
-                                         colidx + p->rp_base, p->n_cols, p->cmap, hot, p->scols, d_flags);
+    if (p->nnz == 0) return;
+    const unsigned g = (unsigned)std::min<int64_t>(blocks_for(p->nnz, 256 * 4), (int64_t)num_sms() * 8);
+    k_copy_cols_enc<<<g, 256, 0, s>>>(colidx + p->rp_base, p->nnz, p->n_cols, p->cmap, hot, p->cols_copy, d_flags);
     post_launch();
 }
 
@@ -943,7 +923,7 @@ bool build_block_plan_small(agcn_plan_s* p, const int32_t* rowptr, const int32_t
     p->nb_small = h.nb_small;
     p->nblocks = h.nb_small + h.ov_chunks;
     p->device_bytes = sizeof(int32_t) * (size_t)(3 * n + 1 + ovc_cap) + sizeof(int4) * (size_t)desc_cap;
-    build_sorted_cols(p, colidx, o, s);
+    build_cols(p, colidx, o, s);
     build_ov_order(p, o.chunk_buckets, s);
     return true;
 }
@@ -1090,7 +1070,7 @@ void build_block_plan(agcn_plan_s* p, const int32_t* rowptr, const int32_t* coli
         AGCN_CUDA(cudaMemsetAsync(p->ov_chunk_start, 0, sizeof(int32_t), s));
     }
 
-    build_sorted_cols(p, colidx, o, s, o.validate ? d_flags : nullptr);
+    build_cols(p, colidx, o, s, o.validate ? d_flags : nullptr);
     build_ov_order(p, o.chunk_buckets, s);
     if (o.validate && nnz > 0) {  // the plan's second (and last) synchronisation: colidx range
         int32_t* pin = static_cast<int32_t*>(pinned_staging(sizeof(int32_t)));
@@ -1139,7 +1119,7 @@ void build_warp_plan(agcn_plan_s* p, const int32_t* rowptr, const int32_t* colid
 void free_plan_arrays(agcn_plan_s* p) {
     void* ptrs[] = {p->perm,  p->sorted_rowptr, p->row_src_off, p->desc,       p->ov_chunk_start,
                     p->tasks, p->rowptr_copy,   p->cols_copy,   p->ov_partial, p->ov_cnt,
-                    p->scols, p->xhot, p->hot_cols, p->ov_order};
+                    p->xhot, p->hot_cols, p->ov_order};
     // Stream-ordered release on the plan's stream, after the last SpMM that used the plan on
     // another stream (p->last_use); no host synchronisation.
     if (p->last_use) cudaStreamWaitEvent(p->stream, p->last_use, 0);
@@ -1155,9 +1135,11 @@ void plan_copy_sorted_colidx(agcn_plan_s* p, int32_t* host_dst) {
     cudaStream_t s = p->stream;
     Scratch tmp(s);
     int32_t* d = tmp.alloc<int32_t>(p->nnz);
-    k_decode_hot<<<(unsigned)std::min<int64_t>(blocks_for(p->nnz, 256), 148 * 16), 256, 0, s>>>(
-        p->scols, p->nnz, p->hot_cols, d);
-    post_launch();
+    if (p->n > 0) {
+        k_gather_sorted_cols<<<blocks_for(p->n, kWarps), kThreads, 0, s>>>(p->n, p->sorted_rowptr, p->row_src_off,
+                                                                        p->cols_copy, p->hot_cols, d);
+        post_launch();
+    }
     AGCN_CUDA(cudaMemcpyAsync(host_dst, d, sizeof(int32_t) * p->nnz, cudaMemcpyDeviceToHost, s));
     AGCN_CUDA(cudaStreamSynchronize(s));
 }

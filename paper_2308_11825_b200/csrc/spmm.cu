@@ -9,9 +9,9 @@
 //    lanes with float4 loads (L*T float4 = the paper's round_dim, lanes past F truncated,
 //    P:493); a warp holds G = 32/L such "combined warps" (sub-warps), which split the
 //    descriptor's contiguous nonzeros evenly (per-sub-warp nnz differ by at most 4).
-//  * The descriptor's colidx (the plan's degree-sorted copy: contiguous from loc) and vals
-//    (one contiguous run per row of the caller's array, via row_src_off) are staged in shared
-//    memory once per descriptor.  Hot columns (-1 - slot) read the plan's compact hot rows.
+//  * The descriptor's colidx (the plan's copy) and vals (the caller's array), one contiguous
+//    run per row at row_src_off, are staged in shared memory once per descriptor.  Hot columns
+//    (-1 - slot) read the plan's compact hot rows.
 //  * Three-level accumulation made deterministic: (1) registers, (2) the
 //    partial rows of sub-warps that share a row are merged in fixed sub-warp order through
 //    shared memory (replaces atomicAdd_block), (3) rows with degree > deg_bound are split
@@ -99,7 +99,7 @@ struct BlockArgs {
     int32_t db;             // deg_bound
     int32_t stage;          // shared-memory entries per warp (>= db + 8, multiple of 4)
     int32_t rso_stage;      // shared-memory row offsets per warp (>= max_block_warps)
-    const int32_t* scols;   // the plan's degree-sorted colidx (hot columns -1 - slot)
+    const int32_t* cols;    // the plan's colidx copy, indexed like vals (hot columns -1 - slot)
     const int32_t* srp;     // sorted rowptr
     const int32_t* rso;     // row_src_off
     const int32_t* perm;    // sorted -> original row
@@ -173,7 +173,7 @@ __global__ void __launch_bounds__(kCtaThreads, 4) k_spmm_block(const __grid_cons
                 const int32_t r = e / d;
                 off = s_rso[r] + (e - r * d);
             }
-            s_col[e] = ldcs_i(a.scols + (int64_t)loc + e);
+            s_col[e] = ldcs_i(a.cols + off);
             s_val[e] = ldcs_f(a.vals + off);
         }
         __syncwarp();
@@ -752,7 +752,7 @@ void spmm_launch(agcn_plan_s* p, const float* vals, const float* X, int32_t F, f
     a.db = p->deg_bound;
     a.stage = ((p->deg_bound + 3) & ~3) + 8;
     a.rso_stage = (p->mbw + 3) & ~3;
-    a.scols = p->scols;
+    a.cols = p->cols_copy;
     a.srp = p->sorted_rowptr;
     a.rso = p->row_src_off;
     a.perm = p->perm;

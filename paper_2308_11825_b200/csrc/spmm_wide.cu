@@ -17,9 +17,9 @@
 //    (rows with degree > deg_bound) writes per-chunk partial rows summed by k_ov_reduce.
 //  * the row offsets / output rows of the descriptor (<= 32 rows) are fetched once per
 //    descriptor, one per lane, and shuffled to the combined warps.
-//  * column indices come from the plan's degree-sorted copy (a descriptor's entries are the
-//    contiguous run from loc), vals from the caller's array through row_src_off, one batch of
-//    pairs ahead (prefetch), both through the read-only path (ld.global.nc).
+//  * column indices come from the plan's copy of colidx and vals from the caller's array, both
+//    indexed like the caller's CSR (a sorted row starts at row_src_off), one batch of pairs
+//    ahead (prefetch), through the read-only path (ld.global.nc).
 //  * X residency in L2 (agcn_l2_hint_t, template XM): 0 plain loads; 1 evict_last on every X
 //    row (X fits in L2); 2 the plan's hot columns (-1 - slot) read the compact hot buffer Xh --
 //    under the launch's persisting access-policy window in HOT_WINDOW mode; 3 as 2 with hot
@@ -93,7 +93,7 @@ struct WideArgs {
     int64_t n_desc;       // descriptors executed from desc (nblocks, or nb_small with pieces)
     int64_t first_ov;     // descriptor index of the first oversized chunk
     int64_t n_zero;       // sorted rows [0, n_zero) have degree 0
-    const int32_t* scols; // the plan's degree-sorted colidx (hot columns -1 - slot)
+    const int32_t* cols;  // the plan's colidx copy, indexed like vals (hot columns -1 - slot)
     const int32_t* srp;   // sorted rowptr
     const int32_t* rso;   // row_src_off
     const int32_t* perm;  // sorted -> original row
@@ -215,7 +215,6 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_wide(const __grid_const
         const bool ov = m.x > a.db;
         const int32_t R = ov ? 1 : (m.w & 0xffff);      // rows of the descriptor (<= 32)
         const int32_t d = ov ? m.w : m.x;               // nonzeros per row (chunk size if ov)
-        const int32_t cd = m.y;                         // the descriptor's column indices: scols[cd ..]
         // per-row data, one row per lane: where the row's entries start in the caller's vals
         // (P:295 step (3) row-pointer update), and its output row
         int32_t rso_l = 0, dst_l = 0;
@@ -250,7 +249,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_wide(const __grid_const
                 cc = 0;
                 vv = 0.f;
                 if (t < Ts) {
-                    cc = __ldg(a.scols + (uint32_t)(cd + r * d + j));
+                    cc = __ldg(a.cols + e);
                     vv = __ldg(a.vals + e);
                 }
             };
@@ -308,13 +307,12 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_wide(const __grid_const
             const bool gact = (FULL || g < NG) && r < R;           // idle groups / lanes: no work
             const int32_t mylen = gact ? len_k : 0;
             const int32_t e0 = __shfl_sync(0xffffffffu, rso_l, r & 31) + p0;  // first entry (vals)
-            const int32_t c0 = cd + (r * d + p0);                                // first entry (cols)
             acc.a = acc.b = make_float4(0.f, 0.f, 0.f, 0.f);
             // (colidx, val) pairs, L per batch, one per lane; the next batch is prefetched
             int32_t c = 0;
             float v = 0.f;
             if (li < mylen) {
-                c = __ldg(a.scols + (uint32_t)(c0 + li));
+                c = __ldg(a.cols + e0 + li);
                 v = __ldg(a.vals + e0 + li);
             }
             for (int32_t base = 0; base < part; base += L) {     // warp-uniform trip count
@@ -322,7 +320,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_wide(const __grid_const
                 int32_t cn = 0;
                 float vn = 0.f;
                 if (jn < mylen) {
-                    cn = __ldg(a.scols + (uint32_t)(c0 + jn));
+                    cn = __ldg(a.cols + e0 + jn);
                     vn = __ldg(a.vals + e0 + jn);
                 }
                 const int32_t nb = mylen - base;                 // valid pairs in this batch (may be <= 0)
@@ -410,14 +408,13 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_chunks(const __grid_con
         const int32_t part = (len + G - 1) / G;
         const int32_t p0 = s * part;
         const int32_t mylen = max(0, min(len - p0, part));
-        const uint32_t cb = (uint32_t)(m.y + p0);
         const int32_t vbb = vb + p0;
         f8 acc;
         acc.a = acc.b = make_float4(0.f, 0.f, 0.f, 0.f);
         int32_t c = 0;
         float v = 0.f;
         if (li < mylen) {
-            c = __ldg(a.scols + cb + li);
+            c = __ldg(a.cols + vbb + li);
             v = __ldg(a.vals + vbb + li);
         }
         for (int32_t base = 0; base < part; base += L) {  // warp-uniform trip count
@@ -425,7 +422,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_chunks(const __grid_con
             int32_t cn = 0;
             float vn = 0.f;
             if (jn < mylen) {
-                cn = __ldg(a.scols + cb + jn);
+                cn = __ldg(a.cols + vbb + jn);
                 vn = __ldg(a.vals + vbb + jn);
             }
             const int32_t nb = mylen - base;
@@ -570,7 +567,7 @@ bool wide_supported(const agcn_plan_s* p, const float* X, const float* Y, int32_
 void launch_wide(agcn_plan_s* p, const float* vals, const float* X, const float* Xh, int32_t F, float* Y,
                  int l2, size_t win, bool fuse_ov, int chunk_shape, bool chunk_order, const Epi& epi,
                  cudaStream_t s) {
-    WideArgs a{p->desc, p->nblocks, p->nb_small, p->n_zero, p->scols, p->sorted_rowptr, p->row_src_off,
+    WideArgs a{p->desc, p->nblocks, p->nb_small, p->n_zero, p->cols_copy, p->sorted_rowptr, p->row_src_off,
                p->perm, vals + p->rp_base, X, Xh, Y, p->ov_partial, chunk_order ? p->ov_order : nullptr,
                p->deg_bound, epi};
     AGCN_CHECK(a.n_desc < (1ll << 31), AGCN_ERR_OVERFLOW, "too many descriptors");
