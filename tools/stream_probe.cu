@@ -48,7 +48,8 @@ __device__ __forceinline__ void fma8(f8& acc, float v, const f8& x) {
 template <int U, int MINB, bool ENC, bool HINTS, bool VALS, bool STORE>
 __global__ void __launch_bounds__(256, MINB)
     k_stream(const float* __restrict__ X, const float* __restrict__ Xh, const int* __restrict__ idx,
-             const float* __restrict__ vals, int64_t n, int CH, float* __restrict__ out, int64_t out_rows) {
+             const float* __restrict__ vals, int64_t n, int CH, float* __restrict__ out, int64_t out_rows,
+             int64_t zero_rows) {
     const int lane = threadIdx.x & 31, s = lane >> 3, li = lane & 7;
     const int64_t gw = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5), W = (int64_t)gridDim.x * 8;
     const int part = CH / 4;
@@ -104,6 +105,14 @@ __global__ void __launch_bounds__(256, MINB)
             acc.a = acc.b = make_float4(0.f, 0.f, 0.f, 0.f);
         }
     }
+    if (STORE) {  // the rest of the output rows (the SpMM's zero rows), after the stream
+        const int64_t done = ((n + CH - 1) / CH) * 4;
+        for (int64_t r = done + gw * 4 + s; r < done + zero_rows; r += W * 4) {
+            float* o = out + (r % out_rows) * 64 + li * 8;
+            __stcs(reinterpret_cast<float4*>(o), make_float4(0.f, 0.f, 0.f, 0.f));
+            __stcs(reinterpret_cast<float4*>(o) + 1, make_float4(0.f, 0.f, 0.f, 0.f));
+        }
+    }
     if (!STORE) {  // keep the loads alive
         float t = acc.a.x + acc.a.y + acc.a.z + acc.a.w + acc.b.x + acc.b.y + acc.b.z + acc.b.w;
         if (t == 123.456f) out[0] = t;
@@ -112,13 +121,13 @@ __global__ void __launch_bounds__(256, MINB)
 
 template <int U, int MINB, bool ENC, bool HINTS, bool VALS, bool STORE>
 int run_t(const float* X, const float* Xh, const int* idx, const float* vals, int64_t n, int CH, float* out,
-          int64_t out_rows, cudaStream_t st) {
+          int64_t out_rows, cudaStream_t st, int64_t zero_rows = 0) {
     auto k = k_stream<U, MINB, ENC, HINTS, VALS, STORE>;
     int occ = 0, sms = 0, dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, 256, 0);
-    k<<<sms * occ, 256, 0, st>>>(X, Xh, idx, vals, n, CH, out, out_rows);
+    k<<<sms * occ, 256, 0, st>>>(X, Xh, idx, vals, n, CH, out, out_rows, zero_rows);
     return cudaGetLastError() == cudaSuccess ? occ : -1;
 }
 
@@ -152,6 +161,15 @@ extern "C" int probe_stream(int shape, int enc, int hints, int vals_store, const
         case 4: return run_u<2, 8>(enc, hints, vals_store, X, Xh, idx, vals, n, CH, out, out_rows, st);
         default: return run_u<4, 3>(enc, hints, vals_store, X, Xh, idx, vals, n, CH, out, out_rows, st);
     }
+}
+
+// the kernel-matched variant: U 4 at 3 CTAs/SM, hot/cold hints, vals stream, output-row stores
+// plus `zero_rows` more zero rows after the stream (the SpMM's degree-0 rows)
+extern "C" int probe_stream_full(const float* X, const float* Xh, const int* idx, const float* vals, int64_t n,
+                                 int CH, float* out, int64_t out_rows, int64_t zero_rows, int hints, void* stream) {
+    cudaStream_t st = (cudaStream_t)stream;
+    return hints ? run_t<4, 3, true, true, true, true>(X, Xh, idx, vals, n, CH, out, out_rows, st, zero_rows)
+                 : run_t<4, 3, true, false, true, true>(X, Xh, idx, vals, n, CH, out, out_rows, st, zero_rows);
 }
 
 // persisting-L2 window over [base, base + bytes) on `stream` (hitRatio 1), after setting the
