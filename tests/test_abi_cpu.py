@@ -108,3 +108,24 @@ def test_product_package_does_not_import_oracle():
                 assert not re.search(r"^\s*(import|from)\s+oracle\b", txt, re.M), f
                 assert not re.search(r"#include\s+[<\"].*oracle", txt), f
                 assert "liboracle" not in txt and "agcn_inputs" not in txt, f
+
+
+def _build_c_example(out):
+    import subprocess
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    lib = os.path.dirname(A_lib_path())
+    cmd = ["gcc", "-O2", "-std=c11", "-Wall", "-Werror", os.path.join(root, "examples", "spmm_c.c"),
+           "-I", os.path.join(root, "include"), "-I", "/usr/local/cuda/include", "-L", lib, "-lagcn",
+           "-L", "/usr/local/cuda/lib64", "-lcudart", "-lm", f"-Wl,-rpath,{lib}:/usr/local/cuda/lib64", "-o", out]
+    return subprocess.run(cmd, capture_output=True, text=True)
+
+
+def A_lib_path():
+    import paper_2308_11825_b200 as A
+    return A.library_path()
+
+
+def test_c_example_compiles(tmp_path):
+    """examples/spmm_c.c: the C ABI used from plain C (gcc, include/agcn.h, libagcn.so)."""
+    r = _build_c_example(str(tmp_path / "spmm_c"))
+    assert r.returncode == 0, r.stderr

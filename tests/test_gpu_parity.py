@@ -809,3 +809,18 @@ def test_chunk_order_and_chunk_kernel(F):
                     Y = p.spmm(cu(vals), cu(X), kernel="wide", chunk_order=order, chunk_shape=shape).cpu().numpy()
                     assert np.array_equal(Y, Y0), (mbw, mwn, buckets, order, shape)
             ref = Y0
+
+
+def test_c_example_runs(tmp_path):
+    """examples/spmm_c.c on the GPU: plan + SpMM from plain C, checked against a double loop
+    (north_star tolerance), the caller's colidx freed after agcn_plan, and equal to
+    agcn_propagate_host on host buffers."""
+    import subprocess
+    import sys
+    sys.path.insert(0, os.path.dirname(__file__))
+    from test_abi_cpu import _build_c_example
+    exe = str(tmp_path / "spmm_c")
+    r = _build_c_example(exe)
+    assert r.returncode == 0, r.stderr
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0 and r.stdout.startswith("ok"), r.stdout + r.stderr
