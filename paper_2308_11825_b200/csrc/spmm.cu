@@ -547,20 +547,36 @@ void launch_warp(const WarpArgs& a, cudaStream_t s) {
 }
 
 // Xh[k] = X[hot_cols[k]] for k < H: the hot rows (the H highest-degree vertices) in a compact
-// buffer, one warp per row (16-byte vectors when F % 4 == 0 and X is aligned)
+// buffer; one thread per 16-byte vector of the flattened [H][F / 4] output (fully coalesced
+// stores, row-contiguous loads), 4 vectors in flight per thread; scalar lanes when F % 4 != 0
 template <bool V4>
 __global__ void k_gather_hot(const float* __restrict__ X, const int32_t* __restrict__ hot_cols,
                              int64_t H, int32_t F, float* __restrict__ Xh) {
-    const int lane = threadIdx.x & 31;
-    const int64_t W = (int64_t)gridDim.x * (blockDim.x / 32);
-    for (int64_t k = (int64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5); k < H; k += W) {
-        const int64_t r = __ldg(hot_cols + k);
+    const int32_t FV = V4 ? F / 4 : F;
+    const int64_t total = H * FV, T = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i0 < total; i0 += 4 * T) {
         if (V4) {
-            const float4* src = reinterpret_cast<const float4*>(X + r * F);
-            float4* dst = reinterpret_cast<float4*>(Xh + k * F);
-            for (int32_t c = lane; c < F / 4; c += 32) dst[c] = __ldg(src + c);
+            float4 v[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int64_t i = i0 + u * T;
+                if (i < total) {
+                    const int64_t k = i / FV, c = i - k * FV;
+                    v[u] = __ldg(reinterpret_cast<const float4*>(X + (int64_t)__ldg(hot_cols + k) * F) + c);
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                if (i0 + u * T < total) reinterpret_cast<float4*>(Xh)[i0 + u * T] = v[u];
         } else {
-            for (int32_t c = lane; c < F; c += 32) Xh[k * F + c] = __ldg(X + r * F + c);
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int64_t i = i0 + u * T;
+                if (i < total) {
+                    const int64_t k = i / FV, c = i - k * FV;
+                    Xh[i] = __ldg(X + (int64_t)__ldg(hot_cols + k) * F + c);
+                }
+            }
         }
     }
 }
@@ -721,7 +737,8 @@ void spmm_launch(agcn_plan_s* p, const float* vals, const float* X, int32_t F, f
             AGCN_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p->xhot), hneed * sizeof(float), s));
             p->xhot_floats = hneed;
         }
-        const unsigned g = (unsigned)std::min<int64_t>((p->n_hot + 7) / 8, (int64_t)num_sms() * 16);
+        const int64_t vec = p->n_hot * (v4 ? F / 4 : F);
+        const unsigned g = (unsigned)std::max<int64_t>(1, std::min<int64_t>((vec + 1023) / 1024, (int64_t)num_sms() * 8));
         if (v4)
             k_gather_hot<true><<<g, 256, 0, s>>>(X, p->hot_cols, p->n_hot, F, p->xhot);
         else
