@@ -78,11 +78,13 @@ class ShardLayout:
         return (q * self.slot_rows + (colidx - self.bounds[q])).astype(np.int64)
 
 
-def propagate(layout: ShardLayout, spmm, X0, bufs, layers: int, all_gather=None):
+def propagate(layout: ShardLayout, spmm, X0, bufs, layers: int, all_gather=None, final_gather: bool = False):
     """Run `layers` propagation layers.
 
     spmm(Xin_padded, out_rows) computes this rank's rows of A.Xin into out_rows (a view of
-    this rank's slot); all_gather(full_buf, slot_view) fills every slot (in place).
+    this rank's slot); all_gather(full_buf, slot_view) fills every slot (in place) BETWEEN
+    layers (the next layer reads every rank's rows); the last layer's output stays row-sharded
+    (each rank holds its own rows) unless final_gather.
     bufs: list of padded buffers to rotate through (>= 1, must not include X0).
     Returns the padded buffer holding the last layer's output.
     """
@@ -90,7 +92,7 @@ def propagate(layout: ShardLayout, spmm, X0, bufs, layers: int, all_gather=None)
     for layer in range(layers):
         nxt = bufs[layer % len(bufs)]
         spmm(cur, layout.own_rows(nxt))
-        if all_gather is not None and layout.P > 1:
+        if all_gather is not None and layout.P > 1 and (layer < layers - 1 or final_gather):
             all_gather(nxt, layout.slot(nxt))
         cur = nxt
     return cur
@@ -128,7 +130,8 @@ def join_columns(chunks):
     return torch.cat(chunks, 1)
 
 
-def propagate_chunked(layout: ShardLayout, spmm, X0_chunks, bufs_chunks, layers: int, all_gather_async=None):
+def propagate_chunked(layout: ShardLayout, spmm, X0_chunks, bufs_chunks, layers: int, all_gather_async=None,
+                      final_gather: bool = False):
     """Column-chunked propagation with the all-gather of chunk k overlapping the SpMM of chunk
     k + 1.  The SpMM is column-separable -- (A X)[:, c] = A X[:, c] -- so every
     layer runs as K narrower SpMMs over contiguous chunk buffers ([P*S, w_k] each, the chunk-
@@ -142,8 +145,9 @@ def propagate_chunked(layout: ShardLayout, spmm, X0_chunks, bufs_chunks, layers:
     spmm(Xin_chunk, out_rows_chunk) as in ``propagate``; all_gather_async(full, slot) starts an
     in-place all-gather and returns a handle with .wait() (device-side ordering of the current
     stream after the collective, e.g. torch.distributed async work); None for one rank.
-    bufs_chunks: per chunk a list of >= 1 padded buffers (not X0's).  Returns the list of the
-    last layer's chunk buffers; every pending all-gather has been waited for."""
+    bufs_chunks: per chunk a list of >= 1 padded buffers (not X0's).  The last layer's output
+    stays row-sharded unless final_gather.  Returns the list of the last layer's chunk buffers;
+    every pending all-gather has been waited for."""
     K = len(X0_chunks)
     cur = list(X0_chunks)
     pending = [None] * K
@@ -154,7 +158,7 @@ def propagate_chunked(layout: ShardLayout, spmm, X0_chunks, bufs_chunks, layers:
                 pending[k].wait()
                 pending[k] = None
             spmm(cur[k], layout.own_rows(nxt[k]))
-            if all_gather_async is not None and layout.P > 1:
+            if all_gather_async is not None and layout.P > 1 and (layer < layers - 1 or final_gather):
                 pending[k] = all_gather_async(nxt[k], layout.slot(nxt[k]))
         cur = nxt
     for k in range(K):
@@ -245,15 +249,19 @@ class PeerBuffers:
             b.close()
 
 
-def propagate_fused(layout: ShardLayout, spmm, X0, peers: PeerBuffers, layers: int, barrier):
+def propagate_fused(layout: ShardLayout, spmm, X0, peers: PeerBuffers, layers: int, barrier,
+                    final_gather: bool = False):
     """``layers`` propagation layers with the fused all-gather: spmm(Xin, out_rows, peer_out)
-    writes this rank's rows locally and into every peer; ``barrier()`` orders the peers'
-    stores before the next layer reads them.  Returns the padded buffer of the last layer."""
+    writes this rank's rows locally and into every peer (not for the last layer unless
+    final_gather: its output stays row-sharded); ``barrier()`` orders the peers' stores before
+    the next layer reads them.  Returns the padded buffer of the last layer."""
     cur = X0
     nb = len(peers.local)
     for layer in range(layers):
         nxt = peers.tensor(layer % nb)
-        spmm(cur, layout.own_rows(nxt), peers.peer_out(layer % nb))
-        barrier()
+        last = layer == layers - 1 and not final_gather
+        spmm(cur, layout.own_rows(nxt), [] if last else peers.peer_out(layer % nb))
+        if not last:
+            barrier()
         cur = nxt
     return cur

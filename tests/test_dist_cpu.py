@@ -46,13 +46,16 @@ def _worker(rank, world, port, q):
             y, _ = oracle.spmm(rp, ci_relabel, w.vals, Xin.numpy(), with_abs=False)
             out_rows.copy_(torch.from_numpy(y.astype(np.float32)))
 
-        out = propagate(lay, spmm, X0, bufs, layers,
-                        lambda full, slot: dist.all_gather_into_tensor(full, slot.clone()))
+        ag = lambda full, slot: dist.all_gather_into_tensor(full, slot.clone())  # noqa: E731
+        out = propagate(lay, spmm, X0, bufs, layers, ag, final_gather=True)
         Y = lay.unpad(out).numpy()
+        # without the final all-gather (the bench's default): this rank's rows are the same
+        own = lay.own_rows(propagate(lay, spmm, X0, [torch.zeros_like(X0) for _ in range(2)], layers, ag)).numpy()
+        own_ok = bool(np.array_equal(own, Y[lay.lo:lay.hi]))
         if rank == 0:
             y1, _ = oracle.spmm(w.rowptr, w.colidx, w.vals, X, with_abs=False)
             y2, _ = oracle.spmm(w.rowptr, w.colidx, w.vals, y1.astype(np.float32), with_abs=False)
-            q.put(("ok", bool(np.array_equal(Y, y2.astype(np.float32))),
+            q.put(("ok", bool(np.array_equal(Y, y2.astype(np.float32))) and own_ok,
                    int(lay.slot_rows), bounds.tolist()))
     except Exception as e:  # pragma: no cover
         q.put(("err", repr(e), 0, []))
@@ -122,7 +125,7 @@ def _worker_chunked(rank, world, port, K, q):
             out_rows.copy_(torch.from_numpy(y.astype(np.float32)))
 
         ag = make_all_gather_async("gloo")
-        out = propagate_chunked(lay, spmm, X0c, bufs, layers, ag)
+        out = propagate_chunked(lay, spmm, X0c, bufs, layers, ag, final_gather=True)
         Y = lay.unpad(join_columns(out)).numpy()
         if rank == 0:
             ref = X

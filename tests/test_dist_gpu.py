@@ -77,7 +77,7 @@ def _worker(rank, world, port, F, q, fused=False):
                 torch.cuda.synchronize()
                 dist.barrier()
 
-            out = propagate_fused(lay, spmm_f, X0, peers, 2, barrier)
+            out = propagate_fused(lay, spmm_f, X0, peers, 2, barrier, final_gather=True)
         elif fused == "chunks":   # column chunks, all-gather of chunk k overlapping SpMM k+1
             from paper_2308_11825_b200.dist import (chunk_widths, join_columns, make_all_gather_async,
                                                     propagate_chunked, split_columns)
@@ -90,11 +90,11 @@ def _worker(rank, world, port, F, q, fused=False):
                 plan.spmm(va_d, Xin, out=out_rows)
                 seen.append(Xin)
 
-            outc = propagate_chunked(lay, spmm_c, X0c, bufs_c, 2, make_all_gather_async("gloo"))
+            outc = propagate_chunked(lay, spmm_c, X0c, bufs_c, 2, make_all_gather_async("gloo"), final_gather=True)
             out = join_columns(outc)
             layers_out = [join_columns(seen[:3]), join_columns(seen[3:6])]
         else:
-            out = propagate(lay, spmm, X0, bufs, 2, make_all_gather("gloo"))
+            out = propagate(lay, spmm, X0, bufs, 2, make_all_gather("gloo"), final_gather=True)
         torch.cuda.synchronize()
         if rank == 0:
             Y1 = lay.unpad(layers_out[1]).cpu().numpy()     # layer-2 input = layer-1 output
@@ -139,7 +139,7 @@ def test_bench_multi_rank_mode(fused):
     port = _free_port()
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
            "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.join(ROOT, "bench.py"),
-           "--gpus", "2", "--steps", "2", "--warmup", "3", "--config", "c3", "--dist-backend", "gloo",
+           "--gpus", "2", "--steps", "2", "--warmup", "3", "--config", "c3", "--layers", "2", "--dist-backend", "gloo",
            "--e2e-steps", "1"] + (["--fused-allgather"] if fused is True else []) + \
           (["--overlap-chunks", "2"] if fused == "chunks" else [])
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT)
