@@ -369,10 +369,10 @@ agcn_status_t agcn_gemm_xw(const float* X, int64_t M, int32_t K, const float* Wt
  *   AGCN_GEMM_FP32: fp32 accuracy, |y - y_ref| <= ~2^-19 sum_k |x_k w_k| + fp32 accumulation --
  *     "3xTF32" on the tcgen05 tensor cores: both operands split in shared memory into a TF32
  *     high part (low 13 mantissa bits cleared) and the exact remainder, x w accumulated as
- *     x_hi w_hi + x_lo w_hi + x_hi w_lo (three kind::tf32 MMAs per K step of 8) when
- *     N in {16, 32, 64, 128, 256} and the split W^T fits in shared memory (K * N <= 128 * 128
- *     class); otherwise a CUDA-core fp32 FFMA kernel.  K in [4, 256], K % 4 == 0;
- *     N in [4, 256], N % 4 == 0.
+ *     x_hi w_hi + x_lo w_hi + x_hi w_lo (three kind::tf32 MMAs per K step of 8) for
+ *     N in {16, 32, 64, 128, 256} (as column slices of W when the split W^T does not fit in
+ *     shared memory with the whole N); other N: a CUDA-core fp32 FFMA kernel.
+ *     K in [4, 256], K % 4 == 0; N in [4, 256], N % 4 == 0.
  *   AGCN_GEMM_TF32: as agcn_gemm_xw.
  * Same pointer / alignment rules as agcn_gemm_xw; asynchronous on `stream`.
  */

@@ -433,7 +433,8 @@ template <int N, int NSK, int CWT>
 __global__ void __launch_bounds__(kX3Threads, 1) k_gemm_3xtf32(const __grid_constant__ CUtensorMap tmX,
                                                               const __grid_constant__ CUtensorMap tmW,
                                                               float* __restrict__ Y, int64_t M, int32_t KT,
-                                                              const float* __restrict__ bias, int32_t relu) {
+                                                              const float* __restrict__ bias, int32_t relu,
+                                                              int64_t ldy) {
     constexpr uint32_t kAcc = N <= 32 ? 32 : N <= 64 ? 64 : N <= 128 ? 128 : 256;
     constexpr int kStage = kBM * kBK * 4;                      // one X k-stage (16 KB)
     extern __shared__ __align__(1024) unsigned char smem_raw[];
@@ -597,7 +598,7 @@ __global__ void __launch_bounds__(kX3Threads, 1) k_gemm_3xtf32(const __grid_cons
                 for (int e = lane; e < 32 * nv; e += 32) {
                     const int r = e / nv, c = e - r * nv;
                     if (row0 + r < M)
-                        __stcs(reinterpret_cast<float4*>(Y + (row0 + r) * N + cb) + c,
+                        __stcs(reinterpret_cast<float4*>(Y + (row0 + r) * ldy + cb) + c,
                                *reinterpret_cast<const float4*>(stg + r * SP + 4 * c));
                 }
                 __syncwarp();
@@ -615,8 +616,8 @@ __global__ void __launch_bounds__(kX3Threads, 1) k_gemm_3xtf32(const __grid_cons
 }
 
 // ---------------------------------------------------------------- fp32 on the CUDA cores
-// The fallback for shapes whose split W^T does not fit in shared memory next to the X ring
-// (K * N > 128 * 128): a plain fp32 FFMA kernel, one thread per (row, 4 consecutive columns),
+// The fallback for output widths that are not a tcgen05 N (16, 32, 64, 128, 256): a plain fp32
+// FFMA kernel, one thread per (row, 4 consecutive columns),
 // K-loop in order with fmaf (the arithmetic of a textbook fp32 GEMM, deterministic).  W^T rows
 // are read through the read-only cache; X rows are reused from L1 by the N / 4 threads of a row.
 __global__ void k_gemm_fp32_cc(const float* __restrict__ X, int64_t M, int32_t K, const float* __restrict__ Wt,
@@ -717,7 +718,7 @@ void launch_gemm(const CUtensorMap& mx, const CUtensorMap& mw, float* Y, int64_t
 
 template <int N, int NSK, int CWT>
 bool try_launch_3x(const CUtensorMap& mx, const CUtensorMap& mw, float* Y, int64_t M, int32_t KT, const float* bias,
-                   int32_t relu, cudaStream_t s) {
+                   int32_t relu, int64_t ldy, cudaStream_t s) {
     constexpr int CW = N < CWT ? N : CWT;
     const size_t smem = 1024 + (size_t)2 * NSK * kBM * kBK * 4 + (size_t)2 * KT * N * kBK * 4 + 256 +
                         (size_t)4 * 32 * (CW + 4) * 4;
@@ -726,17 +727,35 @@ bool try_launch_3x(const CUtensorMap& mx, const CUtensorMap& mw, float* Y, int64
     AGCN_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     const int64_t ntiles = (M + kBM - 1) / kBM;
     const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(ntiles, (int64_t)num_sms()));
-    kern<<<(unsigned)grid, kX3Threads, smem, s>>>(mx, mw, Y, M, KT, bias, relu);
+    kern<<<(unsigned)grid, kX3Threads, smem, s>>>(mx, mw, Y, M, KT, bias, relu, ldy);
     post_launch();
     return true;
 }
 
 template <int N>
 bool launch_3x(const CUtensorMap& mx, const CUtensorMap& mw, float* Y, int64_t M, int32_t KT, const float* bias,
-               int32_t relu, cudaStream_t s) {
-    return try_launch_3x<N, 4, 64>(mx, mw, Y, M, KT, bias, relu, s) ||
-           try_launch_3x<N, 3, 32>(mx, mw, Y, M, KT, bias, relu, s) ||
-           try_launch_3x<N, 2, 32>(mx, mw, Y, M, KT, bias, relu, s);
+               int32_t relu, int64_t ldy, cudaStream_t s) {
+    return try_launch_3x<N, 4, 64>(mx, mw, Y, M, KT, bias, relu, ldy, s) ||
+           try_launch_3x<N, 3, 32>(mx, mw, Y, M, KT, bias, relu, ldy, s) ||
+           try_launch_3x<N, 2, 32>(mx, mw, Y, M, KT, bias, relu, ldy, s);
+}
+
+// Y[:, n0 : n0 + Ns] for one power-of-two slice width Ns (W^T rows n0 .. n0 + Ns: contiguous)
+bool launch_3x_slice(const float* X, int64_t M, int32_t K, const float* Wt, int32_t Ns, int32_t n0, float* Y,
+                     int32_t N, const float* bias, int32_t relu, cudaStream_t s) {
+    const int32_t KT = (K + kBK - 1) / kBK;
+    const CUtensorMap mx = make_map(X, M, K, kBM);
+    const CUtensorMap mw = make_map(Wt + (int64_t)n0 * K, Ns, K, (uint32_t)Ns);
+    float* y = Y + n0;
+    const float* b = bias ? bias + n0 : nullptr;
+    switch (Ns) {
+        case 16: return launch_3x<16>(mx, mw, y, M, KT, b, relu, N, s);
+        case 32: return launch_3x<32>(mx, mw, y, M, KT, b, relu, N, s);
+        case 64: return launch_3x<64>(mx, mw, y, M, KT, b, relu, N, s);
+        case 128: return launch_3x<128>(mx, mw, y, M, KT, b, relu, N, s);
+        case 256: return launch_3x<256>(mx, mw, y, M, KT, b, relu, N, s);
+        default: return false;
+    }
 }
 
 }  // namespace
@@ -749,17 +768,18 @@ void gemm_xw_fp32(const float* X, int64_t M, int32_t K, const float* Wt, int32_t
     AGCN_CHECK(((reinterpret_cast<uintptr_t>(X) | reinterpret_cast<uintptr_t>(Wt) | reinterpret_cast<uintptr_t>(Y)) & 15u) == 0,
                AGCN_ERR_INVALID_ARG, "X, W^T and Y must be 16-byte aligned");
     if (M == 0) return;
-    const int32_t KT = (K + kBK - 1) / kBK;
     bool done = false;
     if (N == 16 || N == 32 || N == 64 || N == 128 || N == 256) {
-        const CUtensorMap mx = make_map(X, M, K, kBM);
-        const CUtensorMap mw = make_map(Wt, N, K, (uint32_t)N);
-        switch (N) {
-            case 16: done = launch_3x<16>(mx, mw, Y, M, KT, bias, relu, s); break;
-            case 32: done = launch_3x<32>(mx, mw, Y, M, KT, bias, relu, s); break;
-            case 64: done = launch_3x<64>(mx, mw, Y, M, KT, bias, relu, s); break;
-            case 128: done = launch_3x<128>(mx, mw, Y, M, KT, bias, relu, s); break;
-            default: done = launch_3x<256>(mx, mw, Y, M, KT, bias, relu, s); break;
+        // one launch, or -- when the split W^T does not fit in shared memory next to the X ring --
+        // column slices of W (each re-reads X; the products are column-separable)
+        for (int32_t Ns = N; Ns >= 16 && !done; Ns /= 2) {
+            // probe the slice width with the first slice (a launch only happens if it fits)
+            if (!launch_3x_slice(X, M, K, Wt, Ns, 0, Y, N, bias, relu, s)) continue;
+            for (int32_t n0 = Ns; n0 < N; n0 += Ns) {
+                const bool ok = launch_3x_slice(X, M, K, Wt, Ns, n0, Y, N, bias, relu, s);
+                AGCN_CHECK(ok, AGCN_ERR_CUDA, "internal: 3xTF32 slice launch");
+            }
+            done = true;
         }
     }
     if (!done) {

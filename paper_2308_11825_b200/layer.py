@@ -5,8 +5,8 @@
 Every step runs in libagcn (no cuBLAS): the dense product X W on the tcgen05 tensor cores
 (agcn_gemm_xw_ex: TMA + tcgen05.mma + TMEM epilogue) -- precision="fp32" (default) splits both
 operands into TF32 high and low parts and accumulates x_hi w_hi + x_lo w_hi + x_hi w_lo
-("3xTF32", fp32 accuracy; a CUDA-core FFMA kernel for shapes whose split W does not fit in
-shared memory), precision="tf32" feeds the operands as TF32; the aggregation, the bias and the
+("3xTF32", fp32 accuracy; column slices of W for the widest shapes, a CUDA-core FFMA kernel
+for output widths that are not a tcgen05 N), precision="tf32" feeds the operands as TF32; the aggregation, the bias and the
 ReLU are the SpMM's fused epilogue or the GEMM's.  The order follows the smaller feature width
 (P:124 computes A'(XW); (A'X)W is the same product):
 
