@@ -40,6 +40,7 @@ def main():
     ap.add_argument("--hot-rows", type=int, default=None)
     ap.add_argument("--mbw", type=int, default=12)
     ap.add_argument("--mwn", type=int, default=32)
+    ap.add_argument("--classes", default=None, help="comma list of class names to run")
     args = ap.parse_args()
     dev = torch.device("cuda:0")
     w = agcn_inputs.make_config("c5")
@@ -50,6 +51,9 @@ def main():
     classes = [("all", 1, 1 << 30), ("zero rows only", 0, 0), ("deg 1-8", 1, 8), ("deg 9-32", 9, 32),
                ("deg 33-128", 33, 128), ("deg 129-384", 129, 384), ("deg 385-512", 385, 512), ("deg > 512", 513, 1 << 30)]
     tot = deg.sum()
+    if args.classes:
+        keep_names = set(args.classes.split(","))
+        classes = [c for c in classes if c[0] in keep_names]
     for name, lo, hi in classes:
         keep = (deg >= lo) & (deg <= hi)
         rp = np.zeros(n + 1, np.int64)
