@@ -102,7 +102,9 @@ typedef enum {
     AGCN_FIELD_SORTED_COLIDX = 2, /* int32[nnz]     colidx in degree-sorted row order (after relabel) */
     AGCN_FIELD_ROW_SRC_OFF = 3,   /* int32[n]       rowptr[perm[k]] - rowptr[0] */
     AGCN_FIELD_TASKS = 4,         /* uint32[4*ntasks] warp tasks (row, col, len, 0) */
-    AGCN_FIELD_SORTED_ROWPTR = 5  /* int32[n+1]     row pointer of the degree-sorted CSR */
+    AGCN_FIELD_SORTED_ROWPTR = 5, /* int32[n+1]     row pointer of the degree-sorted CSR */
+    AGCN_FIELD_HOT_COLS = 6       /* int32[hot_rows] the hot vertices (agcn_opts_t.hot_rows), ascending:
+                                     the columns whose X rows agcn_spmm reads from the compact buffer */
 } agcn_field_t;
 
 /* Fill *opts with the defaults above. */

@@ -144,7 +144,8 @@ class Plan:
         st = self.stats()
         shapes = {"perm": (st["n"],), "blocks": (st["nblocks"], 4),
                   "sorted_colidx": (st["nnz"],), "row_src_off": (st["n"],),
-                  "tasks": (st["ntasks"], 4), "sorted_rowptr": (st["n"] + 1,)}
+                  "tasks": (st["ntasks"], 4), "sorted_rowptr": (st["n"] + 1,),
+                  "hot_cols": (st["hot_rows"],)}
         dt = np.uint32 if field in ("blocks", "tasks") else np.int32
         out = np.zeros(shapes[field], dtype=dt)
         _check(_lib.lib().agcn_plan_copy(self.handle, FIELDS[field],

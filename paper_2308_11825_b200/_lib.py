@@ -12,7 +12,7 @@ c_i32, c_i64, c_u64, c_size, c_vp = (ctypes.c_int32, ctypes.c_int64, ctypes.c_ui
 STATUS = {0: "AGCN_OK", 1: "AGCN_ERR_INVALID_ARG", 2: "AGCN_ERR_BAD_CSR", 3: "AGCN_ERR_OOM",
           4: "AGCN_ERR_CUDA", 5: "AGCN_ERR_OVERFLOW", 6: "AGCN_ERR_UNSUPPORTED"}
 FIELDS = {"perm": 0, "blocks": 1, "sorted_colidx": 2, "row_src_off": 3, "tasks": 4,
-          "sorted_rowptr": 5}
+          "sorted_rowptr": 5, "hot_cols": 6}
 
 
 class Opts(ctypes.Structure):

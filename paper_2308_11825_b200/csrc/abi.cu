@@ -204,6 +204,7 @@ agcn_status_t agcn_plan_copy(agcn_plan_t plan, int32_t field, void* host_dst, si
             case AGCN_FIELD_ROW_SRC_OFF: src = plan->row_src_off; want = 4 * (size_t)plan->n; break;
             case AGCN_FIELD_TASKS: src = plan->tasks; want = 16 * (size_t)plan->ntasks; break;
             case AGCN_FIELD_SORTED_ROWPTR: src = plan->sorted_rowptr; want = 4 * (size_t)(plan->n + 1); break;
+            case AGCN_FIELD_HOT_COLS: src = plan->hot_cols; want = 4 * (size_t)plan->n_hot; break;
             default: throw Error{AGCN_ERR_INVALID_ARG, "unknown field"};
         }
         const bool is_task = field == AGCN_FIELD_TASKS;

@@ -268,6 +268,35 @@ def test_hot_rows_every_mode(F):
                         assert np.array_equal(Y, Y0), (H, kernel, l2, hot_mb)
 
 
+@pytest.mark.parametrize("seed", [0, 1, 2])
+def test_hot_set_is_the_degree_tail(seed):
+    """The hot set (agcn_opts_t.hot_rows, reading Q35) is exactly the tail of the oracle's
+    stable degree order (the H largest (degree, row) keys), on both plan paths and for every H,
+    including H among the oversized rows and ties inside a degree bucket.  Metadata, the decoded
+    colidx copy and the SpMM are bitwise the same for every H."""
+    rowptr, colidx, vals, X = _hub_graph(5000 + 777 * seed, 30 + seed, 64)
+    n = rowptr.size - 1
+    deg = np.diff(rowptr)
+    live = int((deg > 0).sum())
+    o = oracle.plan(rowptr, colidx, 4, 8)                  # deg_bound 32: many oversized rows
+    n_ov = int((deg > 32).sum())
+    assert 1 < n_ov < live
+    Y0 = None
+    for H in (1, n_ov - 1, n_ov, n_ov + 1, n_ov + 37, live - 1, live, 10 ** 9):
+        want = np.sort(o["perm"][n - min(H, live):])
+        for small in (True, False):
+            p = make_plan(rowptr, colidx, max_block_warps=4, max_warp_nzs=8, hot_rows=H, small_plan=small)
+            assert p.stats()["hot_rows"] == min(H, live)
+            assert np.array_equal(p.copy("hot_cols"), want), (H, small)
+            assert np.array_equal(p.copy("perm"), o["perm"])
+            assert np.array_equal(p.copy("blocks"), o["blocks"])
+            assert np.array_equal(p.copy("sorted_colidx"), o["sorted_colidx"])
+            Y = p.spmm(cu(vals), cu(X)).cpu().numpy()
+            if Y0 is None:
+                Y0 = check_spmm(p, rowptr, colidx, vals, X, Y)
+            assert np.array_equal(Y, Y0), (H, small)
+
+
 def test_hot_rows_auto_rule():
     """hot_rows = -1: on for square graphs with n >= 2^19, off otherwise and for padded layouts."""
     rowptr = np.zeros(2 ** 19 + 1, dtype=np.int32)
