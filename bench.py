@@ -291,17 +291,24 @@ def cpu_model() -> str:
     return "unknown"
 
 
-def graph_protocol(A, torch, dev, w, F, rp, ci, va, X, scratch, hbm_gbs, plan_kw, reps=10, cpu=False):
+def _pct(xs, q):
+    """q-th percentile (nearest rank) of the samples xs."""
+    xs = sorted(xs)
+    return xs[min(len(xs) - 1, max(0, int(round(q / 100.0 * (len(xs) - 1)))))]
+
+
+def graph_protocol(A, torch, dev, w, F, rp, ci, va, X, scratch, hbm_gbs, plan_kw, reps=20, cpu=False):
     """The measurement protocol of SURVEY.md 8(d4) for one graph (kernel time,
     preprocessing excluded, against cuSPARSE):
       * agcn_spmm COLD (primary, Nsight Compute's cache control): 512 MB scratch written and
         persisting L2 reset before every rep, CUDA events around one agcn_spmm call;
-      * agcn_spmm WARM: 20 calls captured in one CUDA graph, replayed (no launch gaps);
+      * agcn_spmm WARM: 20 calls captured in one CUDA graph, replayed 10 times (no launch gaps);
+        a sample = one replay / 20;
       * cusparseSpMM directly (baseline/cusparse_spmm.cu) for ALG_DEFAULT and CSR_ALG1/2/3,
         bufferSize + preprocess outside timing, the same cold / warm reps; its output is
         checked against the fp64 oracle on a row sample; speedups against the best algorithm;
       * cpu=True (C1, C2): the oracle on 1 thread and on all host cores (full layer).
-    Medians over `reps`."""
+    Medians (and p10 / p90) over `reps` (>= 20)."""
     import baseline
     import oracle
     ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
@@ -337,20 +344,24 @@ def graph_protocol(A, torch, dev, w, F, rp, ci, va, X, scratch, hbm_gbs, plan_kw
             run()
     g.replay()
     torch.cuda.synchronize()
-    a, b = ev(), ev()
-    with torch.cuda.stream(S):
-        a.record(S)
-        for _ in range(3):
+    warms = []
+    for _ in range(10):
+        a, b = ev(), ev()
+        with torch.cuda.stream(S):
+            a.record(S)
             g.replay()
-        b.record(S)
-    torch.cuda.synchronize()
-    warm = a.elapsed_time(b) / 60
+            b.record(S)
+        b.synchronize()
+        warms.append(a.elapsed_time(b) / 20)
+    warm = statistics.median(warms)
     del g
     cold_ms = statistics.median(cold)
     bc = 4 * (n + 1) + 8 * nnz + 8 * n * F
     row = {"n": n, "nnz": nnz, "F": F, "max_block_warps": st["max_block_warps"],
            "max_warp_nzs": st["max_warp_nzs"], "hot_rows": st["hot_rows"], "plan_ms": plan_ms,
-           "cold_ms": cold_ms, "warm_ms": warm, "spmm_ms": cold_ms,
+           "cold_ms": cold_ms, "warm_ms": warm, "spmm_ms": cold_ms, "cold_reps": len(cold),
+           "cold_p10_ms": _pct(cold, 10), "cold_p90_ms": _pct(cold, 90),
+           "warm_p10_ms": _pct(warms, 10), "warm_p90_ms": _pct(warms, 90),
            "gflops_cold": 2.0 * nnz * F / (cold_ms * 1e-3) / 1e9,
            "b_comp_frac_of_hbm_cold": bc / (cold_ms * 1e-3) / 1e9 / hbm_gbs,
            "b_comp_frac_of_hbm_warm": bc / (warm * 1e-3) / 1e9 / hbm_gbs}
@@ -367,6 +378,7 @@ def graph_protocol(A, torch, dev, w, F, rp, ci, va, X, scratch, hbm_gbs, plan_kw
                 r = {"status": rc}
                 break
             r[f"{mode}_ms"] = statistics.median(ms)
+            r[f"{mode}_p10_ms"], r[f"{mode}_p90_ms"] = _pct(ms, 10), _pct(ms, 90)
             r["buffer_bytes"] = bb
         cs[alg] = r
         if "cold_ms" in r and (best is None or r["cold_ms"] < cs[best]["cold_ms"]):

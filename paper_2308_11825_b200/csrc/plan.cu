@@ -17,6 +17,7 @@
 #include <vector>
 
 #include "internal.h"
+#include "scan_lb.cuh"
 
 namespace agcn {
 namespace {
@@ -67,18 +68,37 @@ __global__ void __launch_bounds__(kThreads) k_deg_hist(const int32_t* __restrict
         ovh += __shfl_xor_sync(0xffffffffu, ovh, o);
         nhv += __shfl_xor_sync(0xffffffffu, nhv, o);
     }
+    // per-CTA totals first: one set of global atomics per CTA, not per warp (C5: 4096 CTAs x 8
+    // warps on the same few addresses serialised the kernel)
+    __shared__ long long s_ov[2][kWarps];
+    __shared__ int32_t s_i[3][kWarps];
+    const int wi = threadIdx.x >> 5;
     if ((threadIdx.x & 31) == 0) {
+        s_ov[0][wi] = ovc;
+        s_ov[1][wi] = ovh;
+        s_i[0][wi] = maxd;
+        s_i[1][wi] = bad;
+        s_i[2][wi] = nhv;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int k = 1; k < kWarps; ++k) {
+            ovc += s_ov[0][k];
+            ovh += s_ov[1][k];
+            maxd = max(maxd, s_i[0][k]);
+            bad |= s_i[1][k];
+            nhv += s_i[2][k];
+        }
         if (maxd) atomicMax(&flags->max_deg, maxd);
         if (bad) flags->bad_rowptr = 1;
         if (ovc) atomicAdd((unsigned long long*)&flags->ov_chunks, (unsigned long long)ovc);
         if (ovh) atomicAdd((unsigned long long*)&flags->ov_chunks_heavy, (unsigned long long)ovh);
         if (nhv) atomicAdd(&flags->n_ov_heavy, nhv);
+        if (blockIdx.x == 0) {
+            flags->rowptr_first = rowptr[0];
+            flags->rowptr_last = rowptr[n];
+        }
     }
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
-        flags->rowptr_first = rowptr[0];
-        flags->rowptr_last = rowptr[n];
-    }
-    __syncthreads();
     for (int b = threadIdx.x; b < nbins; b += kThreads) table[(int64_t)b * ntiles + blockIdx.x] = hist[b];
 }
 
@@ -180,16 +200,20 @@ __global__ void k_ov_init(const int32_t* __restrict__ perm_ov, const int32_t* __
 }
 
 // ---------------------------------------------------------------- (3) sorted CSR
-__global__ void k_sorted_rows(const int32_t* __restrict__ perm, const int32_t* __restrict__ rowptr,
-                              int64_t n, int32_t* __restrict__ sdeg, int32_t* __restrict__ rso) {
-    int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (k < n) {
-        int32_t r = perm[k];
-        int32_t a = rowptr[r];
-        sdeg[k] = rowptr[r + 1] - a;
-        rso[k] = a - rowptr[0];
+// Element k of the sorted-rowptr scan: the degree of sorted row k; on the way, where that row
+// starts in the caller's arrays (row_src_off).  The scan (scan_lb.cuh) turns the sorted degrees
+// into sorted_rowptr in the same pass.
+struct SortedRowsSrc {
+    const int32_t* perm;
+    const int32_t* rowptr;
+    int32_t* rso;
+    __device__ __forceinline__ int32_t get(int64_t k) const {
+        const int32_t r = __ldg(perm + k);
+        const int32_t a = __ldg(rowptr + r);
+        rso[k] = a - __ldg(rowptr);
+        return __ldg(rowptr + r + 1) - a;
     }
-}
+};
 
 // Bucket tables for degrees 1..db (index db+1 = end sentinel), in shared memory.
 struct BinTables {
@@ -1040,11 +1064,12 @@ void build_block_plan(agcn_plan_s* p, const int32_t* rowptr, const int32_t* coli
     // sorted degrees -> sorted_rowptr (scan) and row_src_off (where each sorted row starts in
     // the caller's colidx / vals); the sorted colidx is copied after the descriptors.
     if (n > 0) {
-        k_sorted_rows<<<blocks_for(n, 256), 256, 0, s>>>(p->perm, rowptr, n, p->sorted_rowptr,
-                                                          p->row_src_off);
-        post_launch();
+        const int64_t nt = (n + kLbTile - 1) / kLbTile;
+        launch_scan_lb(SortedRowsSrc{p->perm, rowptr, p->row_src_off}, p->sorted_rowptr, n,
+                       nt > 1 ? tmp.alloc<unsigned long long>(nt + 1) : nullptr, s);
+    } else {
+        AGCN_CUDA(cudaMemsetAsync(p->sorted_rowptr, 0, sizeof(int32_t), s));
     }
-    exclusive_scan_i32(p->sorted_rowptr, p->sorted_rowptr, n, s);
 
     // (4)+(5) Algorithm 1/2 descriptors
     int32_t* d_tab = tmp.alloc<int32_t>(6 * W);

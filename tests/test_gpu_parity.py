@@ -122,6 +122,18 @@ def _rows_csr(degs, n_cols, seed=0):
     return rowptr, colidx
 
 
+@pytest.mark.parametrize("n", [1, 4095, 4096, 4097, 32 * 4096, 33 * 4096 + 1, 300001])
+def test_scan_tile_boundaries(n):
+    """The plan's single-pass look-back scans (bucket table, sorted rowptr fused with
+    row_src_off, chunk starts) at lengths around the 4096-element tile and beyond the 32-tile
+    look-back window: metadata bit-exact against the oracle on the general plan."""
+    rng = np.random.default_rng(n)
+    degs = rng.integers(0, 6, n)
+    degs[rng.integers(0, n, 3)] = [900, 400, 5000]
+    rowptr, colidx = _rows_csr(degs, 777, n)
+    check_plan_vs_oracle(rowptr, colidx, n_cols=777, small_plan=False)
+
+
 @pytest.mark.parametrize("degs", [
     [384], [383], [385], [768], [769], [384 * 5, 1, 0, 384 * 5 + 7],   # around deg_bound
     [0, 0, 0], [0], [70000, 3, 0, 65536, 65537],                        # zero rows, deg >= 2^16
