@@ -104,10 +104,18 @@ def build_hash() -> str:
 
 
 def git_sha() -> str | None:
+    """HEAD of the repo: `git rev-parse` where .git exists, else the `.git_sha` file a post-commit
+    hook writes at the repo root (the GPU box gets the tree without .git)."""
     try:
-        return subprocess.run(["git", "-C", ROOT, "rev-parse", "HEAD"], capture_output=True, text=True,
-                              timeout=10).stdout.strip() or None
+        sha = subprocess.run(["git", "-C", ROOT, "rev-parse", "HEAD"], capture_output=True, text=True,
+                             timeout=10).stdout.strip()
+        if sha:
+            return sha
     except Exception:
+        pass
+    try:
+        return open(os.path.join(ROOT, ".git_sha")).read().strip() or None
+    except OSError:
         return None
 
 
