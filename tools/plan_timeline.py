@@ -53,3 +53,12 @@ for e in evs:
     busy += d
     prev_end = max(prev_end, e.time_range.end)
 print(f"span {prev_end - t0:.1f} us, busy {busy:.1f} us, idle {prev_end - t0 - busy:.1f} us, {len(evs)} activities")
+# host side: CUDA runtime API calls (CUPTI callbacks) on the same clock
+api = [e for e in prof.events() if e.device_type == torch.autograd.DeviceType.CPU and e.name.startswith("cuda")]
+api.sort(key=lambda e: e.time_range.start)
+print(f"\nhost runtime API calls ({len(api)}), start relative to the first GPU activity:")
+print(f"{'start_us':>9} {'dur_us':>8}  name")
+for e in api:
+    d = e.time_range.end - e.time_range.start
+    if d >= 3.0 or e.name.startswith(("cudaStreamSync", "cudaMemcpy", "cudaMalloc", "cudaEventSync")):
+        print(f"{e.time_range.start - t0:9.1f} {d:8.1f}  {e.name}")
