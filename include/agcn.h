@@ -120,14 +120,16 @@ void agcn_default_opts(agcn_opts_t* opts);
  * Degree order is ascending and stable (ties keep original row order); degree-0 rows come
  * first and get no descriptor.  Step (3) of P:295 reorders the CSR: the plan stores the
  * degree-sorted row pointer, per sorted row where its entries start in the caller's vals,
- * and its own degree-sorted copy of colidx (so every block's column indices are contiguous;
- * hot columns re-encoded, see hot_rows).  Ownership: the plan copies what it needs --
- * rowptr and colidx may be freed or changed after return.  The
- * AGCN_PARTITION_WARP plan copies colidx in the original order.  Synchronises the
- * plan stream once mid-way (bucket counts, validation flags); the last kernels run
- * asynchronously on opts.stream, and agcn_spmm on another stream waits for them (event).
- * Block plans of graphs with n <= 32768, nnz <= 2^20, deg_bound <= 512 and at most 1024
- * oversized rows run as one CTA and synchronise once at its end (same metadata).
+ * and its own copy of colidx, kept in the caller's order so that a sorted row's column indices
+ * and vals are read at the same offset (hot columns re-encoded, see hot_rows).  Ownership: the
+ * plan copies what it needs -- no kernel reads rowptr or colidx after return, so they may be
+ * freed or changed then.  Host synchronisation: the general block plan waits for
+ * two events on opts.stream (the bucket counts + rowptr flags, then the colidx range flag), never
+ * for the stream: it returns while its last kernels (degree order, Alg. 1/2 descriptors) still
+ * run asynchronously on opts.stream; agcn_spmm on that stream is ordered after them and
+ * agcn_spmm on another stream waits for them (event).  The AGCN_PARTITION_WARP plan and block
+ * plans of graphs with n <= 32768, nnz <= 2^20, deg_bound <= 512 and at most 1024 oversized rows
+ * (one CTA, same metadata) read one set of flags back mid-way.
  * Limits: deg_bound = max_block_warps*max_warp_nzs <= 2048,
  * max_block_warps < 65536 and max_warp_nzs < 65536 (16-bit info halves) -> otherwise
  * AGCN_ERR_UNSUPPORTED / AGCN_ERR_OVERFLOW.  Returns NULL on error.

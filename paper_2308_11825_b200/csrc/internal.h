@@ -169,9 +169,12 @@ struct PlanFlags {          // device-written, read back once (validation + size
     int32_t rowptr_first;
     int32_t rowptr_last;
     int32_t n_ov_heavy;     // oversized rows of more than kHeavyChunks deg_bound chunks
-    int32_t pad[2];
+    int32_t hot_tau;        // hot set from the histogram (k_hot_tau): rows of degree > hot_tau ...
+    int32_t hot_first;      // ... and the degree-hot_tau rows of rank >= hot_first (row order)
+    int32_t hot_fallback;   // 1: the threshold falls among the oversized rows (use the sorted tail)
     int64_t ov_chunks;      // sum over oversized rows of ceil(deg / deg_bound)
     int64_t ov_chunks_heavy;  // the part of ov_chunks from rows of degree >= kColBlockMinDeg
+    int64_t n_hot;          // hot rows selected by k_hot_tau
 };
 
 constexpr int32_t kHeavyChunks = 16;     // oversized rows above this many chunks: CTA-wide merge

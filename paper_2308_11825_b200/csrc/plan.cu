@@ -35,10 +35,13 @@ __device__ __forceinline__ int32_t row_key(const int32_t* rowptr, int64_t i, int
 }
 
 // ---------------------------------------------------------------- (1)+(2) histogram
+// rp_copy (optional): the plan's scratch copy of rowptr, written on the way (every later plan
+// kernel reads the copy, so nothing reads the caller's rowptr after agcn_plan returns)
 __global__ void __launch_bounds__(kThreads) k_deg_hist(const int32_t* __restrict__ rowptr, int64_t n,
                                                       int32_t db, int32_t nbins, int64_t ntiles,
                                                       int32_t* __restrict__ table,
-                                                      PlanFlags* __restrict__ flags) {
+                                                      PlanFlags* __restrict__ flags,
+                                                      int32_t* __restrict__ rp_copy) {
     extern __shared__ int32_t hist[];
     for (int b = threadIdx.x; b < nbins; b += kThreads) hist[b] = 0;
     __syncthreads();
@@ -47,7 +50,9 @@ __global__ void __launch_bounds__(kThreads) k_deg_hist(const int32_t* __restrict
     long long ovc = 0, ovh = 0;
     int32_t nhv = 0;
     for (int64_t i = lo + threadIdx.x; i < hi; i += kThreads) {
-        int32_t d = rowptr[i + 1] - rowptr[i];
+        const int32_t r0 = rowptr[i];
+        int32_t d = rowptr[i + 1] - r0;
+        if (rp_copy) rp_copy[i] = r0;
         if (d < 0) bad = 1;
         int32_t key = d <= 0 ? 0 : (d <= db ? d : db + 1);
         // power-law degrees: most lanes of a warp share a few keys (C5: 54 % degree 0) ->
@@ -97,6 +102,7 @@ __global__ void __launch_bounds__(kThreads) k_deg_hist(const int32_t* __restrict
         if (blockIdx.x == 0) {
             flags->rowptr_first = rowptr[0];
             flags->rowptr_last = rowptr[n];
+            if (rp_copy) rp_copy[n] = rowptr[n];
         }
     }
     for (int b = threadIdx.x; b < nbins; b += kThreads) table[(int64_t)b * ntiles + blockIdx.x] = hist[b];
@@ -235,20 +241,6 @@ __device__ __forceinline__ int32_t bin_search(const int32_t* a, int32_t db, int3
     return lo - 1;
 }
 
-// Colidx validation (0 <= colidx < n_cols), one flat coalesced pass over the nonzeros.
-// colidx is indexed by rowptr values: the run starts at colidx[rowptr[0]] (read on device).
-__global__ void k_validate_cols(const int32_t* __restrict__ rowptr, const int32_t* __restrict__ colidx_g,
-                                int64_t nnz, int64_t n_cols, PlanFlags* __restrict__ flags) {
-    const int32_t* __restrict__ colidx = colidx_g + __ldg(rowptr);
-    int32_t bad = 0;
-    for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < nnz;
-         q += (int64_t)gridDim.x * blockDim.x) {
-        const int32_t j = __ldcs(colidx + q);
-        bad |= (j < 0) | ((int64_t)j >= n_cols);
-    }
-    if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) flags->bad_colidx = 1;
-}
-
 // The plan's copy of colidx (the caller may free its arrays after agcn_plan),
 // in the caller's order -- the SpMM reads a sorted row's column indices and vals at the same
 // offsets (row_src_off, P:295 step (3)) -- made in one flat, coalesced pass: 4 entries per
@@ -268,9 +260,17 @@ __device__ __forceinline__ int32_t encode_col(int32_t c, int64_t n_cols, const C
     return c;
 }
 
-__global__ void k_copy_cols_enc(const int32_t* __restrict__ cols, int64_t nnz, int64_t n_cols, ColMap cm,
-                                const uint2* __restrict__ hot, int32_t* __restrict__ out,
+// cols: the caller's colidx array when rp != NULL (the run [rp[0], rp[n]) is copied, read on the
+// device; an inconsistent rowptr -- rp[n] - rp[0] != nnz, reported by the plan's flags -- copies
+// nothing), else an array of nnz entries re-encoded in place (out == cols).
+__global__ void k_copy_cols_enc(const int32_t* cols, const int32_t* __restrict__ rp, int64_t n, int64_t nnz,
+                                int64_t n_cols, ColMap cm, const uint2* __restrict__ hot, int32_t* out,
                                 PlanFlags* __restrict__ flags) {
+    if (rp) {
+        const int32_t base = __ldg(rp);
+        if ((int64_t)__ldg(rp + n) - base != nnz) return;
+        cols += base;
+    }
     int32_t bad = 0;
     const int64_t T = (int64_t)gridDim.x * blockDim.x;
     for (int64_t q0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q0 < nnz; q0 += 4 * T) {
@@ -314,6 +314,90 @@ __global__ void k_hot_list(uint2* __restrict__ hot, const int32_t* __restrict__ 
         hot_cols[k++] = (int32_t)(i * 32 + b);
         w &= w - 1;
     }
+}
+
+// The same hot set from the degree histogram alone, so the colidx copy can run before the degree
+// order exists (while the host reads the bucket counts back): the H largest (degree, row) keys
+// of the stable ascending order are every row of degree > tau and the degree-tau rows of rank
+// >= first among them in row order.  One warp: lane l walks its chunk of degrees from the top
+// with the count of all rows above it; the highest lane that reaches H holds tau.  When more
+// than H rows exceed deg_bound (the histogram does not resolve their degrees) the plan takes
+// the tail of the sorted order instead (hot_fallback).
+__global__ void k_hot_tau(const int32_t* __restrict__ bin_cnt, int32_t db, int64_t n, int64_t Hreq,
+                          PlanFlags* __restrict__ f) {
+    const int lane = threadIdx.x & 31;
+    const int64_t live = n - bin_cnt[0];
+    const int64_t H = Hreq < live ? Hreq : live;
+    const int64_t over = bin_cnt[db + 1];
+    const int32_t chunk = (db + 31) / 32;
+    const int32_t lo = 1 + lane * chunk, hi = min(db + 1, lo + chunk);   // degrees [lo, hi)
+    int64_t mine = 0;
+    for (int32_t d = lo; d < hi; ++d) mine += bin_cnt[d];
+    int64_t above = mine;                                   // rows in chunks >= this lane's
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int64_t t = __shfl_down_sync(0xffffffffu, above, o);
+        if (lane + o < 32) above += t;
+    }
+    above = above - mine + over;                            // rows of degree >= hi
+    int32_t tau = 0, first = 0;
+    bool hit = false;
+    if (H > 0 && over <= H) {
+        for (int32_t d = hi - 1; d >= lo; --d) {
+            if (above + bin_cnt[d] >= H) {
+                tau = d;
+                first = (int32_t)(bin_cnt[d] - (H - above));
+                hit = true;
+                break;
+            }
+            above += bin_cnt[d];
+        }
+    }
+    const unsigned b = __ballot_sync(0xffffffffu, hit);
+    if (lane == 0) {
+        f->hot_tau = 0x7fffffff;
+        f->hot_first = 0;
+        f->hot_fallback = H > 0 && over > H;
+        f->n_hot = 0;
+    }
+    __syncwarp();
+    if (b && lane == 31 - __clz(b)) {
+        f->hot_tau = tau;
+        f->hot_first = first;
+        f->n_hot = H;
+    }
+}
+// Pass A, one warp per 32 rows = one bitmap word: ballots of degree > tau and degree == tau, the
+// latter's popcount per word (scanned into ranks).  rp: the plan's rowptr copy.
+__global__ void k_hot_deg_a(const int32_t* __restrict__ rp, int64_t n, const PlanFlags* __restrict__ f,
+                            uint2* __restrict__ hot, uint32_t* __restrict__ eqw, int32_t* __restrict__ eqc) {
+    const int32_t tau = f->hot_tau;
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int32_t d = i < n ? rp[i + 1] - rp[i] : -1;
+    const uint32_t gt = __ballot_sync(0xffffffffu, d > tau), eq = __ballot_sync(0xffffffffu, d == tau);
+    if ((threadIdx.x & 31) == 0 && i < n) {
+        hot[i >> 5] = make_uint2(gt, 0u);
+        eqw[i >> 5] = eq;
+        eqc[i >> 5] = __popc(eq);
+    }
+}
+// Pass B: the degree-tau rows of rank >= first join; cnt[w] = popcount of the final word
+__global__ void k_hot_deg_b(uint2* __restrict__ hot, const uint32_t* __restrict__ eqw,
+                            const int32_t* __restrict__ eqpre, int64_t nw, const PlanFlags* __restrict__ f,
+                            int32_t* __restrict__ cnt) {
+    const int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (w >= nw) return;
+    const int32_t first = f->hot_first;
+    uint32_t e = eqw[w], bits = hot[w].x;
+    int32_t r = eqpre[w];
+    while (e) {
+        const uint32_t b = e & (0u - e);
+        if (r >= first) bits |= b;
+        ++r;
+        e ^= b;
+    }
+    hot[w].x = bits;
+    cnt[w] = __popc(bits);
 }
 
 // Execution order of the oversized-row chunks (kernel-internal; the descriptors keep Alg. 2's
@@ -415,14 +499,6 @@ __global__ void k_rowptr_check(const int32_t* __restrict__ rowptr, int64_t n, in
     }
 }
 
-__global__ void k_copy_cols(const int32_t* __restrict__ colidx, int64_t nnz, int32_t* __restrict__ out,
-                            ColMap cm) {
-    for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < nnz;
-         q += (int64_t)gridDim.x * blockDim.x)
-        out[q] = map_col(colidx[q], cm);
-}
-
-// Fig. 3(b): row i -> tasks {i, c, min(mwn, d - c), 0} for c = 0, mwn, 2 mwn, ...
 __global__ void k_emit_tasks(const int32_t* __restrict__ rp, int64_t n, int32_t mwn,
                              const int32_t* __restrict__ tstart, int4* __restrict__ tasks) {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -502,34 +578,30 @@ void check_csr_flags(const PlanFlags& f, int64_t nnz) {
                "rowptr[n] - rowptr[0] != nnz");
 }
 
-// First phase shared by both partitions: validate colidx (optional, flat pass) then read the
-// flags once.  This is the plan's only host synchronisation.
-void validate_cols(const int32_t* rowptr, const int32_t* colidx, int64_t nnz, int64_t n_cols,
-                   PlanFlags* d_flags, cudaStream_t s) {
-    if (nnz == 0) return;
-    const unsigned g = (unsigned)std::min<int64_t>(blocks_for(nnz, 256), 148 * 16);
-    k_validate_cols<<<g, 256, 0, s>>>(rowptr, colidx, nnz, n_cols, d_flags);
+// The plan's copy of colidx (k_copy_cols_enc, flat, 4 entries per thread in flight): rp is a
+// DEVICE rowptr (the caller's or the plan's copy; the run [rp[0], rp[n]) is copied) or NULL to
+// re-encode p->cols_copy in place.  hot: the hot-column table or NULL; d_flags != NULL:
+// validate the column range on the way.
+void launch_copy_cols(agcn_plan_s* p, const int32_t* cols, const int32_t* rp, const uint2* hot,
+                      PlanFlags* d_flags, cudaStream_t s) {
+    if (p->nnz == 0) return;
+    const unsigned g = (unsigned)std::min<int64_t>(blocks_for(p->nnz, 256 * 4), (int64_t)num_sms() * 8);
+    k_copy_cols_enc<<<g, 256, 0, s>>>(cols, rp, p->n, p->nnz, p->n_cols, p->cmap, hot, p->cols_copy, d_flags);
     post_launch();
 }
 
-// WARP plan: the plan's copy of colidx in the original order (rowptr-relative), relabelled for
-// a padded multi-GPU layout (one flat pass).
-void copy_cols_original(agcn_plan_s* p, const int32_t* colidx, cudaStream_t s) {
-    p->cols_copy = dalloc<int32_t>(p->nnz, s);
-    p->device_bytes += sizeof(int32_t) * (size_t)p->nnz;
-    if (p->nnz > 0) {
-        k_copy_cols<<<(unsigned)std::min<int64_t>(blocks_for(p->nnz, 256), 148 * 16), 256, 0, s>>>(
-            colidx + p->rp_base, p->nnz, p->cols_copy, p->cmap);
-        post_launch();
-    }
+// Hot rows requested (agcn_opts_t.hot_rows) before the degrees are known: square A without a
+// padded layout only; -1: 524288 for graphs of >= 2^19 rows (C5 sweep: profiles/r02af).
+int64_t hot_rows_req(const agcn_plan_s* p, int64_t req) {
+    if (p->n_cols != p->n || p->cmap.nparts > 0 || req == 0) return 0;
+    const int64_t H = req > 0 ? req : (p->n >= (1ll << 19) ? 524288 : 0);
+    return std::min(H, p->n);
 }
 
 // Hot rows of a plan (agcn_opts_t.hot_rows): square A without a padded layout only.
+// ... capped at the rows of degree >= 1 (n_zero known)
 int64_t hot_rows_for(const agcn_plan_s* p, int64_t req) {
-    if (p->n_cols != p->n || p->cmap.nparts > 0 || req == 0) return 0;
-    const int64_t live = p->n - p->n_zero;  // vertices of degree >= 1
-    int64_t H = req > 0 ? req : (p->n >= (1ll << 19) ? 524288 : 0);  // C5 sweep: profiles/r02af
-    return std::max<int64_t>(0, std::min(H, live));
+    return std::max<int64_t>(0, std::min(hot_rows_req(p, req), p->n - p->n_zero));
 }
 
 // BLOCK plan, after the descriptors: the execution order of the oversized chunks (k_ov_keys).
@@ -551,34 +623,30 @@ void build_ov_order(agcn_plan_s* p, int32_t buckets, cudaStream_t s) {
     AGCN_CUDA(cudaMemcpyAsync(p->ov_order, va, sizeof(int32_t) * m, cudaMemcpyDeviceToDevice, s));
 }
 
-// BLOCK plan, after the degree order: the plan's colidx copy with the hot encoding;
-// d_flags != NULL: validate the column range on the way (read back by the caller).
-void build_cols(agcn_plan_s* p, const int32_t* colidx, const agcn_opts_t& o, cudaStream_t s,
-                PlanFlags* d_flags = nullptr) {
-    p->cols_copy = dalloc<int32_t>(p->nnz, s);
-    p->device_bytes += sizeof(int32_t) * (size_t)p->nnz;
-    p->n_hot = hot_rows_for(p, o.hot_rows);
+// BLOCK plan, after the degree order, when the hot set could not be taken from the histogram
+// (k_hot_tau: more than H oversized rows; or the one-CTA plan): the hot_rows highest-degree
+// vertices = the tail of the degree order -> bitmap + prefixes -> hot_cols, then the plan's
+// colidx copy (already made) re-encoded in place.
+void encode_hot_from_tail(agcn_plan_s* p, int64_t H, cudaStream_t s) {
+    p->n_hot = H;
+    if (H <= 0 || p->nnz == 0) return;
     Scratch tmp(s);
-    uint2* hot = nullptr;
-    if (p->n_hot > 0) {
-        const int64_t nw = (p->n_cols + 31) / 32;
-        hot = tmp.alloc<uint2>(nw);
-        int32_t* pre = tmp.alloc<int32_t>(nw + 1);
-        p->hot_cols = dalloc<int32_t>(p->n_hot, s);
-        p->device_bytes += sizeof(int32_t) * (size_t)p->n_hot;
-        AGCN_CUDA(cudaMemsetAsync(hot, 0, sizeof(uint2) * nw, s));
-        k_hot_bits<<<blocks_for(p->n_hot, 256), 256, 0, s>>>(p->perm, p->n, p->n_hot, hot);
-        post_launch();
-        k_popc_words<<<blocks_for(nw, 256), 256, 0, s>>>(hot, nw, pre);
-        post_launch();
-        exclusive_scan_i32(pre, pre, nw, s);
-        k_hot_list<<<blocks_for(nw, 256), 256, 0, s>>>(hot, pre, nw, p->hot_cols);
-        post_launch();
+    const int64_t nw = (p->n_cols + 31) / 32;
+    uint2* hot = tmp.alloc<uint2>(nw);
+    int32_t* pre = tmp.alloc<int32_t>(nw + 1);
+    if (!p->hot_cols) {
+        p->hot_cols = dalloc<int32_t>(H, s);
+        p->device_bytes += sizeof(int32_t) * (size_t)H;
     }
-    if (p->nnz == 0) return;
-    const unsigned g = (unsigned)std::min<int64_t>(blocks_for(p->nnz, 256 * 4), (int64_t)num_sms() * 8);
-    k_copy_cols_enc<<<g, 256, 0, s>>>(colidx + p->rp_base, p->nnz, p->n_cols, p->cmap, hot, p->cols_copy, d_flags);
+    AGCN_CUDA(cudaMemsetAsync(hot, 0, sizeof(uint2) * nw, s));
+    k_hot_bits<<<blocks_for(H, 256), 256, 0, s>>>(p->perm, p->n, H, hot);
     post_launch();
+    k_popc_words<<<blocks_for(nw, 256), 256, 0, s>>>(hot, nw, pre);
+    post_launch();
+    exclusive_scan_i32(pre, pre, nw, s);
+    k_hot_list<<<blocks_for(nw, 256), 256, 0, s>>>(hot, pre, nw, p->hot_cols);
+    post_launch();
+    launch_copy_cols(p, p->cols_copy, nullptr, hot, nullptr, s);
 }
 
 }  // namespace
@@ -600,8 +668,7 @@ void radix_sort_pairs(int32_t*& ka, int32_t*& va, int32_t*& kb, int32_t*& vb, in
         k_bucket_hist<RadixSrc><<<(unsigned)mt, kThreads, 256 * sizeof(int32_t), s>>>(src, m, 256, mt, rt);
         post_launch();
         exclusive_scan_i32(rt, rt, 256 * mt, s);
-        k_bucket_scatter<RadixSrc><<<(unsigned)mt, kThreads, kWarps * 256 * sizeof(int32_t), s>>>(
-            src, m, 256, mt, rt);
+        k_bucket_scatter<RadixSrc><<<(unsigned)mt, kThreads, kWarps * 256 * sizeof(int32_t), s>>>(src, m, 256, mt, rt);
         post_launch();
         std::swap(ka, kb);
         std::swap(va, vb);
@@ -917,6 +984,9 @@ bool build_block_plan_small(agcn_plan_s* p, const int32_t* rowptr, const int32_t
                                                 o.validate, p->perm, p->sorted_rowptr, p->row_src_off,
                                                 p->desc, p->ov_chunk_start, d_out);
     post_launch();
+    // the plan's colidx copy, before the readback: nothing reads the caller's arrays after return
+    p->cols_copy = dalloc<int32_t>(nnz, s);
+    launch_copy_cols(p, colidx, rowptr, nullptr, nullptr, s);
     SmallOut h{};
     auto* pin = static_cast<SmallOut*>(pinned_staging(sizeof(SmallOut)));
     AGCN_CUDA(cudaMemcpyAsync(pin ? pin : &h, d_out, sizeof(SmallOut), cudaMemcpyDeviceToHost, s));
@@ -924,9 +994,9 @@ bool build_block_plan_small(agcn_plan_s* p, const int32_t* rowptr, const int32_t
     if (pin) h = *pin;
     if (h.fallback) {
         for (void* q : {(void*)p->perm, (void*)p->sorted_rowptr, (void*)p->row_src_off, (void*)p->desc,
-                        (void*)p->ov_chunk_start})
+                        (void*)p->ov_chunk_start, (void*)p->cols_copy})
             cudaFreeAsync(q, s);
-        p->perm = p->sorted_rowptr = p->row_src_off = p->ov_chunk_start = nullptr;
+        p->perm = p->sorted_rowptr = p->row_src_off = p->ov_chunk_start = p->cols_copy = nullptr;
         p->desc = nullptr;
         return false;
     }
@@ -946,48 +1016,133 @@ bool build_block_plan_small(agcn_plan_s* p, const int32_t* rowptr, const int32_t
     p->max_deg = h.max_deg;
     p->nb_small = h.nb_small;
     p->nblocks = h.nb_small + h.ov_chunks;
-    p->device_bytes = sizeof(int32_t) * (size_t)(3 * n + 1 + ovc_cap) + sizeof(int4) * (size_t)desc_cap;
-    build_cols(p, colidx, o, s);
+    p->device_bytes = sizeof(int32_t) * (size_t)(3 * n + 1 + ovc_cap + nnz) + sizeof(int4) * (size_t)desc_cap;
+    encode_hot_from_tail(p, hot_rows_for(p, o.hot_rows), s);
     build_ov_order(p, o.chunk_buckets, s);
     return true;
 }
 
 // ---------------------------------------------------------------- block-partition plan
+// Host synchronisation: the plan waits for two events on its stream and never for the stream
+// itself.  Stream order:
+//   [deg_hist (+ the plan's rowptr copy), bucket-table scan, bucket totals, hot threshold]
+//   -> D2H of the flags + bucket counts, event E1
+//   [hot set from the histogram, the colidx copy with the hot encoding + colidx validation]
+//   -> D2H of the colidx flag, event E2
+//   [scatter, oversized radix sort, sorted rows, Alg. 1/2 descriptors, chunk order]
+// The host waits for E1 (sizes, rowptr validity) while the GPU runs the copy, enqueues the
+// rest behind it, then waits for E2 (colidx validity) and returns while the GPU finishes the
+// sort: no GPU idle time at either wait, and the caller's next launches queue behind the plan.
+// After E2 nothing reads the caller's rowptr / colidx (the later kernels read the plan's
+// rowptr copy), so the caller may free or change them once agcn_plan has returned.
+namespace {
+
+// pinned host staging with a reuse guard (an H2D from it must have run before it is rewritten)
+struct PinnedSlot {
+    void* buf = nullptr;
+    size_t cap = 0;
+    cudaEvent_t busy = nullptr;
+    bool pending = false;
+    void* get(size_t bytes) {
+        if (pending) {
+            cudaEventSynchronize(busy);
+            pending = false;
+        }
+        if (bytes > cap) {
+            if (buf) cudaFreeHost(buf);
+            buf = nullptr;
+            cap = 0;
+            AGCN_CUDA(cudaMallocHost(&buf, bytes));
+            cap = bytes;
+        }
+        return buf;
+    }
+    void mark(cudaStream_t s) {
+        if (!busy) AGCN_CUDA(cudaEventCreateWithFlags(&busy, cudaEventDisableTiming));
+        AGCN_CUDA(cudaEventRecord(busy, s));
+        pending = true;
+    }
+};
+// per host thread and device: 0 the readbacks, 1 the colidx flag, 2 the Alg. 1/2 tables; E1, E2
+struct PlanSync {
+    PinnedSlot pin[3];
+    cudaEvent_t e1 = nullptr, e2 = nullptr;
+};
+PlanSync& plan_sync(int dev) {
+    thread_local PlanSync ps[64];
+    PlanSync& r = ps[dev >= 0 && dev < 64 ? dev : 0];
+    if (!r.e1) {
+        AGCN_CUDA(cudaEventCreateWithFlags(&r.e1, cudaEventDisableTiming));
+        AGCN_CUDA(cudaEventCreateWithFlags(&r.e2, cudaEventDisableTiming));
+    }
+    return r;
+}
+
+}  // namespace
+
 void build_block_plan(agcn_plan_s* p, const int32_t* rowptr, const int32_t* colidx,
                       const agcn_opts_t& o, cudaStream_t s) {
     const int64_t n = p->n, nnz = p->nnz;
     const int32_t db = p->deg_bound, nbins = db + 2;
     const int64_t ntiles = std::max<int64_t>(1, (n + kTile - 1) / kTile);
+    PlanSync& ps = plan_sync(p->device);
 
     Scratch tmp(s);
     PlanFlags* d_flags = tmp.alloc<PlanFlags>(1);
     int32_t* bin_cnt = tmp.alloc<int32_t>(nbins);
     int32_t* table = tmp.alloc<int32_t>((size_t)nbins * ntiles + 1);
+    int32_t* rp = tmp.alloc<int32_t>(n + 1);  // the plan's rowptr copy (written by k_deg_hist)
     AGCN_CUDA(cudaMemsetAsync(d_flags, 0, sizeof(PlanFlags), s));
 
-    // (1)+(2a) per-tile bucket histograms, bucket totals, max degree, rowptr validation (the
-    // colidx range is validated inside the sorted-colidx copy at the end, read back once there)
+    // (1)+(2a) per-tile bucket histograms, bucket totals, max degree, rowptr validation
     k_deg_hist<<<(unsigned)ntiles, kThreads, nbins * sizeof(int32_t), s>>>(rowptr, n, db, nbins, ntiles,
-                                                                         table, d_flags);
+                                                                         table, d_flags, rp);
     post_launch();
     exclusive_scan_i32(table, table, (int64_t)nbins * ntiles, s);
     k_bin_totals<<<(nbins + 255) / 256, 256, 0, s>>>(table, ntiles, nbins, n, bin_cnt);
     post_launch();
-
-    std::vector<int32_t> h_cnt(nbins);
-    PlanFlags hf{};
-    // the plan's mid-course synchronisation (bucket counts, flags), through pinned staging
-    if (auto* pin = static_cast<unsigned char*>(pinned_staging(sizeof(PlanFlags) + sizeof(int32_t) * nbins))) {
-        AGCN_CUDA(cudaMemcpyAsync(pin, d_flags, sizeof(PlanFlags), cudaMemcpyDeviceToHost, s));
-        AGCN_CUDA(cudaMemcpyAsync(pin + sizeof(PlanFlags), bin_cnt, sizeof(int32_t) * nbins,
-                                  cudaMemcpyDeviceToHost, s));
-        AGCN_CUDA(cudaStreamSynchronize(s));
-        memcpy(&hf, pin, sizeof(PlanFlags));
-        memcpy(h_cnt.data(), pin + sizeof(PlanFlags), sizeof(int32_t) * nbins);
-    } else {
-        AGCN_CUDA(cudaMemcpyAsync(h_cnt.data(), bin_cnt, sizeof(int32_t) * nbins, cudaMemcpyDeviceToHost, s));
-        read_flags(d_flags, &hf, s);
+    const int64_t Hreq = hot_rows_req(p, o.hot_rows);
+    if (Hreq > 0) {  // hot set from the histogram (reading Q35 = the tail of the stable degree order)
+        k_hot_tau<<<1, 32, 0, s>>>(bin_cnt, db, n, Hreq, d_flags);
+        post_launch();
     }
+    auto* pin0 = static_cast<unsigned char*>(ps.pin[0].get(sizeof(PlanFlags) + sizeof(int32_t) * nbins));
+    AGCN_CUDA(cudaMemcpyAsync(pin0, d_flags, sizeof(PlanFlags), cudaMemcpyDeviceToHost, s));
+    AGCN_CUDA(cudaMemcpyAsync(pin0 + sizeof(PlanFlags), bin_cnt, sizeof(int32_t) * nbins, cudaMemcpyDeviceToHost, s));
+    AGCN_CUDA(cudaEventRecord(ps.e1, s));
+
+    // the plan's colidx copy (caller's order) with the hot encoding and the range check
+    p->cols_copy = dalloc<int32_t>(nnz, s);
+    p->device_bytes = sizeof(int32_t) * (size_t)nnz;
+    uint2* hot = nullptr;
+    if (Hreq > 0 && nnz > 0) {
+        const int64_t nw = (n + 31) / 32;
+        hot = tmp.alloc<uint2>(nw);
+        uint32_t* eqw = tmp.alloc<uint32_t>(nw);
+        int32_t* eqc = tmp.alloc<int32_t>(nw + 1);
+        int32_t* cnt = tmp.alloc<int32_t>(nw + 1);
+        p->hot_cols = dalloc<int32_t>(Hreq, s);
+        p->device_bytes += sizeof(int32_t) * (size_t)Hreq;
+        k_hot_deg_a<<<blocks_for(n, 256), 256, 0, s>>>(rp, n, d_flags, hot, eqw, eqc);
+        post_launch();
+        exclusive_scan_i32(eqc, eqc, nw, s);
+        k_hot_deg_b<<<blocks_for(nw, 256), 256, 0, s>>>(hot, eqw, eqc, nw, d_flags, cnt);
+        post_launch();
+        exclusive_scan_i32(cnt, cnt, nw, s);
+        k_hot_list<<<blocks_for(nw, 256), 256, 0, s>>>(hot, cnt, nw, p->hot_cols);
+        post_launch();
+    }
+    launch_copy_cols(p, colidx, rp, hot, o.validate ? d_flags : nullptr, s);
+    auto* pin1 = static_cast<int32_t*>(ps.pin[1].get(sizeof(int32_t)));
+    AGCN_CUDA(cudaMemcpyAsync(pin1, &d_flags->bad_colidx, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    AGCN_CUDA(cudaEventRecord(ps.e2, s));
+
+    // the bucket counts and flags (the GPU runs the copy meanwhile)
+    AGCN_CUDA(cudaEventSynchronize(ps.e1));
+    PlanFlags hf{};
+    std::vector<int32_t> h_cnt(nbins);
+    memcpy(&hf, pin0, sizeof(PlanFlags));
+    memcpy(h_cnt.data(), pin0 + sizeof(PlanFlags), sizeof(int32_t) * nbins);
     check_csr_flags(hf, nnz);
     p->rp_base = hf.rowptr_first;
 
@@ -995,13 +1150,14 @@ void build_block_plan(agcn_plan_s* p, const int32_t* rowptr, const int32_t* coli
     std::vector<int32_t> br, wn;
     host_patterns(p->mbw, p->mwn, br, wn);
     const int32_t W = db + 2;
-    std::vector<int32_t> tab(6 * W, 0);
-    int32_t* nnz_start = tab.data();
-    int32_t* row_start = tab.data() + W;
-    int32_t* blk_start = tab.data() + 2 * W;
-    int32_t* cntv = tab.data() + 3 * W;
-    int32_t* brv = tab.data() + 4 * W;
-    int32_t* wnv = tab.data() + 5 * W;
+    auto* tab = static_cast<int32_t*>(ps.pin[2].get(sizeof(int32_t) * 6 * W));
+    memset(tab, 0, sizeof(int32_t) * 6 * W);
+    int32_t* nnz_start = tab;
+    int32_t* row_start = tab + W;
+    int32_t* blk_start = tab + 2 * W;
+    int32_t* cntv = tab + 3 * W;
+    int32_t* brv = tab + 4 * W;
+    int32_t* wnv = tab + 5 * W;
     int64_t row = h_cnt[0], loc = 0, blk = 0;
     for (int32_t d = 1; d <= db + 1; ++d) {
         nnz_start[d] = (int32_t)loc;
@@ -1025,24 +1181,23 @@ void build_block_plan(agcn_plan_s* p, const int32_t* rowptr, const int32_t* coli
     p->max_deg = hf.max_deg;
     p->nb_small = blk;
     p->nblocks = blk + hf.ov_chunks;
+    p->n_hot = hot ? hf.n_hot : 0;
     AGCN_CHECK(p->nblocks < (1ll << 31), AGCN_ERR_OVERFLOW, "too many descriptors");
 
-    // plan-owned arrays (the sorted colidx copy follows the descriptors)
+    // plan-owned arrays
     p->perm = dalloc<int32_t>(n, s);
     p->sorted_rowptr = dalloc<int32_t>(n + 1, s);
     p->row_src_off = dalloc<int32_t>(n, s);
     p->desc = dalloc<int4>(p->nblocks, s);
     p->ov_chunk_start = dalloc<int32_t>(p->n_ov + 1, s);
-    p->device_bytes = sizeof(int32_t) * (size_t)(3 * n + 1 + p->n_ov + 1) +
-                      sizeof(int4) * (size_t)p->nblocks;
+    p->device_bytes += sizeof(int32_t) * (size_t)(3 * n + 1 + p->n_ov + 1) + sizeof(int4) * (size_t)p->nblocks;
 
     // (2b) stable scatter into bucket order
     const size_t scat_smem = (size_t)kWarps * nbins * sizeof(int32_t);
     if (scat_smem > 48 * 1024)
         AGCN_CUDA(cudaFuncSetAttribute(k_bucket_scatter<MainSrc>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)scat_smem));
-    k_bucket_scatter<MainSrc><<<(unsigned)ntiles, kThreads, scat_smem, s>>>(
-        MainSrc{rowptr, db, p->perm}, n, nbins, ntiles, table);
+    k_bucket_scatter<MainSrc><<<(unsigned)ntiles, kThreads, scat_smem, s>>>(MainSrc{rp, db, p->perm}, n, nbins, ntiles, table);
     post_launch();
 
     // (2c) oversized rows (degree > deg_bound) keep row order within the bucket; stable LSD
@@ -1053,7 +1208,7 @@ void build_block_plan(agcn_plan_s* p, const int32_t* rowptr, const int32_t* coli
         int32_t* va = tmp.alloc<int32_t>(m);
         int32_t* kb = tmp.alloc<int32_t>(m);
         int32_t* vb = tmp.alloc<int32_t>(m);
-        k_ov_init<<<blocks_for(m, 256), 256, 0, s>>>(p->perm + p->ov_start, rowptr, m, ka, va);
+        k_ov_init<<<blocks_for(m, 256), 256, 0, s>>>(p->perm + p->ov_start, rp, m, ka, va);
         post_launch();
         radix_sort_pairs(ka, va, kb, vb, m, p->max_deg, s);
         AGCN_CUDA(cudaMemcpyAsync(p->perm + p->ov_start, va, sizeof(int32_t) * m,
@@ -1062,10 +1217,10 @@ void build_block_plan(agcn_plan_s* p, const int32_t* rowptr, const int32_t* coli
 
     // (3) "updating the row pointer array to reflect the new row order", O(n):
     // sorted degrees -> sorted_rowptr (scan) and row_src_off (where each sorted row starts in
-    // the caller's colidx / vals); the sorted colidx is copied after the descriptors.
+    // the caller's colidx / vals), one look-back scan pass.
     if (n > 0) {
         const int64_t nt = (n + kLbTile - 1) / kLbTile;
-        launch_scan_lb(SortedRowsSrc{p->perm, rowptr, p->row_src_off}, p->sorted_rowptr, n,
+        launch_scan_lb(SortedRowsSrc{p->perm, rp, p->row_src_off}, p->sorted_rowptr, n,
                        nt > 1 ? tmp.alloc<unsigned long long>(nt + 1) : nullptr, s);
     } else {
         AGCN_CUDA(cudaMemsetAsync(p->sorted_rowptr, 0, sizeof(int32_t), s));
@@ -1073,7 +1228,8 @@ void build_block_plan(agcn_plan_s* p, const int32_t* rowptr, const int32_t* coli
 
     // (4)+(5) Algorithm 1/2 descriptors
     int32_t* d_tab = tmp.alloc<int32_t>(6 * W);
-    AGCN_CUDA(cudaMemcpyAsync(d_tab, tab.data(), sizeof(int32_t) * 6 * W, cudaMemcpyHostToDevice, s));
+    AGCN_CUDA(cudaMemcpyAsync(d_tab, tab, sizeof(int32_t) * 6 * W, cudaMemcpyHostToDevice, s));
+    ps.pin[2].mark(s);
     if (p->nb_small > 0) {
         unsigned g = (unsigned)std::min<int64_t>(blocks_for(p->nb_small, kThreads), 148 * 8);
         size_t smem = 6 * W * sizeof(int32_t);
@@ -1094,17 +1250,13 @@ void build_block_plan(agcn_plan_s* p, const int32_t* rowptr, const int32_t* coli
     } else {
         AGCN_CUDA(cudaMemsetAsync(p->ov_chunk_start, 0, sizeof(int32_t), s));
     }
-
-    build_cols(p, colidx, o, s, o.validate ? d_flags : nullptr);
+    // the hot set among the oversized rows: from the sorted tail, encoded in place
+    if (hot && hf.hot_fallback) encode_hot_from_tail(p, hot_rows_for(p, o.hot_rows), s);
     build_ov_order(p, o.chunk_buckets, s);
-    if (o.validate && nnz > 0) {  // the plan's second (and last) synchronisation: colidx range
-        int32_t* pin = static_cast<int32_t*>(pinned_staging(sizeof(int32_t)));
-        int32_t bad = 0;
-        AGCN_CUDA(cudaMemcpyAsync(pin ? pin : &bad, &d_flags->bad_colidx, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
-        AGCN_CUDA(cudaStreamSynchronize(s));
-        if (pin) bad = *pin;
-        AGCN_CHECK(!bad, AGCN_ERR_BAD_CSR, "colidx out of [0, n_cols)");
-    }
+
+    // the colidx range (the copy has run by now or soon; the sort above stays queued)
+    AGCN_CUDA(cudaEventSynchronize(ps.e2));
+    if (o.validate && nnz > 0) AGCN_CHECK(!*pin1, AGCN_ERR_BAD_CSR, "colidx out of [0, n_cols)");
 }
 
 // ---------------------------------------------------------------- warp-partition plan
@@ -1119,7 +1271,10 @@ void build_warp_plan(agcn_plan_s* p, const int32_t* rowptr, const int32_t* colid
     k_rowptr_check<<<blocks_for(n + 1, 256), 256, 0, s>>>(rowptr, n, p->mwn, p->rowptr_copy, tstart,
                                                           d_flags);
     post_launch();
-    if (o.validate) validate_cols(rowptr, colidx, nnz, p->n_cols, d_flags, s);
+    // the plan's colidx copy (original order, padded-layout relabel) with the range check, before
+    // the readback: nothing reads the caller's arrays after return
+    p->cols_copy = dalloc<int32_t>(nnz, s);
+    launch_copy_cols(p, colidx, rowptr, nullptr, o.validate ? d_flags : nullptr, s);
     exclusive_scan_i32(tstart, tstart, n, s);
     int32_t ntasks = 0;
     AGCN_CUDA(cudaMemcpyAsync(&ntasks, tstart + n, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
@@ -1131,8 +1286,7 @@ void build_warp_plan(agcn_plan_s* p, const int32_t* rowptr, const int32_t* colid
     p->max_deg = hf.max_deg;
     p->rp_base = hf.rowptr_first;
     p->tasks = dalloc<int4>(ntasks, s);
-    p->device_bytes = sizeof(int32_t) * (size_t)(n + 1) + sizeof(int4) * (size_t)ntasks;
-    copy_cols_original(p, colidx, s);
+    p->device_bytes = sizeof(int32_t) * (size_t)(n + 1 + nnz) + sizeof(int4) * (size_t)ntasks;
     if (n > 0) {
         k_emit_tasks<<<blocks_for(n, 256), 256, 0, s>>>(p->rowptr_copy, n, p->mwn, tstart, p->tasks);
         post_launch();

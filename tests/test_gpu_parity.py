@@ -309,6 +309,31 @@ def test_hot_set_is_the_degree_tail(seed):
             assert np.array_equal(Y, Y0), (H, small)
 
 
+@pytest.mark.parametrize("partition,small", [("block", False), ("block", True), ("warp", False)])
+def test_plan_does_not_read_caller_arrays_after_return(partition, small):
+    """agcn_plan returns while its last kernels still run (the general block plan waits for
+    events, not the stream); none of them may read the caller's rowptr / colidx.  The caller's
+    arrays are overwritten on another stream right after the call, without any ordering: the
+    plan's metadata and SpMM must still match the oracle."""
+    w = gen.make_config("c3", vals_kind="uniform")
+    o = oracle.plan(w.rowptr, w.colidx, 12, 32)
+    other = torch.cuda.Stream()
+    for rep in range(3):
+        rp, ci = cu(w.rowptr), cu(w.colidx)
+        torch.cuda.synchronize()
+        p = A.Plan(rp, ci, hot_rows=20000, small_plan=small, partition=partition)
+        with torch.cuda.stream(other):
+            ci.fill_(-7)
+            rp.fill_(3)
+        torch.cuda.synchronize()
+        if partition == "block":
+            assert np.array_equal(p.copy("perm"), o["perm"])
+            assert np.array_equal(p.copy("blocks"), o["blocks"])
+            assert np.array_equal(p.copy("sorted_colidx"), o["sorted_colidx"])
+            assert np.array_equal(p.copy("hot_cols"), np.sort(o["perm"][w.n - p.stats()["hot_rows"]:]))
+        check_spmm(p, w.rowptr, w.colidx, w.vals, w.X())
+
+
 def test_hot_rows_auto_rule():
     """hot_rows = -1: on for square graphs with n >= 2^19, off otherwise and for padded layouts."""
     rowptr = np.zeros(2 ** 19 + 1, dtype=np.int32)
