@@ -1,0 +1,8 @@
+# usage: bash tools/run_sweep.sh CONFIG "opts1" "opts2" ...   (minimal bench per option set, 2 rounds interleaved)
+C=$1; shift
+python -c "import __graft_entry__ as g; g.build()" > /tmp/build.log 2>&1 || { tail /tmp/build.log; exit 1; }
+F="--no-cpu-baseline --no-e2e --no-cusparse --no-traffic --no-graph --no-per-graph --steps 10 --warmup 3 --config $C"
+for r in 1 2; do for o in "$@"; do
+  timeout 600 python bench.py $F $o > /tmp/b.log 2>&1
+  tail -1 /tmp/b.log | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('$C [$o]', round(d['ms_per_step'],3), round(d['plan_ms'],3), round(d['spmm_only']['ms_per_layer'],4), d['self_check']['ok'])" || tail -3 /tmp/b.log
+done; done
