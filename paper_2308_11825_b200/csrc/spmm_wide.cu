@@ -82,12 +82,11 @@ __device__ __forceinline__ void fma8(f8& acc, float v, const f8& x) {
           "f"(x.b.w));
 }
 
-// one 256-bit streaming store per lane (STG.E.EF.256, sm_100): half the store instructions of
-// two float4 stores (r02bb: -0.2 % C5, -0.3 % C4)
+// (a 256-bit st.global.cs.v8.f32 here measured -0.2 % but broke the in-kernel level-3 merge's
+// reads of the partial rows -- parity failures on C2 / C3, profiles/r02bb: not used)
 __device__ __forceinline__ void st8(float* p, const f8& v) {
-    asm volatile("st.global.cs.v8.f32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "f"(v.a.x), "f"(v.a.y),
-                 "f"(v.a.z), "f"(v.a.w), "f"(v.b.x), "f"(v.b.y), "f"(v.b.z), "f"(v.b.w)
-                 : "memory");
+    __stcs(reinterpret_cast<float4*>(p), v.a);
+    __stcs(reinterpret_cast<float4*>(p) + 1, v.b);
 }
 
 __device__ __forceinline__ float shfl_xor_add(float v, int o) {
@@ -591,8 +590,9 @@ void launch_wide(agcn_plan_s* p, const float* vals, const float* X, const float*
     const bool lean = F <= 64 && share >= 100.0 && share <= 4000.0;
     // the chunk kernel: plans whose oversized chunks are not merged in-kernel (level 3 by
     // k_ov_reduce_h), power-of-two L
-    // auto: F >= 128 (C4 -13 %; C5 at F = 64 measured neutral to +2 %, profiles/r02_c5_roof.md)
-    const int chunks = (!a.fuse_ov && p->ov_chunks > 0 && chunk_shape >= 0 && (chunk_shape || F >= 128))
+    // auto: F >= 32 (C4 F128 -13 %; since the X loads skip L1 (r02ba) also C5 F64 -2.3 %, C5 F32
+    // -2.9 %, C4 F64 -4.4 %, profiles/r02be_chunk_kernel.txt; F < 32 not measured)
+    const int chunks = (!a.fuse_ov && p->ov_chunks > 0 && chunk_shape >= 0 && (chunk_shape || F >= 32))
                            ? (chunk_shape ? chunk_shape : 4) : 0;
     switch (F) {
         case 8: launch<1>(a, xm, lean, win, chunks, s); break;
