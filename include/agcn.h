@@ -212,7 +212,7 @@ typedef struct {
     float* peer_out[8];
     int32_t npeer;        /* 0 (default) .. 8 */
     /* WIDE kernel, plans with more than 16384 oversized-row chunks: the chunks run in a kernel
-       of their own (k_spmm_chunks) before the other descriptors.  0 (default): auto (F >= 128:
+       of their own (k_spmm_chunks) before the other descriptors.  0 (default): auto (F >= 32:
        U 4 rows in flight per lane at 4 CTAs/SM; else off); -1: off (one kernel for every
        descriptor); 3, 4: U 4 at that many CTAs/SM; 6: U 2 at 6 CTAs/SM.  Results are bitwise
        the same. */
