@@ -1037,7 +1037,20 @@ bool build_block_plan_small(agcn_plan_s* p, const int32_t* rowptr, const int32_t
 // rowptr copy), so the caller may free or change them once agcn_plan has returned.
 namespace {
 
-// pinned host staging with a reuse guard (an H2D from it must have run before it is rewritten)
+// Small device -> host read-backs without a copy engine: a one-CTA kernel stores the words
+// straight into mapped pinned host memory (PCIe posted writes).  A cudaMemcpyAsync would queue
+// on the D2H copy engine -- behind the previous job's gigabyte copy-out in the pipelined
+// executor.  Visible to the host once an event recorded after the kernel has completed.
+__global__ void k_readback(const uint32_t* __restrict__ src, uint32_t* dst, int32_t nwords) {
+    for (int32_t i = threadIdx.x; i < nwords; i += blockDim.x) dst[i] = src[i];
+}
+void readback(void* host_mapped, const void* dev, size_t bytes, cudaStream_t s) {
+    k_readback<<<1, 256, 0, s>>>(static_cast<const uint32_t*>(dev), static_cast<uint32_t*>(host_mapped),
+                                 (int32_t)(bytes / 4));
+    post_launch();
+}
+
+// mapped pinned host staging (cudaHostAllocMapped: device-writable through the same pointer)
 struct PinnedSlot {
     void* buf = nullptr;
     size_t cap = 0;
@@ -1052,7 +1065,7 @@ struct PinnedSlot {
             if (buf) cudaFreeHost(buf);
             buf = nullptr;
             cap = 0;
-            AGCN_CUDA(cudaMallocHost(&buf, bytes));
+            AGCN_CUDA(cudaHostAlloc(&buf, bytes, cudaHostAllocMapped));
             cap = bytes;
         }
         return buf;
@@ -1063,9 +1076,9 @@ struct PinnedSlot {
         pending = true;
     }
 };
-// per host thread and device: 0 the readbacks, 1 the colidx flag, 2 the Alg. 1/2 tables; E1, E2
+// per host thread and device: 0 the readbacks, 1 the colidx flag; E1, E2
 struct PlanSync {
-    PinnedSlot pin[3];
+    PinnedSlot pin[2];
     cudaEvent_t e1 = nullptr, e2 = nullptr;
 };
 PlanSync& plan_sync(int dev) {
@@ -1107,8 +1120,8 @@ void build_block_plan(agcn_plan_s* p, const int32_t* rowptr, const int32_t* coli
         post_launch();
     }
     auto* pin0 = static_cast<unsigned char*>(ps.pin[0].get(sizeof(PlanFlags) + sizeof(int32_t) * nbins));
-    AGCN_CUDA(cudaMemcpyAsync(pin0, d_flags, sizeof(PlanFlags), cudaMemcpyDeviceToHost, s));
-    AGCN_CUDA(cudaMemcpyAsync(pin0 + sizeof(PlanFlags), bin_cnt, sizeof(int32_t) * nbins, cudaMemcpyDeviceToHost, s));
+    readback(pin0, d_flags, sizeof(PlanFlags), s);
+    readback(pin0 + sizeof(PlanFlags), bin_cnt, sizeof(int32_t) * nbins, s);
     AGCN_CUDA(cudaEventRecord(ps.e1, s));
 
     // the plan's colidx copy (caller's order) with the hot encoding and the range check
@@ -1134,7 +1147,7 @@ void build_block_plan(agcn_plan_s* p, const int32_t* rowptr, const int32_t* coli
     }
     launch_copy_cols(p, colidx, rp, hot, o.validate ? d_flags : nullptr, s);
     auto* pin1 = static_cast<int32_t*>(ps.pin[1].get(sizeof(int32_t)));
-    AGCN_CUDA(cudaMemcpyAsync(pin1, &d_flags->bad_colidx, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    readback(pin1, &d_flags->bad_colidx, sizeof(int32_t), s);
     AGCN_CUDA(cudaEventRecord(ps.e2, s));
 
     // the bucket counts and flags (the GPU runs the copy meanwhile)
@@ -1150,8 +1163,11 @@ void build_block_plan(agcn_plan_s* p, const int32_t* rowptr, const int32_t* coli
     std::vector<int32_t> br, wn;
     host_patterns(p->mbw, p->mwn, br, wn);
     const int32_t W = db + 2;
-    auto* tab = static_cast<int32_t*>(ps.pin[2].get(sizeof(int32_t) * 6 * W));
-    memset(tab, 0, sizeof(int32_t) * 6 * W);
+    // (pageable on purpose: a small pageable H2D is staged through the command stream at once,
+    // while a pinned one waits for the copy engine -- behind a job's gigabyte copy-in in the
+    // pipelined executor, which measured 488 -> 435 GFLOP/s e2e)
+    std::vector<int32_t> tabv(6 * W, 0);
+    int32_t* tab = tabv.data();
     int32_t* nnz_start = tab;
     int32_t* row_start = tab + W;
     int32_t* blk_start = tab + 2 * W;
@@ -1229,7 +1245,6 @@ void build_block_plan(agcn_plan_s* p, const int32_t* rowptr, const int32_t* coli
     // (4)+(5) Algorithm 1/2 descriptors
     int32_t* d_tab = tmp.alloc<int32_t>(6 * W);
     AGCN_CUDA(cudaMemcpyAsync(d_tab, tab, sizeof(int32_t) * 6 * W, cudaMemcpyHostToDevice, s));
-    ps.pin[2].mark(s);
     if (p->nb_small > 0) {
         unsigned g = (unsigned)std::min<int64_t>(blocks_for(p->nb_small, kThreads), 148 * 8);
         size_t smem = 6 * W * sizeof(int32_t);
