@@ -246,7 +246,7 @@ agcn_status_t agcn_plan_destroy(agcn_plan_t plan);
  * a host-only rule in n, nnz and the SM count (sms <= 0: the current device's), measured on
  * B200 (profiles/r01at_auto_partition.md).  With share = nnz / (sms * 24):
  * share < 8 -> (12, 32); share < 960 -> (4, 16), (8, 16) or (8, 32) for share / 2.5 below
- * 128, below 256, at least 256; else (32, 16) if nnz < 64 n (mean degree < 64), else (12, 32).  Never fails for
+ * 128, below 256, at least 256; else (32, 16) if nnz < 64 n (mean degree < 64), else (8, 32).  Never fails for
  * n, nnz >= 0 and non-NULL outputs (else AGCN_ERR_INVALID_ARG).
  */
 agcn_status_t agcn_auto_partition(int64_t n, int64_t nnz, int32_t sms, int32_t* max_block_warps,

@@ -1361,9 +1361,12 @@ static void keep_pool_cached(int dev) {
 //     degree order ascending) does not set the critical path: (4,16) / (8,16) / (8,32)
 //   * otherwise, mean degree < 64:                    (32, 16) -- many short rows: 32-row
 //     descriptors amortise the per-descriptor metadata chain (C5 3.27 vs 3.42 ms at (12, 32))
-//   * otherwise:                                       (12, 32)  (C4: best of the sweep)
+//   * otherwise:                                       (8, 32)   -- deg_bound 256: with the X
+//     loads skipping L1 and the chunks in their own 32-warp/SM kernel, more of a dense-hub
+//     graph's rows go to the faster chunk kernel (C4 3.23 vs 3.31 ms at (12, 32); 192-256 all
+//     within 0.5 %, profiles/r02bk_c4_partition.txt)
 // (Round 1 kept dense-hub graphs, mean degree >= 256, at (24, 32) to keep their rows whole;
-// with the oversized chunks executed in column-position order (round 2) (12, 32) is faster on
+// with the oversized chunks executed in column-position order (round 2) (12, 32) was faster on
 // C4: 3.64 vs 3.78 ms, profiles/r02x_chunk_order.txt, r02ad_partition_sweep.txt.)
 void auto_partition(int64_t n, int64_t nnz, int32_t sms, int32_t* mbw, int32_t* mwn) {
     if (sms <= 0) {
@@ -1385,6 +1388,9 @@ void auto_partition(int64_t n, int64_t nnz, int32_t sms, int32_t* mbw, int32_t* 
     if (n > 0 && nnz < 64 * n) {
         *mbw = 32;
         *mwn = 16;
+    } else {
+        *mbw = 8;
+        *mwn = 32;
     }
 }
 

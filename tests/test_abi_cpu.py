@@ -82,7 +82,7 @@ def test_auto_partition_rule():
     import paper_2308_11825_b200 as A
     from paper_2308_11825_b200 import _lib
     cfg = {"c1": (2708, 10556, (12, 32)), "c2": (19717, 88648, (4, 16)),
-           "c3": (169343, 1166243, (8, 16)), "c4": (232965, 114615891, (12, 32)),
+           "c3": (169343, 1166243, (8, 16)), "c4": (232965, 114615891, (8, 32)),
            "c5": (8388608, 134217728, (32, 16))}
     for name, (n, nnz, want) in cfg.items():
         assert A.auto_partition(n, nnz, 148) == want, name
@@ -92,7 +92,7 @@ def test_auto_partition_rule():
     assert A.auto_partition(10 ** 6, 320 * slots, 148) == (8, 16)        # share / 2.5 = 128
     assert A.auto_partition(10 ** 6, 640 * slots, 148) == (8, 32)        # share / 2.5 = 256
     assert A.auto_partition(10 ** 6, 960 * slots, 148) == (32, 16)       # large, mean degree < 64
-    assert A.auto_partition(10 ** 4, 960 * slots, 148) == (12, 32)       # large, mean degree >= 64
+    assert A.auto_partition(10 ** 4, 960 * slots, 148) == (8, 32)        # large, mean degree >= 64
     assert A.auto_partition(1000, 256 * 1000, 148) == (4, 16)             # dense but small: share rule
     assert A.auto_partition(0, 0, 148) == (12, 32)
     L = _lib.lib()
