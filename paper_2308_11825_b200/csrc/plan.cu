@@ -1050,17 +1050,12 @@ void readback(void* host_mapped, const void* dev, size_t bytes, cudaStream_t s) 
     post_launch();
 }
 
-// mapped pinned host staging (cudaHostAllocMapped: device-writable through the same pointer)
+// mapped pinned host staging (cudaHostAllocMapped: device-writable through the same pointer);
+// only written by read-back kernels the host has waited for before the next plan reuses it
 struct PinnedSlot {
     void* buf = nullptr;
     size_t cap = 0;
-    cudaEvent_t busy = nullptr;
-    bool pending = false;
     void* get(size_t bytes) {
-        if (pending) {
-            cudaEventSynchronize(busy);
-            pending = false;
-        }
         if (bytes > cap) {
             if (buf) cudaFreeHost(buf);
             buf = nullptr;
@@ -1069,11 +1064,6 @@ struct PinnedSlot {
             cap = bytes;
         }
         return buf;
-    }
-    void mark(cudaStream_t s) {
-        if (!busy) AGCN_CUDA(cudaEventCreateWithFlags(&busy, cudaEventDisableTiming));
-        AGCN_CUDA(cudaEventRecord(busy, s));
-        pending = true;
     }
 };
 // per host thread and device: 0 the readbacks, 1 the colidx flag; E1, E2
