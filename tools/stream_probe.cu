@@ -17,20 +17,26 @@ struct f8 {
     float4 a, b;
 };
 
+// PROBE_NA (-DPROBE_NA): the loads skip L1 allocation (.L1::no_allocate), as k_spmm_wide's do
+#ifdef PROBE_NA
+#define NA ".L1::no_allocate"
+#else
+#define NA ""
+#endif
 template <int HINT>  // 0 plain, 1 evict_last, 2 evict_first
 __device__ __forceinline__ void ld8(f8& r, const float* p) {
     if (HINT == 1)
-        asm volatile("ld.global.nc.L2::evict_last.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+        asm volatile("ld.global.nc" NA ".L2::evict_last.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
                      : "=f"(r.a.x), "=f"(r.a.y), "=f"(r.a.z), "=f"(r.a.w), "=f"(r.b.x), "=f"(r.b.y),
                        "=f"(r.b.z), "=f"(r.b.w)
                      : "l"(p));
     else if (HINT == 2)
-        asm volatile("ld.global.nc.L2::evict_first.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+        asm volatile("ld.global.nc" NA ".L2::evict_first.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
                      : "=f"(r.a.x), "=f"(r.a.y), "=f"(r.a.z), "=f"(r.a.w), "=f"(r.b.x), "=f"(r.b.y),
                        "=f"(r.b.z), "=f"(r.b.w)
                      : "l"(p));
     else
-        asm volatile("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+        asm volatile("ld.global.nc" NA ".v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
                      : "=f"(r.a.x), "=f"(r.a.y), "=f"(r.a.z), "=f"(r.a.w), "=f"(r.b.x), "=f"(r.b.y),
                        "=f"(r.b.z), "=f"(r.b.w)
                      : "l"(p));

@@ -29,9 +29,10 @@ import paper_2308_11825_b200 as agcn  # noqa: E402
 
 def build_probe():
     src = os.path.join(ROOT, "tools", "stream_probe.cu")
-    so = "/tmp/stream_probe.so"
+    na = os.environ.get("PROBE_NA") == "1"   # loads with .L1::no_allocate (as the kernel's)
+    so = "/tmp/stream_probe%s.so" % ("_na" if na else "")
     subprocess.check_call(["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-shared",
-                           "-Xcompiler", "-fPIC", "-lineinfo", src, "-o", so])
+                           "-Xcompiler", "-fPIC", "-lineinfo"] + (["-DPROBE_NA"] if na else []) + [src, "-o", so])
     lib = ctypes.CDLL(so)
     lib.probe_stream.argtypes = [ctypes.c_int] * 4 + [ctypes.c_void_p] * 4 + [ctypes.c_int64, ctypes.c_int,
                                                                             ctypes.c_void_p, ctypes.c_int64,
