@@ -115,6 +115,7 @@ struct WideArgs {
     const int32_t* ov_cs; // [n_ov + 1] first chunk of oversized row k
     int32_t* ov_cnt;      // [n_ov] chunks of row k finished (zero between launches)
     int64_t ov_start;     // sorted position of the first oversized row
+    int32_t zero_in_chunks;  // k_spmm_chunks writes the degree-0 rows (k_spmm_wide then skips them)
 };
 
 // one X-row slice of 8 floats for column code c (XM: see the file comment)
@@ -390,6 +391,23 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_wide(const __grid_const
     zero_rows();
 }
 
+// 32 degree-0 rows (sorted positions [32 zb, 32 zb + 32)) written as zero rows of Y, one per
+// combined warp and step (reading Q16)
+template <int L>
+__device__ __forceinline__ void zero_batch(const WideArgs& a, int64_t zb, int lane, int s, int li) {
+    constexpr int G = 32 / L, F = 8 * L;
+    const int64_t r0 = zb * 32;
+    if (r0 >= a.n_zero) return;
+    const int32_t pr = r0 + lane < a.n_zero ? __ldg(a.perm + r0 + lane) : -1;
+    f8 z;
+    z.a = z.b = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll 4
+    for (int i = 0; i < 32; i += G) {
+        const int32_t o = __shfl_sync(0xffffffffu, pr, i + s);
+        if (o >= 0) st8(a.Y + (int64_t)o * F + li * 8, z);
+    }
+}
+
 // The oversized-row chunks {deg, loc, row, nnz <= deg_bound} on their own: all G
 // combined warps of a warp split one chunk into contiguous parts (the main kernel's R = 1 case,
 // same split and the same xor-tree merge, so bitwise the same partial rows) with nothing else
@@ -462,7 +480,12 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_chunks(const __grid_con
             acc.b.w = shfl_xor_add(acc.b.w, o);
         }
         if (s == 0) st8(a.ovp + (int64_t)i * F + li * 8, acc);
+        // the degree-0 rows, one batch of 32 after every chunk: their DRAM writes overlap this
+        // kernel's L2-bound gathers instead of forming a write-bound tail of k_spmm_wide
+        if (a.zero_in_chunks) zero_batch<L>(a, (int64_t)i0, lane, s, li);
     }
+    if (a.zero_in_chunks)
+        for (int64_t zb = (int64_t)nch + gw; zb * 32 < a.n_zero; zb += W) zero_batch<L>(a, zb, lane, s, li);
 }
 
 // launch `kern` on a persistent grid (SMs x occupancy, capped by the work) with the hot
@@ -552,7 +575,10 @@ void launch(const WideArgs& a, int xm, bool lean, size_t win, int chunks, cudaSt
         }
     }
     WideArgs b = a;
-    if (L && chunks) b.n_desc = a.first_ov;
+    if (L && chunks) {
+        b.n_desc = a.first_ov;
+        if (a.zero_in_chunks) b.n_zero = 0;   // written by k_spmm_chunks
+    }
     switch (xm) {
         case 0: lean ? launch_e<L, U2, 4, 0>(b, 0, s) : launch_e<L, U4, 3, 0>(b, 0, s); break;
         case 1: lean ? launch_e<L, U2, 4, 1>(b, 0, s) : launch_e<L, U4, 3, 1>(b, 0, s); break;
@@ -594,6 +620,7 @@ void launch_wide(agcn_plan_s* p, const float* vals, const float* X, const float*
     // -2.9 %, C4 F64 -4.4 %, profiles/r02be_chunk_kernel.txt; F < 32 not measured)
     const int chunks = (!a.fuse_ov && p->ov_chunks > 0 && chunk_shape >= 0 && (chunk_shape || F >= 32))
                            ? (chunk_shape ? chunk_shape : 4) : 0;
+    a.zero_in_chunks = chunks && (F & (F - 1)) == 0 && !epi.active();
     switch (F) {
         case 8: launch<1>(a, xm, lean, win, chunks, s); break;
         case 16: launch<2>(a, xm, lean, win, chunks, s); break;
