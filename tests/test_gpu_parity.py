@@ -334,6 +334,30 @@ def test_plan_does_not_read_caller_arrays_after_return(partition, small):
         check_spmm(p, w.rowptr, w.colidx, w.vals, w.X())
 
 
+@pytest.mark.parametrize("F", [32, 64, 128, 256, 40])
+def test_chunk_kernel_writes_zero_rows(F):
+    """Plans with more than 16384 oversized chunks run them in k_spmm_chunks, which also writes
+    the degree-0 rows (one batch of 32 after every chunk, the rest after its last chunk):
+    bitwise the same Y as the single-kernel path (chunk_shape -1), every row checked against
+    the oracle, zero rows exactly 0."""
+    rng = np.random.default_rng(F)
+    n = 70000
+    degs = np.zeros(n, np.int64)
+    live = rng.permutation(n)[:30000]
+    degs[live[:12000]] = rng.integers(5, 9, 12000)      # deg_bound 4: 2 chunks each -> > 16384 chunks
+    degs[live[12000:]] = rng.integers(1, 5, 18000)
+    rowptr, colidx = _rows_csr(degs, n, F)
+    vals = rng.uniform(-1, 1, colidx.size).astype(np.float32)
+    X = rng.uniform(-1, 1, (n, F)).astype(np.float32)
+    p = make_plan(rowptr, colidx, max_block_warps=1, max_warp_nzs=4, small_plan=False)
+    assert p.stats()["n_oversized_blocks"] > 16384
+    Y = p.spmm(cu(vals), cu(X)).cpu().numpy()
+    Y1 = p.spmm(cu(vals), cu(X), chunk_shape=-1).cpu().numpy()
+    assert np.array_equal(Y, Y1)
+    assert not Y[degs == 0].any()
+    check_spmm(p, rowptr, colidx, vals, X, Y)
+
+
 def test_hot_rows_auto_rule():
     """hot_rows = -1: on for square graphs with n >= 2^19, off otherwise and for padded layouts."""
     rowptr = np.zeros(2 ** 19 + 1, dtype=np.int32)
